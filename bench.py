@@ -1,0 +1,437 @@
+"""Benchmark of the RT O-DU codebook hot path (driver contract: ONE JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[2], "batch of 1024 independent slots on 1
+B200, throughput mode"; per rank at N>1, configs[3]-style cells sharded by
+rank with one NCCL all-gather of the codebooks per step):
+  * cell N=780 subcarriers, E=10 eMBB users, L=195 -> cap 4 packets per
+    mini-slot, M=7 mini-slots (numerology 3); actor 2x256 (random init,
+    make_agent on substream(0, "agent-init")), fp32 SIMT, stochastic head;
+  * synthetic schedules (engine._synthetic_schedule's generator: uniform
+    random RB owners, 65 RBs of 12 SCs) and per-branch noise;
+  * one step = K2 actor + K3 codebook for 1024 slots + K1 Mode-R arrival
+    tree (97,655 node states per slot, 3.2 GB written).
+value = codebooks/s over all ranks (each codebook carries its full arrival
+tree).  The single-slot latency against the 125 us numerology-3 budget (the
+first half of BASELINE's metric) is measured in the same run through the
+drop-in build_codebook call and reported under "latency_us".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("codebook-gen latency per slot (µs vs 125 µs budget); "
+          "codebooks/sec at 1/2/4/8 GPUs")
+UNIT = "codebooks/s"
+GEOM = dict(total_scs=780, num_embb=10, urllc_sc_len=195, minislots=7, rb_size=12)
+HIDDEN = (256, 256)
+SLOTS = 1024
+BUDGET_US = 125.0
+HBM_FALLBACK_GBS = 6650.0
+L2_FLUSH_BYTES = 256 << 20
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def synthetic_inputs(cell, slots, seed=0):
+    """Schedules as engine._synthetic_schedule draws them (engine.py:296-302)
+    and the per-branch noise of ``slots`` consecutive stochastic calls."""
+    from paper_2506_00167_b200 import draw_branch_noise, make_streams, substream
+    rng = substream(seed, "scenario")
+    allocs = np.empty((slots, cell.num_embb), dtype=np.int32)
+    for s in range(slots):
+        owners = rng.integers(0, cell.num_embb, size=cell.num_rbs)
+        allocs[s] = np.bincount(owners, minlength=cell.num_embb) * cell.rb_size
+        rng.integers(0, 6, size=cell.num_embb)  # MCS draw (keeps the stream aligned)
+    eps = draw_branch_noise(make_streams(seed, cell.num_branches), cell.num_branches,
+                            cell.num_embb, slots)
+    return allocs, eps
+
+
+def make_cell_agent():
+    from paper_2506_00167_b200 import AgentHyper, CellConfig, make_agent, substream
+    cell = CellConfig(**GEOM)
+    agent = make_agent(cell, AgentHyper(actor_hidden=HIDDEN), substream(0, "agent-init"))
+    return cell, agent
+
+
+# ------------------------------------------------------------- CPU baseline
+def _cpu_worker_init(weights, biases):
+    global _W, _B
+    _W, _B = weights, biases
+
+
+def _cpu_worker(args):
+    from oracle import arrival_tree, slot
+    allocs, eps, n, l, m = args
+    t0 = time.perf_counter()
+    for s in range(allocs.shape[0]):
+        book = slot.slot_codebook(_W, _B, allocs[s], n, l, eps[s])
+        arrival_tree.node_states(book, m)
+    return time.perf_counter() - t0, allocs.shape[0]
+
+
+def cpu_baseline(agent, cell, allocs, eps, cores=None):
+    """The oracle port (float64 numpy restatement of the reference path,
+    plus the Mode-R tree restatement) on all host cores, one process per
+    core with single-threaded BLAS.  Returns (codebooks/s, cores, wall s)."""
+    import multiprocessing as mp
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["OMP_NUM_THREADS"] = "1"
+    cores = cores or os.cpu_count() or 1
+    cores = max(1, min(cores, allocs.shape[0]))
+    chunks = np.array_split(np.arange(allocs.shape[0]), cores)
+    jobs = [(allocs[c], eps[c], cell.total_scs, cell.urllc_sc_len, cell.minislots)
+            for c in chunks if len(c)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(len(jobs), initializer=_cpu_worker_init,
+                  initargs=(agent.actor.weights, agent.actor.biases)) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(_cpu_worker, jobs)
+        wall = time.perf_counter() - t0
+    done = sum(r[1] for r in res)
+    return done / wall, len(jobs), wall
+
+
+def single_core_latency_us(agent, cell, allocs, eps, samples=64):
+    from oracle import slot
+    times = []
+    for s in range(samples):
+        t0 = time.perf_counter_ns()
+        slot.slot_codebook(agent.actor.weights, agent.actor.biases, allocs[s], cell.total_scs,
+                           cell.urllc_sc_len, eps[s])
+        times.append((time.perf_counter_ns() - t0) / 1e3)
+    return float(np.median(times))
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
+
+    def __enter__(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7 and parts[0].replace(".", "").isdigit():
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        busy = [r for r in rows if r[2].isdigit() and int(r[2]) > 0] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in busy for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": float(statistics.median(float(r[0]) for r in busy)),
+                "sm_max_mhz": float(max(float(r[1]) for r in rows)),
+                "reasons": reasons, "samples": len(busy)}
+
+
+def measured_peak_hbm():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json (of measured)"
+    except (OSError, KeyError, ValueError):
+        return HBM_FALLBACK_GBS, "B200_PROFILING.md fallback (of fallback)"
+
+
+def committed_traffic():
+    """dram read+write bytes per K1 launch from the committed ncu --set full
+    capture (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_tree_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return None
+
+
+# --------------------------------------------------------------- reference
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    cell, agent = make_cell_agent()
+    allocs, eps = synthetic_inputs(cell, SLOTS)
+    per_step, cores = [], 0
+    for i in range(args.warmup + args.steps):
+        rate, cores, wall = cpu_baseline(agent, cell, allocs, eps)
+        if i >= args.warmup:
+            per_step.append(wall)
+    wall = float(np.mean(per_step))
+    value = SLOTS / wall
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": wall * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(world, "none"),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{SLOTS} slots per step (cfg2 geometry codebook + Mode-R "
+                                   "tree restatement), all host cores"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_block(world, l2):
+    return {"workload": "cfg3: 1024 independent slots per rank (N=780, E=10, L=195, cap 4, "
+                        "M=7), actor 2x256, stochastic, Mode-R arrival tree"
+                        + (", NCCL codebook all-gather" if world > 1 else ""),
+            "slots_per_rank": SLOTS, "global_batch": SLOTS * world, "cells": SLOTS * world,
+            "actor": "2x256", "precision": "fp32 actor / fp64 projection",
+            "parallelism": f"cell-sharded x{world}", "l2": l2}
+
+
+# -------------------------------------------------------------------- ours
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2506_00167_b200 import CodebookEngine, DevicePolicy, _native
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cell, agent = make_cell_agent()
+    allocs, eps = synthetic_inputs(cell, SLOTS, seed=rank)
+    pol = DevicePolicy(agent.actor, args.precision)
+    eng = CodebookEngine(pol, cell, max_slots=SLOTS, with_tree=not args.no_tree, device=dev)
+    alloc_d = torch.from_numpy(allocs).to(dev)
+    eps_d = torch.from_numpy(eps).to(dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+    lib = _native.lib()
+    st = stream.cuda_stream
+
+    def allgather(local):
+        out = torch.empty((world,) + tuple(local.shape), dtype=local.dtype, device=dev)
+        dist.all_gather_into_tensor(out, local)   # NCCL over NVLink: the one exchange
+        return out
+
+    def step(events=None):
+        """K2 -> K3 (-> K1) for all slots (+ all-gather); events = (start,
+        tree_start, tree_end, end) recorded on the launching stream."""
+        if events:
+            events[0].record(stream)
+        _native.check(lib.cyr_actor_forward_device(pol.handle, alloc_d.data_ptr(), SLOTS,
+                                                   cell.total_scs, cell.num_branches,
+                                                   eng.raw.data_ptr(), st))
+        _native.check(lib.cyr_codebook_from_raw_device(
+            pol.handle, eng.raw.data_ptr(), alloc_d.data_ptr(), eps_d.data_ptr(), SLOTS,
+            cell.total_scs, cell.urllc_sc_len, eng.codebooks.data_ptr(), None, None, None, None,
+            eng.status.data_ptr(), st))
+        if events:
+            events[1].record(stream)
+        if not args.no_tree:
+            _native.check(lib.cyr_tree_expand_device(eng.codebooks.data_ptr(), SLOTS, eng.users,
+                                                     eng.cap, cell.minislots,
+                                                     eng.node_state.data_ptr(), st))
+        if events:
+            events[2].record(stream)
+        if world > 1:
+            allgather(eng.codebooks)
+        if events:
+            events[3].record(stream)
+
+    launches_per_step = 2 + (0 if args.no_tree else 1)
+    for _ in range(args.warmup):
+        step()
+    eng.check()
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clocks:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.fill_(i)                      # L2 flush between timed steps (untimed)
+            step(evs[i])
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        eng.check()
+        step_ms = [e[0].elapsed_time(e[3]) for e in evs]
+        tree_ms = [e[1].elapsed_time(e[2]) for e in evs]
+
+        # ---- e2e through the public API with host buffers (pinned H2D/D2H)
+        alloc_h = torch.from_numpy(allocs).pin_memory()
+        eps_h = torch.from_numpy(eps).pin_memory()
+        out_h = torch.empty((SLOTS, cell.num_branches + 1, cell.num_embb), dtype=torch.int32,
+                            pin_memory=True)
+        for _ in range(2):
+            eng.run_host(alloc_h, eps_h, out_h)
+        if world > 1:
+            dist.barrier()
+        e2e = []
+        for i in range(args.steps):
+            flush.fill_(i)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            eng.run_host(alloc_h, eps_h, out_h)
+            if world > 1:
+                allgather(eng.codebooks)
+                torch.cuda.synchronize()
+            e2e.append(time.perf_counter() - t0)
+
+        # ---- single-slot latency through the drop-in build_codebook
+        lat = latency_run(agent, cell, allocs, args.latency_slots)
+
+    mean_ms = float(np.mean(step_ms))
+    mean_e2e = float(np.mean(e2e))
+    if world > 1:
+        t = torch.tensor([mean_ms, mean_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        mean_ms, mean_e2e = float(t[0]), float(t[1])
+    if rank != 0:
+        return 0
+
+    total = SLOTS * world
+    peak, peak_src = measured_peak_hbm()
+    roofline = None
+    if not args.no_tree:
+        nodes = eng.nodes
+        tree_bytes = SLOTS * (nodes * eng.stride * 2 + (cell.num_branches + 1) * cell.num_embb * 4)
+        tree_ms = float(np.mean(tree_ms))
+        achieved = tree_bytes / (tree_ms * 1e-3) / 1e9
+        traffic = committed_traffic()
+        roofline = {"kernel": "K1 tree_kernel (Mode-R node states)", "bound": "hbm",
+                    "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "peak_source": peak_src, "algorithmic_bytes_per_launch": tree_bytes,
+                    "kernel_ms": tree_ms, "share_of_step": tree_ms / mean_ms,
+                    "traffic": None if traffic is None else traffic.get("bytes_per_launch"),
+                    "traffic_source": None if traffic is None else traffic.get("source")}
+
+    cores_rate, cores, cpu_wall = cpu_baseline(agent, cell, allocs, eps) if world == 1 else \
+        (None, None, None)
+    core1 = single_core_latency_us(agent, cell, allocs, eps) if world == 1 else None
+    line = {
+        "metric": METRIC, "value": total / (mean_ms * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "fp32", "data": "synthetic",
+        "config": config_block(world, "flushed (256 MiB write) between timed steps"),
+        "e2e": {"value": total / mean_e2e, "unit": UNIT,
+                "h2d_bytes_per_step": int(allocs.nbytes + eps.nbytes),
+                "d2h_bytes_per_step": int(SLOTS * (cell.num_branches + 1) * cell.num_embb * 4),
+                "note": "CodebookEngine.run_host: pinned H2D of schedules+noise, K2/K3/K1, "
+                        "D2H of the codebooks (node states stay in HBM)"},
+        "latency_us": lat,
+        "roofline": roofline,
+        "cpu_baseline": None if cores_rate is None else {
+            "value": cores_rate, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{SLOTS} slots (one step's workload) over {cores} processes, "
+                      f"{cpu_wall:.2f} s wall; oracle float64 restatement + Mode-R tree",
+            "single_core_slot_us": core1},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def latency_run(agent, cell, allocs, n):
+    """Per-slot latency of the drop-in build_codebook (host-observed and
+    device), stochastic and deterministic, cfg2 geometry."""
+    from paper_2506_00167_b200 import ScheduleVector, build_codebook, make_streams, policy_for
+    from paper_2506_00167_b200 import set_weight_sync
+    out = {"budget_us": BUDGET_US}
+    for sync in ("manual", "check"):
+        set_weight_sync(sync)
+        pol = policy_for(agent)
+        streams = make_streams(7, cell.num_branches)
+        for mode in ("stochastic", "deterministic"):
+            if sync == "check" and mode == "deterministic":
+                continue
+            det = mode == "deterministic"
+            for s in range(20):
+                build_codebook(agent, ScheduleVector(allocs[s], [0] * cell.num_embb), streams, det)
+            host, device = [], []
+            for s in range(n):
+                cb = build_codebook(agent, ScheduleVector(allocs[s % len(allocs)],
+                                                          [0] * cell.num_embb), streams, det)
+                host.append(cb.gen_ns / 1e3)
+                device.append(cb.device_ns / 1e3)
+            key = mode if sync == "manual" else f"{mode}_weight_check"
+            out[key] = {"host_p50": float(np.percentile(host, 50)),
+                        "host_p99": float(np.percentile(host, 99)),
+                        "host_max": float(np.max(host)),
+                        "device_p50": float(np.percentile(device, 50)),
+                        "device_p99": float(np.percentile(device, 99)),
+                        "slots": n}
+    set_weight_sync("check")
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--precision", choices=("fp32", "fp64"), default="fp32")
+    ap.add_argument("--no-tree", action="store_true")
+    ap.add_argument("--latency-slots", type=int, default=2000)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

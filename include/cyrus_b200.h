@@ -1,0 +1,157 @@
+/*
+ * cyrus_b200.h — C ABI of the B200-native RT O-DU puncturing-codebook path.
+ *
+ * Drop-in boundary for the reference's hot path:
+ *   punctsim.engine.build_codebook(agent, schedule, streams, deterministic)
+ *     /root/reference/pkg/src/punctsim/engine.py:97-116
+ * and its callees
+ *   sac.policy_branch_actions          sac.py:334-355
+ *   neural.forward / split_head /
+ *     sample_squashed / action_to_scs  neural.py:66-84, 144-183
+ *   enforcer.kl_project_batch /
+ *     apportion_batch / enforce_batch  enforcer.py:49-165, 201-207
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no torch types cross this boundary;
+ *   - "_device" entry points take DEVICE pointers, are asynchronous on the
+ *     given cudaStream_t (passed as void*), and never synchronise;
+ *   - "_host" entry points take HOST pointers and return when results are
+ *     in host memory (the reference's synchronous call semantics);
+ *   - every entry point returns a status code (below); the Python layer maps
+ *     CYR_INFEASIBLE -> InfeasibleDemandError(ValueError) (enforcer.py:28-29)
+ *     and CYR_BAD_ARG -> ValueError (enforcer.py:60-63, neural.py:73-74).
+ *
+ * Layouts (row-major, C order)
+ *   alloc     [S][E]            int32   per-slot eMBB allocation n_e
+ *   eps       [S][cap][E]       float64 branch-j noise (row j-1), or NULL =
+ *                                       deterministic actor mean (sac.py:349)
+ *   codebook  [S][cap+1][E]     int32   column j sums to j*L, column 0 zero
+ *   node_state[S][nodes][Epad]  int16   Mode-R arrival-tree cumulative
+ *                                       punctures, BFS order
+ *   weights blob (policy create/update): per layer W (out,in) row-major
+ *     float64 followed by b (out) — the PSIMMLP1 payload order
+ *     (neural.py:186-196).
+ */
+#ifndef CYRUS_B200_H
+#define CYRUS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum cyr_status {
+  CYR_OK = 0,
+  CYR_INFEASIBLE = 1,  /* demand > total capacity  (InfeasibleDemandError) */
+  CYR_BAD_ARG = 2,     /* shape / range / negative input (ValueError)       */
+  CYR_CUDA_ERROR = 3,  /* CUDA runtime failure                             */
+  CYR_UNSUPPORTED = 4  /* geometry outside the kernels' compiled envelope   */
+};
+
+enum cyr_precision {
+  CYR_FP32 = 0, /* fp32 SIMT actor GEMM (default), fp64 head + projection  */
+  CYR_FP64 = 1  /* fp64 actor GEMM: logits within 1e-15 of the reference   */
+};
+
+typedef struct cyr_policy cyr_policy;
+
+/* ---- library ----------------------------------------------------------- */
+int cyr_version(void);
+const char* cyr_status_string(int status);
+/* SM count / compute capability of the current device. */
+int cyr_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
+/* Last CUDA error string seen by the library (diagnostics). */
+const char* cyr_last_error(void);
+
+/* ---- policy: the device-resident actor (sac.SacAgent.actor) ------------- */
+/* Replaces the actor object of sac.py:96-127 as seen by build_codebook.
+ * sizes = [E+1, *hidden, 2E]; E <= 32, every width <= 1024. */
+int cyr_policy_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
+                      const double* weights_blob, int32_t precision);
+/* Re-publish after an in-place actor update (Adam, neural.py:122-141). */
+int cyr_policy_update(cyr_policy* policy, const double* weights_blob);
+/* Load a PSIMMLP1 checkpoint file (neural.py:211-225) straight to device. */
+int cyr_policy_load(cyr_policy** out, const char* path, int32_t precision);
+int cyr_policy_destroy(cyr_policy* policy);
+int cyr_policy_info(const cyr_policy* policy, int32_t* num_users, int32_t* n_sizes,
+                    int32_t* precision);
+
+/* ---- actor forward (K2) -------------------------------------------------- */
+/* raw[S*cap][2E] (float for CYR_FP32, double for CYR_FP64): actor logits of
+ * branch columns j=1..cap, inputs [alloc/N, j/cap] (sac.py:344-347). */
+int cyr_actor_forward_device(const cyr_policy* policy, const int32_t* alloc,
+                             int32_t S, int32_t N, int32_t cap, void* raw,
+                             void* stream);
+
+/* ---- fused action -> codebook (K3) --------------------------------------- */
+/* From logits: head (neural.py:144-165), SC mapping (neural.py:181-183),
+ * KL projection + Huntington-Hill per slot (enforcer.py:49-165), one slot =
+ * one coupled enforcement call (engine.py:108-110).
+ * Optional diagnostics (NULL to skip): m_hat[S][cap][E], nu[S][cap],
+ * margin[S][cap] (relative HH boundary gap), iters[S] (bisection steps).
+ * status: device int32, set to a nonzero cyr_status by any failing slot.  */
+int cyr_codebook_from_raw_device(const cyr_policy* policy, const void* raw,
+                                 const int32_t* alloc, const double* eps,
+                                 int32_t S, int32_t N, int32_t L,
+                                 int32_t* codebook, double* m_hat, double* nu,
+                                 double* margin, int32_t* iters,
+                                 int32_t* status, void* stream);
+
+/* K2 + K3 in one call; raw_workspace holds S*cap*2E logits (element size
+ * by precision, see cyr_raw_bytes). */
+size_t cyr_raw_bytes(const cyr_policy* policy, int32_t S, int32_t cap);
+int cyr_codebook_device(const cyr_policy* policy, const int32_t* alloc,
+                        const double* eps, int32_t S, int32_t N, int32_t L,
+                        int32_t* codebook, void* raw_workspace,
+                        int32_t* status, void* stream);
+
+/* Synchronous host-buffer path (the reference's call semantics): copies
+ * alloc/eps in, runs K2+K3 on the policy's own stream (replayed as one CUDA
+ * graph per shape), copies the codebook out, returns when it is on the
+ * host.  device_ns (optional) receives the CUDA-event time of the device
+ * section.  Validation happens on the host before any launch. */
+int cyr_codebook_host(cyr_policy* policy, const int32_t* alloc, const double* eps,
+                      int32_t S, int32_t N, int32_t L, int32_t* codebook,
+                      int64_t* device_ns);
+
+/* ---- standalone enforcer (K3 core) ---------------------------------------- */
+/* enforce_batch(b, caps, demands) with ALL R rows forming one coupled call
+ * (enforcer.py:201-207).  b, caps [R][E] float64; demand [R] int64.
+ * Outputs (NULL to skip except grants): m_hat [R][E], nu [R],
+ * degenerate [R] (uint8), grants [R][E] int64, margin [R].
+ * R <= 256, E <= 32. */
+int cyr_enforce_batch_device(const double* b, const double* caps, const int64_t* demand,
+                             int32_t R, int32_t E, double* m_hat, double* nu,
+                             uint8_t* degenerate, int64_t* grants, double* margin,
+                             int32_t* status, void* stream);
+
+/* kl_project_batch(b, caps, demand) alone (enforcer.py:49-115): float64
+ * demand, one coupled call, R <= 256.  Outputs m_hat [R][E], nu [R] and
+ * degenerate [R] (the last two may be NULL). */
+int cyr_kl_project_batch_device(const double* b, const double* caps, const double* demand,
+                                int32_t R, int32_t E, double* m_hat, double* nu,
+                                uint8_t* degenerate, int32_t* status, void* stream);
+
+/* apportion_batch(m_hat, caps, demand) alone (enforcer.py:118-165); rows
+ * are independent; any R.  E <= 32. */
+int cyr_apportion_batch_device(const double* m_hat, const double* caps, const int64_t* demand,
+                               int32_t R, int32_t E, int64_t* grants, double* margin,
+                               int32_t* status, void* stream);
+
+/* ---- arrival tree, Mode R (K1) ------------------------------------------- */
+/* Node count excluding the root: sum_{t=1..M} (cap+1)^t. */
+int64_t cyr_tree_num_nodes(int32_t cap, int32_t M);
+/* int16 lanes per node record (E rounded up to a multiple of 8). */
+int32_t cyr_tree_state_stride(int32_t E);
+/* node_state[s][off(t) + q][:E] = sum of codebook[s][digit_i(q)] over the
+ * t digits of q in base cap+1 (engine.py:230 lookups, engine.py:240-241
+ * per-user sums); padding lanes are written as zero. */
+int cyr_tree_expand_device(const int32_t* codebook, int32_t S, int32_t E, int32_t cap,
+                           int32_t M, int16_t* node_state, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CYRUS_B200_H */

@@ -1,0 +1,120 @@
+"""ctypes binding of the in-tree C-ABI library (include/cyrus_b200.h).
+
+There is no CPU fallback: if ``libcyrus_b200.so`` is missing or fails to
+load, every product entry point raises ``NativeLibraryError``.  The
+signatures below are the complete ABI; tests/test_abi.py checks that the
+library exports every symbol the header declares.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcyrus_b200.so")
+
+CYR_OK, CYR_INFEASIBLE, CYR_BAD_ARG, CYR_CUDA_ERROR, CYR_UNSUPPORTED = range(5)
+CYR_FP32, CYR_FP64 = 0, 1
+PRECISIONS = {"fp32": CYR_FP32, "fp64": CYR_FP64}
+
+_c_int, _c_i32, _c_i64 = ctypes.c_int, ctypes.c_int32, ctypes.c_int64
+_vp, _cp = ctypes.c_void_p, ctypes.c_char_p
+_pi32 = ctypes.POINTER(ctypes.c_int32)
+_pi64 = ctypes.POINTER(ctypes.c_int64)
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "cyr_version": (_c_int, []),
+    "cyr_status_string": (_cp, [_c_int]),
+    "cyr_device_info": (_c_int, [_pi32, _pi32, _pi32]),
+    "cyr_last_error": (_cp, []),
+    "cyr_policy_create": (_c_int, [ctypes.POINTER(_vp), _vp, _c_i32, _vp, _c_i32]),
+    "cyr_policy_update": (_c_int, [_vp, _vp]),
+    "cyr_policy_load": (_c_int, [ctypes.POINTER(_vp), _cp, _c_i32]),
+    "cyr_policy_destroy": (_c_int, [_vp]),
+    "cyr_policy_info": (_c_int, [_vp, _pi32, _pi32, _pi32]),
+    "cyr_actor_forward_device": (_c_int, [_vp, _vp, _c_i32, _c_i32, _c_i32, _vp, _vp]),
+    "cyr_codebook_from_raw_device": (
+        _c_int, [_vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "cyr_raw_bytes": (ctypes.c_size_t, [_vp, _c_i32, _c_i32]),
+    "cyr_codebook_device": (_c_int, [_vp, _vp, _vp, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp, _vp]),
+    "cyr_codebook_host": (_c_int, [_vp, _vp, _vp, _c_i32, _c_i32, _c_i32, _vp, _pi64]),
+    "cyr_enforce_batch_device": (
+        _c_int, [_vp, _vp, _vp, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "cyr_kl_project_batch_device": (_c_int, [_vp, _vp, _vp, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp]),
+    "cyr_apportion_batch_device": (_c_int, [_vp, _vp, _vp, _c_i32, _c_i32, _vp, _vp, _vp, _vp]),
+    "cyr_tree_num_nodes": (_c_i64, [_c_i32, _c_i32]),
+    "cyr_tree_state_stride": (_c_i32, [_c_i32]),
+    "cyr_tree_expand_device": (_c_int, [_vp, _c_i32, _c_i32, _c_i32, _c_i32, _vp, _vp]),
+}
+
+
+class NativeLibraryError(RuntimeError):
+    """The CUDA library is missing or unusable; there is no fallback."""
+
+
+class InfeasibleDemandError(ValueError):
+    """Demand exceeds the total puncturable allocation (enforcer.py:28-29)."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise NativeLibraryError(
+                f"{LIB_PATH} is missing; build it with `python -m paper_2506_00167_b200._build` "
+                "(there is no CPU fallback for the codebook path)")
+        try:
+            handle = ctypes.CDLL(LIB_PATH)
+        except OSError as exc:
+            raise NativeLibraryError(f"cannot load {LIB_PATH}: {exc}") from exc
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def check(status: int, what: str = "") -> None:
+    """Map a cyr_status to the reference's exception types."""
+    if status == CYR_OK:
+        return
+    l = lib()
+    msg = l.cyr_status_string(status).decode()
+    if what:
+        msg = f"{what}: {msg}"
+    if status == CYR_INFEASIBLE:
+        raise InfeasibleDemandError(msg)
+    if status == CYR_CUDA_ERROR:
+        detail = l.cyr_last_error().decode()
+        raise CudaError(f"{msg} ({detail})" if detail else msg)
+    raise ValueError(msg)
+
+
+def ptr(x) -> int | None:
+    """Raw address of a numpy array or torch tensor (None passes NULL)."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    return x.ctypes.data
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream

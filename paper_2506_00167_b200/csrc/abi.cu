@@ -1,0 +1,476 @@
+// abi.cu — the extern "C" boundary declared in include/cyrus_b200.h.
+//
+// Owns the device policy (the reference's SacAgent.actor, sac.py:96-127),
+// argument validation with the reference's error semantics, and the
+// synchronous host-buffer path that a drop-in build_codebook call uses:
+// H2D(alloc, eps) -> K2 actor -> K3 codebook -> D2H(codebook, status),
+// captured once per shape into a CUDA graph and replayed on the policy's own
+// stream (one launch per slot instead of five API calls).
+#include "cyrus_internal.cuh"
+#include "cyrus_b200.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return CYR_CUDA_ERROR;
+}
+
+#define CYR_CUDA(call)                                 \
+  do {                                                 \
+    cudaError_t e_ = (call);                           \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+int sm_count_of_current_device() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
+
+}  // namespace
+
+struct cyr_policy {
+  int precision = CYR_FP32;
+  std::vector<int> sizes;
+  int E = 0;
+  size_t elem = 4;
+  cyr::ActorDesc desc{};
+  void* blob_d = nullptr;
+  size_t blob_elems = 0;
+  int sm_count = 148;
+  // host path
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int buf_S = 0, buf_cap = 0;
+  int32_t* alloc_d = nullptr;
+  double* eps_d = nullptr;
+  void* raw_d = nullptr;
+  int32_t* cb_d = nullptr;
+  int32_t* status_d = nullptr;
+  unsigned char* pin = nullptr;
+  int32_t* pin_alloc = nullptr;
+  double* pin_eps = nullptr;
+  int32_t* pin_cb = nullptr;
+  int32_t* pin_status = nullptr;
+  std::map<std::tuple<int, int, int, int>, cudaGraphExec_t> graphs;
+};
+
+namespace {
+
+// W (out,in) row-major float64 + b -> Wt [in][out_pad] + b in the policy dtype
+template <typename T>
+void pack_blob(const cyr_policy& p, const double* src, std::vector<T>& dst) {
+  dst.assign(p.blob_elems, T(0));
+  size_t off = 0;
+  for (int l = 0; l < p.desc.n_layers; ++l) {
+    const cyr::LayerDesc& L = p.desc.layer[l];
+    for (int o = 0; o < L.out; ++o)
+      for (int i = 0; i < L.in; ++i)
+        dst[L.w_off + (size_t)i * L.out_pad + o] = (T)src[off + (size_t)o * L.in + i];
+    off += (size_t)L.out * L.in;
+    for (int o = 0; o < L.out; ++o) dst[L.b_off + o] = (T)src[off + o];
+    off += L.out;
+  }
+}
+
+int upload(cyr_policy* p, const double* blob) {
+  if (p->precision == CYR_FP64) {
+    std::vector<double> h;
+    pack_blob(*p, blob, h);
+    CYR_CUDA(cudaMemcpy(p->blob_d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+  } else {
+    std::vector<float> h;
+    pack_blob(*p, blob, h);
+    CYR_CUDA(cudaMemcpy(p->blob_d, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+  }
+  return CYR_OK;
+}
+
+void release_host_path(cyr_policy* p) {
+  for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
+  p->graphs.clear();
+  cudaFree(p->alloc_d);
+  cudaFree(p->eps_d);
+  cudaFree(p->raw_d);
+  cudaFree(p->cb_d);
+  cudaFree(p->status_d);
+  cudaFreeHost(p->pin);
+  p->alloc_d = nullptr;
+  p->eps_d = nullptr;
+  p->raw_d = nullptr;
+  p->cb_d = nullptr;
+  p->status_d = nullptr;
+  p->pin = nullptr;
+  p->buf_S = p->buf_cap = 0;
+}
+
+int ensure_host_path(cyr_policy* p, int S, int cap) {
+  if (!p->stream) {
+    CYR_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    CYR_CUDA(cudaEventCreate(&p->ev0));
+    CYR_CUDA(cudaEventCreate(&p->ev1));
+  }
+  if (S <= p->buf_S && cap <= p->buf_cap) return CYR_OK;
+  release_host_path(p);
+  const int E = p->E;
+  const size_t n_alloc = (size_t)S * E, n_eps = (size_t)S * cap * E;
+  const size_t n_cb = (size_t)S * (cap + 1) * E;
+  CYR_CUDA(cudaMalloc(&p->alloc_d, n_alloc * 4));
+  CYR_CUDA(cudaMalloc(&p->eps_d, n_eps * 8));
+  CYR_CUDA(cudaMalloc(&p->raw_d, (size_t)S * cap * 2 * E * p->elem));
+  CYR_CUDA(cudaMalloc(&p->cb_d, n_cb * 4));
+  CYR_CUDA(cudaMalloc(&p->status_d, 16));
+  const size_t a = (n_alloc * 4 + 15) / 16 * 16, e = n_eps * 8, c = (n_cb * 4 + 15) / 16 * 16;
+  CYR_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p->pin), a + e + c + 16, cudaHostAllocDefault));
+  p->pin_alloc = reinterpret_cast<int32_t*>(p->pin);
+  p->pin_eps = reinterpret_cast<double*>(p->pin + a);
+  p->pin_cb = reinterpret_cast<int32_t*>(p->pin + a + e);
+  p->pin_status = reinterpret_cast<int32_t*>(p->pin + a + e + c);
+  p->buf_S = S;
+  p->buf_cap = cap;
+  return CYR_OK;
+}
+
+int check_geometry(int S, int E, int N, int L, int* cap_out) {
+  if (S < 0 || E < 1 || E > cyr::kMaxUsers || N <= 0 || L <= 0 || L >= N) return CYR_BAD_ARG;
+  const int cap = N / L;
+  if (cap < 1 || cap > 32) return CYR_UNSUPPORTED;
+  *cap_out = cap;
+  return CYR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cyr_version(void) { return 1; }
+
+const char* cyr_status_string(int status) {
+  switch (status) {
+    case CYR_OK: return "ok";
+    case CYR_INFEASIBLE: return "demand exceeds total capacity";
+    case CYR_BAD_ARG: return "invalid argument";
+    case CYR_CUDA_ERROR: return "CUDA error";
+    case CYR_UNSUPPORTED: return "unsupported geometry";
+    default: return "unknown status";
+  }
+}
+
+const char* cyr_last_error(void) { return g_last_error.c_str(); }
+
+int cyr_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor) {
+  int dev = 0;
+  CYR_CUDA(cudaGetDevice(&dev));
+  int v = 0;
+  if (sm_count) {
+    CYR_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+    *sm_count = v;
+  }
+  if (cc_major) {
+    CYR_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMajor, dev));
+    *cc_major = v;
+  }
+  if (cc_minor) {
+    CYR_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMinor, dev));
+    *cc_minor = v;
+  }
+  return CYR_OK;
+}
+
+int cyr_policy_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
+                      const double* weights_blob, int32_t precision) {
+  if (!out || !sizes || !weights_blob || n_sizes < 2 || n_sizes - 1 > cyr::kMaxLayers)
+    return CYR_BAD_ARG;
+  if (precision != CYR_FP32 && precision != CYR_FP64) return CYR_BAD_ARG;
+  const int E = sizes[0] - 1;
+  if (E < 1 || E > cyr::kMaxUsers || sizes[n_sizes - 1] != 2 * E) return CYR_BAD_ARG;
+  for (int i = 0; i < n_sizes; ++i)
+    if (sizes[i] < 1 || sizes[i] > cyr::kMaxWidth) return CYR_UNSUPPORTED;
+  cyr_policy* p = new cyr_policy();
+  p->precision = precision;
+  p->sizes.assign(sizes, sizes + n_sizes);
+  p->E = E;
+  p->elem = precision == CYR_FP64 ? 8 : 4;
+  p->sm_count = sm_count_of_current_device();
+  const int vec = 16 / (int)p->elem;
+  size_t off = 0;
+  p->desc.n_layers = n_sizes - 1;
+  p->desc.max_width = 0;
+  for (int l = 0; l < n_sizes - 1; ++l) {
+    cyr::LayerDesc& L = p->desc.layer[l];
+    L.in = sizes[l];
+    L.out = sizes[l + 1];
+    L.out_pad = (L.out + vec - 1) / vec * vec;
+    L.w_off = (long long)off;
+    off += (size_t)L.in * L.out_pad;
+    L.b_off = (long long)off;
+    off += (size_t)(L.out + vec - 1) / vec * vec;
+    p->desc.max_width = std::max(p->desc.max_width, std::max(L.in, L.out_pad));
+  }
+  p->blob_elems = off;
+  cudaError_t e = cudaMalloc(&p->blob_d, off * p->elem);
+  if (e != cudaSuccess) {
+    delete p;
+    return cuda_fail(e, "cudaMalloc(policy)");
+  }
+  const int rc = upload(p, weights_blob);
+  if (rc != CYR_OK) {
+    cudaFree(p->blob_d);
+    delete p;
+    return rc;
+  }
+  *out = p;
+  return CYR_OK;
+}
+
+int cyr_policy_update(cyr_policy* p, const double* weights_blob) {
+  if (!p || !weights_blob) return CYR_BAD_ARG;
+  CYR_CUDA(cudaDeviceSynchronize());  // no launch may still read the old weights
+  return upload(p, weights_blob);
+}
+
+int cyr_policy_load(cyr_policy** out, const char* path, int32_t precision) {
+  if (!out || !path) return CYR_BAD_ARG;
+  FILE* fh = std::fopen(path, "rb");
+  if (!fh) {
+    g_last_error = std::string("cannot open ") + path;
+    return CYR_BAD_ARG;
+  }
+  std::vector<unsigned char> data;
+  unsigned char buf[1 << 16];
+  size_t got;
+  while ((got = std::fread(buf, 1, sizeof buf, fh)) > 0) data.insert(data.end(), buf, buf + got);
+  std::fclose(fh);
+  auto fail = [&](const char* why) {
+    g_last_error = std::string(path) + ": " + why;
+    return CYR_BAD_ARG;
+  };
+  if (data.size() < 16 || std::memcmp(data.data(), "PSIMMLP1", 8) != 0)
+    return fail("not a network checkpoint");
+  uint32_t version, n_sizes;
+  std::memcpy(&version, data.data() + 8, 4);
+  std::memcpy(&n_sizes, data.data() + 12, 4);
+  if (version != 1) return fail("unsupported format version");
+  if (n_sizes < 2 || n_sizes > cyr::kMaxLayers + 1 || data.size() < 16 + 4ull * n_sizes)
+    return fail("bad header");
+  std::vector<int32_t> sizes(n_sizes);
+  for (uint32_t i = 0; i < n_sizes; ++i) {
+    uint32_t v;
+    std::memcpy(&v, data.data() + 16 + 4 * i, 4);
+    sizes[i] = (int32_t)v;
+  }
+  size_t count = 0;
+  for (uint32_t i = 0; i + 1 < n_sizes; ++i)
+    count += (size_t)sizes[i] * sizes[i + 1] + sizes[i + 1];
+  const size_t base = 16 + 4ull * n_sizes;
+  if (data.size() < base + 8 * count) return fail("checkpoint truncated");
+  if (data.size() > base + 8 * count) return fail("trailing bytes");
+  std::vector<double> blob(count);
+  std::memcpy(blob.data(), data.data() + base, 8 * count);  // little-endian host
+  return cyr_policy_create(out, sizes.data(), (int32_t)n_sizes, blob.data(), precision);
+}
+
+int cyr_policy_destroy(cyr_policy* p) {
+  if (!p) return CYR_OK;
+  cudaDeviceSynchronize();
+  release_host_path(p);
+  if (p->stream) cudaStreamDestroy(p->stream);
+  if (p->ev0) cudaEventDestroy(p->ev0);
+  if (p->ev1) cudaEventDestroy(p->ev1);
+  cudaFree(p->blob_d);
+  delete p;
+  return CYR_OK;
+}
+
+int cyr_policy_info(const cyr_policy* p, int32_t* num_users, int32_t* n_sizes, int32_t* precision) {
+  if (!p) return CYR_BAD_ARG;
+  if (num_users) *num_users = p->E;
+  if (n_sizes) *n_sizes = (int32_t)p->sizes.size();
+  if (precision) *precision = p->precision;
+  return CYR_OK;
+}
+
+int cyr_actor_forward_device(const cyr_policy* p, const int32_t* alloc, int32_t S, int32_t N,
+                             int32_t cap, void* raw, void* stream) {
+  if (!p || (S > 0 && (!alloc || !raw)) || N <= 0 || cap < 1) return CYR_BAD_ARG;
+  const int rc = cyr_launch_actor(p->precision, p->desc, p->blob_d, alloc, S, p->E, N, cap, raw,
+                                  p->sm_count, static_cast<cudaStream_t>(stream));
+  if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+  return rc;
+}
+
+size_t cyr_raw_bytes(const cyr_policy* p, int32_t S, int32_t cap) {
+  if (!p || S < 0 || cap < 0) return 0;
+  return (size_t)S * cap * 2 * p->E * p->elem;
+}
+
+int cyr_codebook_from_raw_device(const cyr_policy* p, const void* raw, const int32_t* alloc,
+                                 const double* eps, int32_t S, int32_t N, int32_t L,
+                                 int32_t* codebook, double* m_hat, double* nu, double* margin,
+                                 int32_t* iters, int32_t* status, void* stream) {
+  if (!p) return CYR_BAD_ARG;
+  int cap = 0;
+  int rc = check_geometry(S, p->E, N, L, &cap);
+  if (rc != CYR_OK) return rc;
+  if (S > 0 && (!raw || !alloc || !codebook)) return CYR_BAD_ARG;
+  rc = cyr_launch_codebook(p->precision, raw, alloc, eps, S, p->E, N, L, cap, codebook, m_hat, nu,
+                           margin, iters, status, static_cast<cudaStream_t>(stream));
+  if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+  return rc;
+}
+
+int cyr_codebook_device(const cyr_policy* p, const int32_t* alloc, const double* eps, int32_t S,
+                        int32_t N, int32_t L, int32_t* codebook, void* raw_workspace,
+                        int32_t* status, void* stream) {
+  if (!p) return CYR_BAD_ARG;
+  int cap = 0;
+  int rc = check_geometry(S, p->E, N, L, &cap);
+  if (rc != CYR_OK) return rc;
+  rc = cyr_actor_forward_device(p, alloc, S, N, cap, raw_workspace, stream);
+  if (rc != CYR_OK) return rc;
+  return cyr_codebook_from_raw_device(p, raw_workspace, alloc, eps, S, N, L, codebook, nullptr,
+                                      nullptr, nullptr, nullptr, status, stream);
+}
+
+int cyr_codebook_host(cyr_policy* p, const int32_t* alloc, const double* eps, int32_t S,
+                      int32_t N, int32_t L, int32_t* codebook, int64_t* device_ns) {
+  if (!p || !alloc || !codebook) return CYR_BAD_ARG;
+  int cap = 0;
+  int rc = check_geometry(S, p->E, N, L, &cap);
+  if (rc != CYR_OK) return rc;
+  if (S == 0) return CYR_OK;
+  const int E = p->E;
+  // reference validation order: negative inputs (ValueError), then
+  // demand > capacity (InfeasibleDemandError, enforcer.py:64)
+  for (int s = 0; s < S; ++s) {
+    long long total = 0;
+    for (int e = 0; e < E; ++e) {
+      if (alloc[(size_t)s * E + e] < 0) return CYR_BAD_ARG;
+      total += alloc[(size_t)s * E + e];
+    }
+    if ((long long)cap * L > total) return CYR_INFEASIBLE;
+  }
+  rc = ensure_host_path(p, S, cap);
+  if (rc != CYR_OK) return rc;
+  std::memcpy(p->pin_alloc, alloc, (size_t)S * E * 4);
+  const bool det = (eps == nullptr);
+  if (!det) std::memcpy(p->pin_eps, eps, (size_t)S * cap * E * 8);
+
+  const auto key = std::make_tuple(S, N, L, det ? 1 : 0);
+  auto it = p->graphs.find(key);
+  if (it == p->graphs.end()) {
+    cudaStream_t st = p->stream;
+    CYR_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+    cudaEventRecordWithFlags(p->ev0, st, cudaEventRecordExternal);
+    cudaMemcpyAsync(p->alloc_d, p->pin_alloc, (size_t)S * E * 4, cudaMemcpyHostToDevice, st);
+    if (!det)
+      cudaMemcpyAsync(p->eps_d, p->pin_eps, (size_t)S * cap * E * 8, cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(p->status_d, 0, 4, st);
+    int lrc = cyr_launch_actor(p->precision, p->desc, p->blob_d, p->alloc_d, S, E, N, cap,
+                               p->raw_d, p->sm_count, st);
+    if (lrc == CYR_OK)
+      lrc = cyr_launch_codebook(p->precision, p->raw_d, p->alloc_d, det ? nullptr : p->eps_d, S,
+                                E, N, L, cap, p->cb_d, nullptr, nullptr, nullptr, nullptr,
+                                p->status_d, st);
+    cudaMemcpyAsync(p->pin_cb, p->cb_d, (size_t)S * (cap + 1) * E * 4, cudaMemcpyDeviceToHost,
+                    st);
+    cudaMemcpyAsync(p->pin_status, p->status_d, 4, cudaMemcpyDeviceToHost, st);
+    cudaEventRecordWithFlags(p->ev1, st, cudaEventRecordExternal);
+    cudaGraph_t graph = nullptr;
+    CYR_CUDA(cudaStreamEndCapture(st, &graph));
+    if (lrc != CYR_OK) {
+      cudaGraphDestroy(graph);
+      return lrc;
+    }
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+    it = p->graphs.emplace(key, exec).first;
+  }
+  CYR_CUDA(cudaGraphLaunch(it->second, p->stream));
+  CYR_CUDA(cudaStreamSynchronize(p->stream));
+  if (*p->pin_status != CYR_OK) return *p->pin_status;
+  std::memcpy(codebook, p->pin_cb, (size_t)S * (cap + 1) * E * 4);
+  if (device_ns) {
+    float ms = 0.f;
+    CYR_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+    *device_ns = (int64_t)std::llround((double)ms * 1e6);
+  }
+  return CYR_OK;
+}
+
+int cyr_enforce_batch_device(const double* b, const double* caps, const int64_t* demand,
+                             int32_t R, int32_t E, double* m_hat, double* nu,
+                             uint8_t* degenerate, int64_t* grants, double* margin,
+                             int32_t* status, void* stream) {
+  if (R < 0 || E < 1) return CYR_BAD_ARG;
+  if (R > 0 && (!b || !caps || !demand || !grants)) return CYR_BAD_ARG;
+  const int rc = cyr_launch_enforce(b, caps, nullptr, demand, R, E, m_hat, nu, degenerate, grants, margin,
+                                    status, static_cast<cudaStream_t>(stream));
+  if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+  return rc;
+}
+
+int cyr_kl_project_batch_device(const double* b, const double* caps, const double* demand,
+                                int32_t R, int32_t E, double* m_hat, double* nu,
+                                uint8_t* degenerate, int32_t* status, void* stream) {
+  if (R < 0 || E < 1) return CYR_BAD_ARG;
+  if (R > 0 && (!b || !caps || !demand || !m_hat)) return CYR_BAD_ARG;
+  const int rc = cyr_launch_enforce(b, caps, demand, nullptr, R, E, m_hat, nu, degenerate,
+                                    nullptr, nullptr, status, static_cast<cudaStream_t>(stream));
+  if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+  return rc;
+}
+
+int cyr_apportion_batch_device(const double* m_hat, const double* caps, const int64_t* demand,
+                                int32_t R, int32_t E, int64_t* grants, double* margin,
+                                int32_t* status, void* stream) {
+  if (R < 0 || E < 1) return CYR_BAD_ARG;
+  if (R > 0 && (!m_hat || !caps || !demand || !grants)) return CYR_BAD_ARG;
+  const int rc = cyr_launch_apportion(m_hat, caps, demand, R, E, grants, margin, status,
+                                      static_cast<cudaStream_t>(stream));
+  if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+  return rc;
+}
+
+int64_t cyr_tree_num_nodes(int32_t cap, int32_t M) {
+  if (cap < 1 || M < 1) return 0;
+  int64_t total = 0, level = 1;
+  for (int t = 0; t < M; ++t) {
+    level *= (cap + 1);
+    total += level;
+  }
+  return total;
+}
+
+int32_t cyr_tree_state_stride(int32_t E) { return E < 1 ? 0 : (E + 7) / 8 * 8; }
+
+int cyr_tree_expand_device(const int32_t* codebook, int32_t S, int32_t E, int32_t cap, int32_t M,
+                           int16_t* node_state, void* stream) {
+  if (S < 0 || (S > 0 && (!codebook || !node_state))) return CYR_BAD_ARG;
+  const int rc = cyr_launch_tree(codebook, S, E, cap, M, node_state,
+                                 sm_count_of_current_device(), static_cast<cudaStream_t>(stream));
+  if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,153 @@
+// cyrus_internal.cuh — shared device helpers and host-side structs.
+//
+// Exactness rules for everything downstream of the actor logits (the
+// reference is IEEE float64 numpy, enforcer.py / neural.py):
+//   * every float64 op on the decision path is written with explicit _rn
+//     intrinsics so nvcc cannot contract a*b+c into an FMA;
+//   * row sums follow numpy's contiguous reduction: 0.0 + pairwise8(row)
+//     (numpy/_core/src/umath/loops_utils.h pairwise sum: 8 accumulators,
+//     fixed combination tree, sequential tail; n < 8 is plain sequential).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cyr {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kMaxUsers = 32;          // users are warp lanes
+constexpr int kMaxLayers = 8;
+constexpr int kMaxWidth = 1024;
+constexpr double kMassFloor = 1e-250;  // enforcer.py:25
+constexpr double kRelWidth = 1e-13;    // enforcer.py:22
+constexpr int kMaxIters = 200;         // enforcer.py:21
+constexpr double kLogSigmaMin = -20.0; // neural.py:15
+constexpr double kLogSigmaMax = 2.0;   // neural.py:16
+
+// ---------------------------------------------------------------- warp math
+__device__ __forceinline__ double shfl_d(double v, int src) {
+  return __shfl_sync(kFull, v, src);
+}
+
+// numpy float64 sum of the contiguous run v[0..n) held one element per lane
+// (lanes >= n ignored).  Every lane returns the same bits.  n <= 32.
+__device__ __forceinline__ double np_row_sum(double v, int n) {
+  double acc;
+  if (n < 8) {
+    acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+      const double x = shfl_d(v, i);
+      if (i < n) acc = __dadd_rn(acc, x);
+    }
+  } else {
+    const int j = threadIdx.x & 7;
+    const int whole = n & ~7;
+    double r = shfl_d(v, j);
+#pragma unroll
+    for (int blk = 1; blk < 4; ++blk) {
+      const double x = shfl_d(v, j + 8 * blk);
+      if (8 * blk < whole) r = __dadd_rn(r, x);
+    }
+    // ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)); IEEE addition commutes exactly,
+    // so the xor butterfly leaves that exact value in every lane.
+    r = __dadd_rn(r, __shfl_xor_sync(kFull, r, 1));
+    r = __dadd_rn(r, __shfl_xor_sync(kFull, r, 2));
+    r = __dadd_rn(r, __shfl_xor_sync(kFull, r, 4));
+    acc = r;
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+      const double x = shfl_d(v, (whole + i) & 31);
+      if (whole + i < n) acc = __dadd_rn(acc, x);
+    }
+  }
+  return __dadd_rn(0.0, acc);
+}
+
+__device__ __forceinline__ double warp_min_d(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = fmin(v, __shfl_xor_sync(kFull, v, off));
+  return v;
+}
+
+// ------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// TMA bulk copy global -> shared, completion counted on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// TMA bulk copy shared -> global (bulk-group completion).
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---------------------------------------------------------- shared structs
+struct LayerDesc {
+  int in, out, out_pad;   // Wt is [in][out_pad], row bytes multiple of 16
+  long long w_off;        // element offset of Wt in the blob
+  long long b_off;        // element offset of the bias
+};
+
+struct ActorDesc {
+  int n_layers;
+  int max_width;
+  LayerDesc layer[kMaxLayers];
+};
+
+}  // namespace cyr
+
+// --------------------------------------------------------- internal launch
+// (defined in the .cu files; status codes follow cyr_status)
+int cyr_launch_actor(int precision, const cyr::ActorDesc& desc, const void* blob,
+                     const int32_t* alloc, int S, int E, int N, int cap, void* raw,
+                     int sm_count, cudaStream_t stream);
+int cyr_launch_codebook(int precision, const void* raw, const int32_t* alloc, const double* eps,
+                        int S, int E, int N, int L, int cap, int32_t* codebook, double* m_hat,
+                        double* nu, double* margin, int32_t* iters, int32_t* status,
+                        cudaStream_t stream);
+int cyr_launch_enforce(const double* b, const double* caps, const double* demand_f,
+                       const int64_t* demand, int R, int E,
+                       double* m_hat, double* nu, uint8_t* degenerate, int64_t* grants,
+                       double* margin, int32_t* status, cudaStream_t stream);
+int cyr_launch_apportion(const double* m_hat, const double* caps, const int64_t* demand, int R,
+                         int E, int64_t* grants, double* margin, int32_t* status,
+                         cudaStream_t stream);
+int cyr_launch_tree(const int32_t* codebook, int S, int E, int cap, int M, int16_t* out,
+                    int sm_count, cudaStream_t stream);

@@ -1,0 +1,135 @@
+"""CPU: pin the oracle against the reference's golden vectors and KATs.
+
+The oracle (oracle/) is the checker for every GPU parity test, so it must
+itself reproduce the reference bit for bit.  Fixtures come from the
+unmodified reference (tests/golden/make_golden.py); the known-answer tests
+are the reference's own (pkg/tests/test_enforcer.py:20-105,
+pkg/tests/test_engine.py:81-99).
+"""
+
+import numpy as np
+import pytest
+from hypothesis import given, settings, strategies as st
+
+from oracle import arrival_tree, mlp, projection, slot
+
+
+def test_pairwise8_is_numpys_row_sum():
+    rng = np.random.default_rng(3)
+    for n in list(range(1, 40)) + [64, 127, 128, 129, 200, 300]:
+        x = rng.random((5, n)) * 10.0 ** rng.uniform(-8, 8, (5, n))
+        got = x.sum(axis=1)
+        for r in range(5):
+            assert projection.pairwise8(x[r]) == got[r]
+        assert projection.pairwise8(x[0]) == x[0].sum()
+
+
+@pytest.mark.parametrize("name", ["desk", "cfg1", "cfg2", "paper", "stress", "cfg5"])
+@pytest.mark.parametrize("mode", ["det", "sto"])
+def test_oracle_codebooks_bit_exact(golden, name, mode):
+    cfg = golden.config(name)
+    agent = cfg.agent()  # asserts the weight digest equals the reference's
+    eps = None if mode == "det" else cfg["eps"]
+    books, infos = slot.batch_codebooks(agent.actor.weights, agent.actor.biases, cfg["alloc"],
+                                        cfg.meta["total_scs"], cfg.meta["urllc_sc_len"], eps,
+                                        details=True)
+    assert np.array_equal(books, cfg[f"{mode}/codebook"])
+    for s, info in enumerate(infos):
+        assert np.array_equal(info["b"], cfg[f"{mode}/b"][s])
+        assert np.array_equal(info["m_hat"], cfg[f"{mode}/m_hat"][s])
+        assert np.array_equal(info["nu"], cfg[f"{mode}/nu"][s])
+        assert np.array_equal(info["degenerate"], cfg[f"{mode}/degenerate"][s])
+
+
+def test_oracle_enforcer_corpus_bit_exact(golden):
+    groups = 0
+    for b, caps, dem, m_hat, nu, deg, grants in golden.enforcer_groups():
+        got, info = projection.enforce(b, caps, dem, with_details=True)
+        assert np.array_equal(got, grants)
+        assert np.array_equal(info["m_hat"], m_hat)
+        assert np.array_equal(info["nu"], nu)
+        assert np.array_equal(info["degenerate"], deg)
+        groups += 1
+    assert groups == 400
+
+
+# ---- the reference's own known-answer tests (pkg/tests/test_enforcer.py)
+def _proj(b, caps, d):
+    m, nu, deg, _ = projection.project(np.atleast_2d(np.asarray(b, float)),
+                                       np.atleast_2d(np.asarray(caps, float)),
+                                       np.asarray([d], float))
+    return m[0], deg[0]
+
+
+def _seats(m, caps, d):
+    return list(projection.apportion(np.atleast_2d(m), np.atleast_2d(np.asarray(caps, float)),
+                                     np.asarray([d]))[0])
+
+
+def test_kat_worked_example():
+    m, _ = _proj([8.0, 4.0, 4.0], [5, 10, 10], 12)
+    assert np.allclose(m, [5.0, 3.5, 3.5], atol=1e-9)
+    assert _seats(m, [5, 10, 10], 12) == [5, 4, 3]
+
+
+def test_kat_degenerate_spreads_slack():
+    m, deg = _proj([1.0, 0.0, 0.0], [2, 4, 2], 8)
+    assert deg and m[0] == 2.0 and np.allclose(m, [2.0, 4.0, 2.0], atol=1e-9)
+    m, _ = _proj([1.0, 0.0, 0.0], [2, 6, 2], 6)
+    assert m[0] == 2.0 and abs(m[1] - 3.0) < 1e-9 and abs(m[2] - 1.0) < 1e-9
+
+
+def test_kat_ties_caps_and_errors():
+    assert _seats(np.array([2.0, 2.0, 2.0]), [4, 4, 4], 2) == [1, 1, 0]
+    assert _seats(np.array([5.0, 0.1]), [3, 4], 6) == [3, 3]
+    with pytest.raises(projection.InfeasibleDemand):
+        _proj([1.0, 1.0], [3, 3], 7)
+    with pytest.raises(ValueError):
+        projection.apportion(np.array([[1.0, 1.0]]), np.array([[3.0, 3.0]]), np.array([-1]))
+
+
+@settings(max_examples=200, deadline=None)
+@given(st.integers(1, 5).flatmap(lambda e: st.tuples(
+    st.lists(st.floats(0.0, 50.0), min_size=e, max_size=e),
+    st.lists(st.integers(1, 30), min_size=e, max_size=e),
+    st.floats(0.0, 1.0))))
+def test_oracle_feasibility_property(args):
+    b, caps, frac = args
+    demand = int(round(frac * sum(caps)))
+    m, _ = _proj(b, caps, demand)
+    assert abs(m.sum() - demand) < 1e-6 * max(demand, 1)
+    assert np.all(m >= -1e-12) and np.all(m <= np.asarray(caps) + 1e-9)
+    seats = _seats(m, caps, demand)
+    assert sum(seats) == demand and all(0 <= s <= c for s, c in zip(seats, caps))
+
+
+def test_codebook_column_contract(golden):
+    # test_engine.py:81-99: col 0 zero, col j sums to j*L, 0 <= m <= n
+    for name in golden.names:
+        cfg = golden.config(name)
+        l = cfg.meta["urllc_sc_len"]
+        for mode in ("det", "sto"):
+            books = cfg[f"{mode}/codebook"]
+            assert (books[:, 0] == 0).all()
+            for j in range(1, books.shape[1]):
+                assert (books[:, j].sum(axis=1) == j * l).all()
+            assert (books >= 0).all() and (books <= cfg["alloc"][:, None, :]).all()
+
+
+def test_tree_oracle_structure():
+    book = np.array([[0, 0, 0], [1, 2, 0], [3, 0, 5]])
+    states = arrival_tree.node_states(book, 3)
+    assert states.shape == (3 + 9 + 27, 3)
+    # node of path (2, 1): level 2, index 2*3+1 = 7 -> offset 3 + 7
+    assert list(states[3 + 7]) == [4, 2, 5]
+    arr = arrival_tree.node_arrivals(2, 3)
+    assert arr[3 + 7] == 3 and arr.max() == 6
+
+
+def test_head_matches_reference_formula():
+    raw = np.array([[0.5], [-0.5], [-30.0], [5.0]])
+    a = mlp.head(raw, 2)
+    assert np.array_equal(a, np.tanh(raw[:2]))
+    eps = np.array([[0.7], [-1.1]])
+    a = mlp.head(raw, 2, eps)
+    assert np.array_equal(a, np.tanh(raw[:2] + np.exp(np.array([[-20.0], [2.0]])) * eps))

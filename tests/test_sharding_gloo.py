@@ -1,0 +1,68 @@
+"""CPU, world_size 2 over gloo: the multi-GPU O-DU batch path's host logic.
+
+Each rank computes its contiguous block of cells and one all-gather
+assembles the batch (paper_2506_00167_b200/sharding.py).  On CPU the
+per-shard compute is the oracle (test infrastructure); the assembled result
+must equal the single-process oracle batch and the reference's codebooks.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, cells, queue):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import slot
+        from paper_2506_00167_b200 import sharding
+        from tests.golden_util import Golden
+        cfg = Golden.load().config("cfg2")
+        agent = cfg.agent()
+        allocs = np.asarray(cfg["alloc"][:cells])
+        eps = np.asarray(cfg["eps"][:cells])
+
+        def compute(a, e):
+            books = slot.batch_codebooks(agent.actor.weights, agent.actor.biases, a,
+                                         cfg.meta["total_scs"], cfg.meta["urllc_sc_len"], e)
+            return torch.from_numpy(np.asarray(books, dtype=np.int32).reshape(len(a), -1, a.shape[1]))
+
+        full, local = sharding.build_codebooks_sharded(compute, allocs, eps)
+        lo, hi = sharding.shard_bounds(cells, world, rank)
+        queue.put((rank, full.numpy(), (lo, hi), local.shape[0]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cells", [8, 7])
+def test_two_rank_shard_and_gather(golden, cells):
+    ctx = mp.get_context("spawn")
+    queue = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, cells, queue)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = [queue.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    expect = golden.config("cfg2")["sto/codebook"][:cells]
+    spans = {}
+    for rank, full, span, n_local in results:
+        assert np.array_equal(full, expect), f"rank {rank} assembled a different batch"
+        assert n_local == span[1] - span[0]
+        spans[rank] = span
+    assert spans[0][1] == spans[1][0] and spans[1][1] == cells
