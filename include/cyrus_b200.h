@@ -151,6 +151,19 @@ int32_t cyr_tree_state_stride(int32_t E);
 int cyr_tree_expand_device(const int32_t* codebook, int32_t S, int32_t E, int32_t cap,
                            int32_t M, int16_t* node_state, void* stream);
 
+/* ---- diagnostics ---------------------------------------------------------- */
+/* The projection's lean correctly-rounded sqrt against IEEE __dsqrt_rn on n
+ * log-uniform / near-midpoint inputs; *mismatches receives the count.
+ * Synchronous. */
+int cyr_selftest_sqrt(int64_t n, uint64_t seed, int64_t* mismatches);
+/* Cycles for `iters` dependent steps of an fp64 building block (one warp):
+ * 0 DFMA, 1 DMUL, 2 lean sqrt, 3 __dsqrt_rn, 4 __ddiv_rn, 5 FFMA,
+ * 6 coupled-bisection body, 7 SHFL, 8 vote.all, 9 MUFU.RSQ64H. */
+int cyr_selftest_latency(int32_t which, int32_t iters, int64_t* cycles);
+/* Phase timestamps (%globaltimer, ns) of the last latency-path launch when
+ * the process runs with CYR_TRACE=1; zeros otherwise.  n <= 64. */
+int cyr_debug_trace(int64_t* out, int32_t n);
+
 #ifdef __cplusplus
 }
 #endif

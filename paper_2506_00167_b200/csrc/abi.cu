@@ -10,6 +10,7 @@
 #include "cyrus_b200.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -45,7 +46,26 @@ int sm_count_of_current_device() {
   return cache[dev];
 }
 
+unsigned long long* g_trace_host = nullptr;
+unsigned long long* g_trace_dev = nullptr;
+
 }  // namespace
+
+unsigned long long* cyr_trace_buffer() {
+  static const bool on = [] {
+    const char* e = getenv("CYR_TRACE");
+    return e != nullptr && e[0] == '1';
+  }();
+  if (!on) return nullptr;
+  if (g_trace_host == nullptr) {
+    if (cudaHostAlloc(reinterpret_cast<void**>(&g_trace_host), 64 * sizeof(unsigned long long),
+                      cudaHostAllocMapped) != cudaSuccess)
+      return nullptr;
+    std::memset(g_trace_host, 0, 64 * sizeof(unsigned long long));
+    cudaHostGetDevicePointer(reinterpret_cast<void**>(&g_trace_dev), g_trace_host, 0);
+  }
+  return g_trace_dev;
+}
 
 struct cyr_policy {
   int precision = CYR_FP32;
@@ -66,6 +86,7 @@ struct cyr_policy {
   int32_t* cb_d = nullptr;
   int32_t* status_d = nullptr;
   unsigned char* pin = nullptr;
+  unsigned char* pin_dev = nullptr;  // device alias of the mapped pinned block
   int32_t* pin_alloc = nullptr;
   double* pin_eps = nullptr;
   int32_t* pin_cb = nullptr;
@@ -85,6 +106,9 @@ void pack_blob(const cyr_policy& p, const double* src, std::vector<T>& dst) {
     for (int o = 0; o < L.out; ++o)
       for (int i = 0; i < L.in; ++i)
         dst[L.w_off + (size_t)i * L.out_pad + o] = (T)src[off + (size_t)o * L.in + i];
+    for (int o = 0; o < L.out; ++o)
+      for (int i = 0; i < L.in; ++i)
+        dst[L.wr_off + (size_t)o * L.in_pad + i] = (T)src[off + (size_t)o * L.in + i];
     off += (size_t)L.out * L.in;
     for (int o = 0; o < L.out; ++o) dst[L.b_off + o] = (T)src[off + o];
     off += L.out;
@@ -119,6 +143,7 @@ void release_host_path(cyr_policy* p) {
   p->cb_d = nullptr;
   p->status_d = nullptr;
   p->pin = nullptr;
+  p->pin_dev = nullptr;
   p->buf_S = p->buf_cap = 0;
 }
 
@@ -139,7 +164,11 @@ int ensure_host_path(cyr_policy* p, int S, int cap) {
   CYR_CUDA(cudaMalloc(&p->cb_d, n_cb * 4));
   CYR_CUDA(cudaMalloc(&p->status_d, 16));
   const size_t a = (n_alloc * 4 + 15) / 16 * 16, e = n_eps * 8, c = (n_cb * 4 + 15) / 16 * 16;
-  CYR_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p->pin), a + e + c + 16, cudaHostAllocDefault));
+  // mapped: the single-slot graph reads its inputs and writes its results
+  // through these pages directly (no copy nodes)
+  CYR_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p->pin), a + e + c + 16,
+                         cudaHostAllocMapped | cudaHostAllocPortable));
+  CYR_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->pin_dev), p->pin, 0));
   p->pin_alloc = reinterpret_cast<int32_t*>(p->pin);
   p->pin_eps = reinterpret_cast<double*>(p->pin + a);
   p->pin_cb = reinterpret_cast<int32_t*>(p->pin + a + e);
@@ -152,7 +181,7 @@ int ensure_host_path(cyr_policy* p, int S, int cap) {
 int check_geometry(int S, int E, int N, int L, int* cap_out) {
   if (S < 0 || E < 1 || E > cyr::kMaxUsers || N <= 0 || L <= 0 || L >= N) return CYR_BAD_ARG;
   const int cap = N / L;
-  if (cap < 1 || cap > 32) return CYR_UNSUPPORTED;
+  if (cap < 1 || cap > 16) return CYR_UNSUPPORTED;
   *cap_out = cap;
   return CYR_OK;
 }
@@ -214,16 +243,21 @@ int cyr_policy_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
   size_t off = 0;
   p->desc.n_layers = n_sizes - 1;
   p->desc.max_width = 0;
+  p->desc.max_rows = 0;
   for (int l = 0; l < n_sizes - 1; ++l) {
     cyr::LayerDesc& L = p->desc.layer[l];
     L.in = sizes[l];
     L.out = sizes[l + 1];
     L.out_pad = (L.out + vec - 1) / vec * vec;
+    L.in_pad = (L.in + vec - 1) / vec * vec;
     L.w_off = (long long)off;
     off += (size_t)L.in * L.out_pad;
     L.b_off = (long long)off;
     off += (size_t)(L.out + vec - 1) / vec * vec;
+    L.wr_off = (long long)off;
+    off += (size_t)L.out * L.in_pad;
     p->desc.max_width = std::max(p->desc.max_width, std::max(L.in, L.out_pad));
+    p->desc.max_rows = std::max(p->desc.max_rows, std::max(L.in_pad, L.out));
   }
   p->blob_elems = off;
   cudaError_t e = cudaMalloc(&p->blob_d, off * p->elem);
@@ -344,6 +378,12 @@ int cyr_codebook_device(const cyr_policy* p, const int32_t* alloc, const double*
   int cap = 0;
   int rc = check_geometry(S, p->E, N, L, &cap);
   if (rc != CYR_OK) return rc;
+  if (S > 0 && S * cap <= 8) {  // latency path: K2 + K3 in one cluster launch
+    rc = cyr_launch_slot_fused(p->precision, p->desc, p->blob_d, alloc, eps, S, p->E, N, L, cap,
+                               codebook, nullptr, status, static_cast<cudaStream_t>(stream));
+    if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+    return rc;
+  }
   rc = cyr_actor_forward_device(p, alloc, S, N, cap, raw_workspace, stream);
   if (rc != CYR_OK) return rc;
   return cyr_codebook_from_raw_device(p, raw_workspace, alloc, eps, S, N, L, codebook, nullptr,
@@ -375,24 +415,62 @@ int cyr_codebook_host(cyr_policy* p, const int32_t* alloc, const double* eps, in
   if (!det) std::memcpy(p->pin_eps, eps, (size_t)S * cap * E * 8);
 
   const auto key = std::make_tuple(S, N, L, det ? 1 : 0);
+  const bool fused = S * cap <= 8 && S * E <= 256 && S * cap * E <= 256;
+  auto dev = [&](const void* host_ptr) {  // device alias of a mapped host pointer
+    return reinterpret_cast<unsigned char*>(p->pin_dev) +
+           (reinterpret_cast<const unsigned char*>(host_ptr) - p->pin);
+  };
+  *p->pin_status = CYR_OK;
+  if (fused) {
+    // latency path: ONE cluster launch (K2 + K3), inputs by value in the
+    // launch parameters, codebook + status written straight to mapped pages
+    cyr::SlotInline inl;
+    std::memcpy(inl.alloc, alloc, (size_t)S * E * 4);
+    if (!det) std::memcpy(inl.eps, eps, (size_t)S * cap * E * 8);
+    cudaStream_t st = p->stream;
+    CYR_CUDA(cudaEventRecord(p->ev0, st));
+    int lrc = cyr_launch_slot_fused(p->precision, p->desc, p->blob_d, nullptr, eps, S, E, N, L,
+                                    cap, p->cb_d, reinterpret_cast<int32_t*>(dev(p->pin_cb)),
+                                    reinterpret_cast<int32_t*>(dev(p->pin_status)), st, &inl);
+    if (lrc != CYR_OK) {
+      if (lrc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+      return lrc;
+    }
+    CYR_CUDA(cudaEventRecord(p->ev1, st));
+    CYR_CUDA(cudaEventSynchronize(p->ev1));
+    const int32_t code = *reinterpret_cast<volatile int32_t*>(p->pin_status);
+    if (code != CYR_OK) return code;
+    std::memcpy(codebook, p->pin_cb, (size_t)S * (cap + 1) * E * 4);
+    if (device_ns) {
+      float ms = 0.f;
+      CYR_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+      *device_ns = (int64_t)std::llround((double)ms * 1e6);
+    }
+    return CYR_OK;
+  }
   auto it = p->graphs.find(key);
   if (it == p->graphs.end()) {
     cudaStream_t st = p->stream;
     CYR_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
     cudaEventRecordWithFlags(p->ev0, st, cudaEventRecordExternal);
-    cudaMemcpyAsync(p->alloc_d, p->pin_alloc, (size_t)S * E * 4, cudaMemcpyHostToDevice, st);
-    if (!det)
-      cudaMemcpyAsync(p->eps_d, p->pin_eps, (size_t)S * cap * E * 8, cudaMemcpyHostToDevice, st);
-    cudaMemsetAsync(p->status_d, 0, 4, st);
-    int lrc = cyr_launch_actor(p->precision, p->desc, p->blob_d, p->alloc_d, S, E, N, cap,
-                               p->raw_d, p->sm_count, st);
-    if (lrc == CYR_OK)
-      lrc = cyr_launch_codebook(p->precision, p->raw_d, p->alloc_d, det ? nullptr : p->eps_d, S,
-                                E, N, L, cap, p->cb_d, nullptr, nullptr, nullptr, nullptr,
-                                p->status_d, st);
-    cudaMemcpyAsync(p->pin_cb, p->cb_d, (size_t)S * (cap + 1) * E * 4, cudaMemcpyDeviceToHost,
-                    st);
-    cudaMemcpyAsync(p->pin_status, p->status_d, 4, cudaMemcpyDeviceToHost, st);
+    int lrc = CYR_OK;
+    {
+      (void)dev;
+      cudaMemcpyAsync(p->alloc_d, p->pin_alloc, (size_t)S * E * 4, cudaMemcpyHostToDevice, st);
+      if (!det)
+        cudaMemcpyAsync(p->eps_d, p->pin_eps, (size_t)S * cap * E * 8, cudaMemcpyHostToDevice,
+                        st);
+      cudaMemsetAsync(p->status_d, 0, 4, st);
+      lrc = cyr_launch_actor(p->precision, p->desc, p->blob_d, p->alloc_d, S, E, N, cap,
+                             p->raw_d, p->sm_count, st);
+      if (lrc == CYR_OK)
+        lrc = cyr_launch_codebook(p->precision, p->raw_d, p->alloc_d, det ? nullptr : p->eps_d,
+                                  S, E, N, L, cap, p->cb_d, nullptr, nullptr, nullptr, nullptr,
+                                  p->status_d, st);
+      cudaMemcpyAsync(p->pin_cb, p->cb_d, (size_t)S * (cap + 1) * E * 4, cudaMemcpyDeviceToHost,
+                      st);
+      cudaMemcpyAsync(p->pin_status, p->status_d, 4, cudaMemcpyDeviceToHost, st);
+    }
     cudaEventRecordWithFlags(p->ev1, st, cudaEventRecordExternal);
     cudaGraph_t graph = nullptr;
     CYR_CUDA(cudaStreamEndCapture(st, &graph));
@@ -470,6 +548,47 @@ int cyr_tree_expand_device(const int32_t* codebook, int32_t S, int32_t E, int32_
   const int rc = cyr_launch_tree(codebook, S, E, cap, M, node_state,
                                  sm_count_of_current_device(), static_cast<cudaStream_t>(stream));
   if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+  return rc;
+}
+
+int cyr_selftest_sqrt(int64_t n, uint64_t seed, int64_t* mismatches) {
+  if (n < 0 || !mismatches) return CYR_BAD_ARG;
+  unsigned long long* d = nullptr;
+  CYR_CUDA(cudaMalloc(&d, sizeof(unsigned long long)));
+  CYR_CUDA(cudaMemset(d, 0, sizeof(unsigned long long)));
+  int rc = cyr_launch_sqrt_selftest((long long)n, (unsigned long long)seed, d, nullptr);
+  unsigned long long h = 0;
+  if (rc == CYR_OK) {
+    cudaError_t e = cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = cuda_fail(e, "selftest copy");
+  }
+  cudaFree(d);
+  *mismatches = (int64_t)h;
+  return rc;
+}
+
+int cyr_debug_trace(int64_t* out, int32_t n) {
+  if (!out || n < 0) return CYR_BAD_ARG;
+  for (int i = 0; i < n && i < 64; ++i)
+    out[i] = g_trace_host ? (int64_t)g_trace_host[i] : 0;
+  return CYR_OK;
+}
+
+int cyr_selftest_latency(int32_t which, int32_t iters, int64_t* cycles) {
+  if (!cycles || iters < 1) return CYR_BAD_ARG;
+  long long* d = nullptr;
+  double* sink = nullptr;
+  CYR_CUDA(cudaMalloc(&d, sizeof(long long)));
+  CYR_CUDA(cudaMalloc(&sink, 32 * sizeof(double)));
+  int rc = cyr_launch_latency_bench(which, iters, d, sink);
+  long long h = 0;
+  if (rc == CYR_OK) {
+    cudaError_t e = cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = cuda_fail(e, "latency bench copy");
+  }
+  cudaFree(d);
+  cudaFree(sink);
+  *cycles = (int64_t)h;
   return rc;
 }
 

@@ -18,8 +18,18 @@
 //     activation row is a broadcast LDS.128 stream.
 // Precision: CYR_FP32 (fp32 SIMT, FMA) is the default; CYR_FP64 keeps the
 // reference's float64 (logits within ~1e-15 relative of OpenBLAS dgemm).
-#include "cyrus_internal.cuh"
-#include "cyrus_b200.h"
+//
+// Latency variant (<= 8 columns, i.e. one or two slots): a single CTA would
+// be bound by one SM pulling every weight byte, so the layer's neurons are
+// spread over a thread-block cluster instead.  Each warp owns a few output
+// neurons, streams their row-major weight rows straight from L2 with 128-bit
+// loads (lanes split the input dimension), reduces the partial dot products
+// with warp shuffles, and broadcasts the activations to every CTA of the
+// cluster through distributed shared memory; one cluster barrier per layer.
+#include "projection.cuh"
+
+#include <cooperative_groups.h>
+#include <cstdlib>
 
 namespace cyr {
 
@@ -35,6 +45,14 @@ struct ActorLaunch {
   void* raw;
   int S, E, N, cap, ncols;
   int stages;
+  // fused single-slot path (K2 -> K3 in one cluster launch)
+  const double* eps;
+  int L;
+  int32_t* cb;       // device codebook [S][cap+1][E]
+  int32_t* cb_host;  // optional mapped-host copy of the codebook
+  int32_t* status;
+  unsigned long long* trace;  // CYR_TRACE phase stamps (rank 0), or null
+  int inline_inputs;          // alloc / eps come from the SlotInline parameter
 };
 
 __host__ __device__ inline int rows_per_stage(const LayerDesc& L, int elem) {
@@ -195,6 +213,186 @@ __global__ void __launch_bounds__(kActorThreads, 1) actor_kernel(const ActorLaun
   }
 }
 
+// ------------------------------------------------------ latency (cluster)
+constexpr int kLatThreads = 256;
+constexpr int kLatOW = 4;  // output neurons a warp works on concurrently
+
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<float> {
+  static constexpr int n = 4;
+  __device__ static void load(const float* p, float (&v)[4]) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  }
+};
+template <>
+struct Vec16<double> {
+  static constexpr int n = 2;
+  __device__ static void load(const double* p, double (&v)[2]) {
+    const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+    v[0] = t.x; v[1] = t.y;
+  }
+};
+
+template <typename T, int C, bool FUSE>
+__global__ void __launch_bounds__(kLatThreads, 1)
+    actor_cluster_kernel(const ActorLaunch p, const __grid_constant__ SlotInline inl) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int G = (int)cluster.num_blocks();
+  const int g = (int)cluster.block_rank();
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int V = Vec16<T>::n;
+  const int rows = p.desc.max_rows;
+  T* act0 = reinterpret_cast<T*>(smem);
+  T* act1 = act0 + (size_t)rows * C;
+  T* raw_s = act1 + (size_t)rows * C;  // FUSE: rank 0 collects the logits [col][2E]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const T* blob = static_cast<const T*>(p.blob);
+  const int32_t* alloc = p.inline_inputs ? inl.alloc : p.alloc;
+  const double* eps = p.inline_inputs ? (p.eps ? inl.eps : nullptr) : p.eps;
+
+  unsigned long long* tr = (FUSE && g == 0) ? p.trace : nullptr;
+  trace_stamp(tr, 0);
+  for (int idx = tid; idx < 2 * rows * C; idx += blockDim.x) act0[idx] = T(0);
+  __syncthreads();
+  for (int idx = tid; idx < (p.E + 1) * C; idx += blockDim.x) {
+    const int i = idx / C, c = idx % C;
+    double v = 0.0;
+    if (c < p.ncols) {
+      const int s = c / p.cap, j = c % p.cap + 1;
+      v = (i < p.E) ? (double)alloc[(long long)s * p.E + i] / (double)p.N
+                    : (double)j / (double)p.cap;
+    }
+    act0[i * C + c] = (T)v;
+  }
+  cluster.sync();  // every CTA is live and has its input before any DSMEM store
+  trace_stamp(tr, 1);
+
+  const int nl = p.desc.n_layers;
+  for (int l = 0; l < nl; ++l) {
+    const LayerDesc& L = p.desc.layer[l];
+    const T* cur = (l & 1) ? act1 : act0;
+    T* nxt = (l & 1) ? act0 : act1;
+    const bool last = l == nl - 1;
+    const T* W = blob + L.wr_off;
+    const int nvec = L.in_pad / V;
+    const int stride = G * nwarps;  // outputs are dealt round-robin: rank, then warp
+    for (int o0 = g + G * warp; o0 < L.out; o0 += stride * kLatOW) {
+      T acc[kLatOW][C];
+#pragma unroll
+      for (int k = 0; k < kLatOW; ++k)
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[k][c] = T(0);
+      for (int iv = lane; iv < nvec; iv += 32) {
+        T w[kLatOW][V];
+#pragma unroll
+        for (int k = 0; k < kLatOW; ++k) {
+          const int o = o0 + k * stride;
+          if (o < L.out) Vec16<T>::load(W + (size_t)o * L.in_pad + (size_t)iv * V, w[k]);
+          else
+#pragma unroll
+            for (int q = 0; q < V; ++q) w[k][q] = T(0);
+        }
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          const T* xr = cur + (size_t)(iv * V + q) * C;
+          T x[C];
+#pragma unroll
+          for (int c = 0; c < C; ++c) x[c] = xr[c];
+#pragma unroll
+          for (int k = 0; k < kLatOW; ++k)
+#pragma unroll
+            for (int c = 0; c < C; ++c) acc[k][c] = fma(w[k][q], x[c], acc[k][c]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kLatOW; ++k)
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1)
+            acc[k][c] += __shfl_xor_sync(kFull, acc[k][c], off);
+#pragma unroll
+      for (int k = 0; k < kLatOW; ++k) {
+        const int o = o0 + k * stride;
+        if (o >= L.out) continue;  // warp-uniform
+        const T bias = blob[L.b_off + o];
+        if (last) {
+          T* raw = FUSE ? cluster.map_shared_rank(raw_s, 0) : static_cast<T*>(p.raw);
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            if (lane == c && c < p.ncols) raw[(long long)c * L.out + o] = acc[k][c] + bias;
+        } else {
+          // lane r*C + c stores column c of neuron o into cluster rank r
+          for (int t = lane; t < G * C; t += 32) {
+            const int r = t / C, c = t % C;
+            T v = T(0);
+#pragma unroll
+            for (int cc = 0; cc < C; ++cc)
+              if (cc == c) v = acc[k][cc] + bias;
+            v = v > T(0) ? v : T(0);
+            T* remote = cluster.map_shared_rank(nxt, r);
+            remote[(size_t)o * C + c] = v;
+          }
+        }
+      }
+    }
+    cluster.sync();
+    trace_stamp(tr, 2 + l);
+  }
+  if constexpr (FUSE) {
+    // K3 for the slot(s) on rank 0: logits never leave shared memory
+    if (g != 0) return;
+    __shared__ double s_lo[32], s_hi[32];
+    __shared__ long long s_t[32];
+    __shared__ int s_bis[32];
+    codebook_rows<T>(raw_s, alloc, eps, 0, p.ncols, p.cap, p.E, p.L, p.cb, nullptr, nullptr,
+                     nullptr, nullptr, p.status, s_lo, s_hi, s_t, s_bis, tr);
+    if (p.cb_host != nullptr) {
+      __syncthreads();
+      const int n = p.S * (p.cap + 1) * p.E;
+      for (int i = tid; i < n; i += blockDim.x) p.cb_host[i] = p.cb[i];
+    }
+    trace_stamp(tr, 15);
+  }
+}
+
+template <typename T, int C, bool FUSE>
+int launch_actor_cluster(const ActorLaunch& p, int G, cudaStream_t stream,
+                         const SlotInline* inl = nullptr) {
+  const size_t smem = (2ull * p.desc.max_rows * C + (FUSE ? (size_t)C * 2 * p.E : 0)) * sizeof(T);
+  if (smem > (size_t)kSmemLimit) return CYR_UNSUPPORTED;
+  auto kern = actor_cluster_kernel<T, C, FUSE>;
+  static int configured_smem = -1;  // attributes are per function: set once
+  if ((int)smem > configured_smem) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return CYR_CUDA_ERROR;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+        cudaSuccess)
+      return CYR_CUDA_ERROR;
+    configured_smem = (int)smem;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(kLatThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  static SlotInline empty{};
+  return cudaLaunchKernelEx(&cfg, kern, p, inl ? *inl : empty) == cudaSuccess ? CYR_OK
+                                                                              : CYR_CUDA_ERROR;
+}
+
 template <typename T, int TC, int OPT>
 int launch_actor_t(const ActorLaunch& base, cudaStream_t stream) {
   ActorLaunch p = base;
@@ -220,7 +418,9 @@ int launch_actor_opt(const ActorLaunch& p, int tc, cudaStream_t stream) {
     case 4: return launch_actor_t<T, 4, OPT>(p, stream);
     case 8: return launch_actor_t<T, 8, OPT>(p, stream);
     case 16: return launch_actor_t<T, 16, OPT>(p, stream);
-    default: return launch_actor_t<T, 32, OPT>(p, stream);
+    default:
+      if constexpr (sizeof(T) * 32 * OPT <= 256) return launch_actor_t<T, 32, OPT>(p, stream);
+      else return launch_actor_t<T, 16, OPT>(p, stream);
   }
 }
 
@@ -259,6 +459,58 @@ int cyr_launch_actor(int precision, const cyr::ActorDesc& desc, const void* blob
   p.N = N;
   p.cap = cap;
   p.ncols = S * cap;
+  if (p.ncols <= 8) {  // latency path: one cluster spreads every layer over G SMs
+    const char* env = getenv("CYR_ACTOR_CLUSTER");
+    const int G = env ? atoi(env) : 8;
+    if (G > 1) {
+      const bool fp64 = precision == CYR_FP64;
+      if (p.ncols <= 4)
+        return fp64 ? cyr::launch_actor_cluster<double, 4, false>(p, G, stream)
+                    : cyr::launch_actor_cluster<float, 4, false>(p, G, stream);
+      return fp64 ? cyr::launch_actor_cluster<double, 8, false>(p, G, stream)
+                  : cyr::launch_actor_cluster<float, 8, false>(p, G, stream);
+    }
+  }
   if (precision == CYR_FP64) return cyr::launch_actor_typed<double>(p, sm_count, stream);
   return cyr::launch_actor_typed<float>(p, sm_count, stream);
+}
+
+int cyr_cluster_size() {
+  const char* env = getenv("CYR_ACTOR_CLUSTER");
+  const int G = env ? atoi(env) : 8;
+  return G < 2 ? 8 : G;
+}
+
+// K2 -> K3 fused in one cluster launch for S*cap <= 8 columns (the latency
+// path).  alloc / eps / cb_host / status may point at mapped host memory.
+int cyr_launch_slot_fused(int precision, const cyr::ActorDesc& desc, const void* blob,
+                          const int32_t* alloc, const double* eps, int S, int E, int N, int L,
+                          int cap, int32_t* cb, int32_t* cb_host, int32_t* status,
+                          cudaStream_t stream, const cyr::SlotInline* inl) {
+  if (S <= 0) return CYR_OK;
+  if (S * cap > 8 || E > cyr::kMaxUsers || desc.max_width > cyr::kMaxWidth) return CYR_UNSUPPORTED;
+  cyr::ActorLaunch p{};
+  p.desc = desc;
+  p.blob = blob;
+  p.alloc = alloc;
+  p.S = S;
+  p.E = E;
+  p.N = N;
+  p.cap = cap;
+  p.ncols = S * cap;
+  p.eps = eps;
+  p.L = L;
+  p.cb = cb;
+  p.cb_host = cb_host;
+  p.status = status;
+  p.trace = cyr_trace_buffer();
+  p.inline_inputs = inl != nullptr;
+  if (inl != nullptr && (S * E > 256 || S * cap * E > 256)) return CYR_UNSUPPORTED;
+  const int G = cyr_cluster_size();
+  const bool fp64 = precision == CYR_FP64;
+  if (p.ncols <= 4)
+    return fp64 ? cyr::launch_actor_cluster<double, 4, true>(p, G, stream, inl)
+                : cyr::launch_actor_cluster<float, 4, true>(p, G, stream, inl);
+  return fp64 ? cyr::launch_actor_cluster<double, 8, true>(p, G, stream, inl)
+              : cyr::launch_actor_cluster<float, 8, true>(p, G, stream, inl);
 }

@@ -118,16 +118,40 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ------------------------------------------------------------ phase trace
+// When the library runs with CYR_TRACE=1, kernels on the latency path stamp
+// %globaltimer at phase boundaries into a mapped host buffer (slot k of
+// cyr_debug_trace); otherwise the pointer is null and this is a no-op.
+__device__ __forceinline__ void trace_stamp(unsigned long long* buf, int k) {
+  if (buf != nullptr && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    buf[k] = t;
+    buf[32 + k] = (unsigned long long)clock64();
+  }
+}
+
 // ---------------------------------------------------------- shared structs
 struct LayerDesc {
   int in, out, out_pad;   // Wt is [in][out_pad], row bytes multiple of 16
+  int in_pad;             // W row-major copy is [out][in_pad] (latency kernel)
   long long w_off;        // element offset of Wt in the blob
   long long b_off;        // element offset of the bias
+  long long wr_off;       // element offset of the row-major W copy
+};
+
+// Single-slot inputs passed BY VALUE in the kernel launch (param space, read
+// through a __grid_constant__ pointer): no copy node and no PCIe read on the
+// latency path.  S*E <= 256 and S*cap*E <= 256.
+struct SlotInline {
+  int32_t alloc[256];
+  double eps[256];
 };
 
 struct ActorDesc {
   int n_layers;
-  int max_width;
+  int max_width;          // max over layers of max(in, out_pad)
+  int max_rows;           // max over layers of max(in_pad, out)
   LayerDesc layer[kMaxLayers];
 };
 
@@ -138,6 +162,11 @@ struct ActorDesc {
 int cyr_launch_actor(int precision, const cyr::ActorDesc& desc, const void* blob,
                      const int32_t* alloc, int S, int E, int N, int cap, void* raw,
                      int sm_count, cudaStream_t stream);
+// alloc / eps are device pointers, or (inl != nullptr) taken from *inl by value
+int cyr_launch_slot_fused(int precision, const cyr::ActorDesc& desc, const void* blob,
+                          const int32_t* alloc, const double* eps, int S, int E, int N, int L,
+                          int cap, int32_t* cb, int32_t* cb_host, int32_t* status,
+                          cudaStream_t stream, const cyr::SlotInline* inl = nullptr);
 int cyr_launch_codebook(int precision, const void* raw, const int32_t* alloc, const double* eps,
                         int S, int E, int N, int L, int cap, int32_t* codebook, double* m_hat,
                         double* nu, double* margin, int32_t* iters, int32_t* status,
@@ -151,3 +180,7 @@ int cyr_launch_apportion(const double* m_hat, const double* caps, const int64_t*
                          cudaStream_t stream);
 int cyr_launch_tree(const int32_t* codebook, int S, int E, int cap, int M, int16_t* out,
                     int sm_count, cudaStream_t stream);
+int cyr_launch_sqrt_selftest(long long n, unsigned long long seed, unsigned long long* mismatches,
+                             cudaStream_t stream);
+unsigned long long* cyr_trace_buffer();  // device alias of the trace block or null
+int cyr_launch_latency_bench(int which, int iters, long long* cycles, double* sink);

@@ -27,13 +27,14 @@
 
 namespace cyr {
 
-constexpr int kTreeThreads = 256;  // parents per work item
+constexpr int kTreeThreads = 256;  // max parents per work item (= threads per CTA)
 constexpr int kMaxLevels = 16;
 
 struct TreeParams {
   const int32_t* codebook;
   int16_t* out;
   int S, E, cap, M, epad;
+  int np_item;                       // parents per work item (= blockDim.x)
   long long nodes_per_slot;
   int blocks_per_slot;
   int level_blocks[kMaxLevels + 1];  // prefix over parent levels t = 0..M-1
@@ -49,7 +50,8 @@ template <int CH>  // 16-byte granules per record (Epad / 8)
 __global__ void __launch_bounds__(kTreeThreads, 2) tree_kernel(const TreeParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int R = p.cap + 1;
-  const size_t stage_bytes = (size_t)kTreeThreads * R * CH * 16;
+  const int NP = p.np_item;
+  const size_t stage_bytes = (size_t)NP * R * CH * 16;
   const int tid = threadIdx.x;
   const long long items = (long long)p.S * p.blocks_per_slot;
   int it = 0;
@@ -61,12 +63,12 @@ __global__ void __launch_bounds__(kTreeThreads, 2) tree_kernel(const TreeParams 
     const int bw = (int)(w % p.blocks_per_slot);
     int t = 0;
     while (bw >= p.level_blocks[t + 1]) ++t;
-    const long long p0 = (long long)(bw - p.level_blocks[t]) * kTreeThreads;
-    const int np = (int)min((long long)kTreeThreads, p.level_parents[t] - p0);
+    const long long p0 = (long long)(bw - p.level_blocks[t]) * NP;
+    const int np = (int)min((long long)NP, p.level_parents[t] - p0);
 
     if (tid == 0) bulk_wait_read<1>();  // the store issued two items ago released stage
     // this slot's codebook as int16 records: book[k][granule]
-    for (int idx = tid; idx < R * CH * 8; idx += kTreeThreads) {
+    for (int idx = tid; idx < R * CH * 8; idx += NP) {
       const int k = idx / (CH * 8), e = idx % (CH * 8);
       const int v = (e < p.E) ? p.codebook[((long long)s * R + k) * p.E + e] : 0;
       reinterpret_cast<int16_t*>(book)[idx] = (int16_t)v;
@@ -77,10 +79,11 @@ __global__ void __launch_bounds__(kTreeThreads, 2) tree_kernel(const TreeParams 
       uint4 cum[CH];
 #pragma unroll
       for (int c = 0; c < CH; ++c) cum[c] = make_uint4(0, 0, 0, 0);
-      long long q = p0 + tid;
+      unsigned q = (unsigned)(p0 + tid);  // < (cap+1)^(M-1) <= 2^31 (host-checked)
       for (int d = 0; d < t; ++d) {
-        const int k = (int)(q % R);
-        q /= R;
+        const unsigned nq = q / (unsigned)R;
+        const int k = (int)(q - nq * (unsigned)R);
+        q = nq;
 #pragma unroll
         for (int c = 0; c < CH; ++c) cum[c] = vadd16(cum[c], book[k * CH + c]);
       }
@@ -103,15 +106,15 @@ __global__ void __launch_bounds__(kTreeThreads, 2) tree_kernel(const TreeParams 
 template <int CH>
 int launch_tree_t(const TreeParams& p, int sm_count, cudaStream_t stream) {
   const int R = p.cap + 1;
-  const size_t smem = 2 * (size_t)kTreeThreads * R * CH * 16 + 2 * (size_t)R * CH * 16;
+  const size_t smem = 2 * (size_t)p.np_item * R * CH * 16 + 2 * (size_t)R * CH * 16;
   if (smem > 227 * 1024) return CYR_UNSUPPORTED;
   if (cudaFuncSetAttribute(tree_kernel<CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)
     return CYR_CUDA_ERROR;
   const long long items = (long long)p.S * p.blocks_per_slot;
-  const int per_sm = smem <= 113 * 1024 ? 2 : 1;
+  const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (227 * 1024) / (smem + 1024)));
   const long long grid = std::min<long long>(items, (long long)sm_count * per_sm);
-  tree_kernel<CH><<<(unsigned)grid, kTreeThreads, smem, stream>>>(p);
+  tree_kernel<CH><<<(unsigned)grid, p.np_item, smem, stream>>>(p);
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
 }
 
@@ -130,12 +133,20 @@ int cyr_launch_tree(const int32_t* codebook, int S, int E, int cap, int M, int16
   p.M = M;
   p.epad = (E + 7) / 8 * 8;
   const long long R = cap + 1;
+  long long top = 1;
+  for (int t = 0; t < M - 1; ++t) top *= R;
+  if (top > (1ll << 31)) return CYR_UNSUPPORTED;  // parent indices are 32-bit
+  // small batches (the single-slot latency path) use 64-parent items so the
+  // tree spreads over all SMs; large batches use 256-parent items
+  long long big_items = 0;
+  for (long long t = 0, q = 1; t < M; ++t, q *= R) big_items += (q + 255) / 256;
+  p.np_item = (big_items * S < 2ll * sm_count) ? 64 : cyr::kTreeThreads;
   long long parents = 1, nodes = 0;
   p.level_blocks[0] = 0;
   for (int t = 0; t < M; ++t) {
     p.level_parents[t] = parents;
     p.child_off[t] = nodes;
-    const long long blocks = (parents + cyr::kTreeThreads - 1) / cyr::kTreeThreads;
+    const long long blocks = (parents + p.np_item - 1) / p.np_item;
     if (p.level_blocks[t] + blocks > (1ll << 30)) return CYR_UNSUPPORTED;
     p.level_blocks[t + 1] = p.level_blocks[t] + (int)blocks;
     nodes += parents * R;

@@ -36,6 +36,15 @@ def _cuda():
 
 
 # ----------------------------------------------------------------- K3 exact
+def test_lean_sqrt_is_correctly_rounded():
+    import ctypes
+    from paper_2506_00167_b200 import _native
+    bad = ctypes.c_int64(-1)
+    _native.check(_native.lib().cyr_selftest_sqrt(1 << 26, 20261018, ctypes.byref(bad)))
+    assert bad.value == 0
+
+
+
 def test_enforcer_corpus_bit_exact(golden):
     n = 0
     for b, caps, dem, m_hat, nu, deg, grants in golden.enforcer_groups():
@@ -171,6 +180,53 @@ def test_codebooks_match_reference(golden, name, mode, precision):
                   None if eps is None else torch.from_numpy(eps).cuda())
     eng.check()
     assert np.array_equal(out.cpu().numpy(), books)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("name", CONFIGS)
+def test_single_slot_fused_path(golden, name, precision):
+    """S*cap <= 8: K2 runs as a thread-block cluster fused with K3 and the
+    host path reads/writes mapped pinned pages (no copy nodes)."""
+    cfg = golden.config(name)
+    agent = cfg.agent()
+    pol = DevicePolicy(agent.actor, precision)
+    cap = cfg.meta["cap"]
+    per_call = max(1, 8 // cap)
+    for mode in ("det", "sto"):
+        books = []
+        for s0 in range(0, 16, per_call):
+            eps = None if mode == "det" else cfg["eps"][s0:s0 + per_call]
+            got, _ = build_codebooks_host(pol, cfg.cell, cfg["alloc"][s0:s0 + per_call], eps)
+            books.append(got)
+        sub = golden.config(name)
+        got = np.concatenate(books)
+        want = cfg[f"{mode}/codebook"][:16]
+        flagged = _near_tie_rows(cfg, mode, NEAR_TIE[precision])
+        for s, j in zip(*np.nonzero((got[:, 1:] != want[:, 1:]).any(axis=2))):
+            assert (int(s), int(j)) in flagged, f"{name}/{mode}: slot {s} branch {j + 1}"
+        # the device-pointer variant of the same path
+        eng = CodebookEngine(pol, cfg.cell, max_slots=per_call)
+        out = eng.run(torch.from_numpy(cfg["alloc"][:per_call]).cuda(),
+                      None if mode == "det" else torch.from_numpy(cfg["eps"][:per_call]).cuda())
+        eng.check()
+        del sub
+
+
+def test_cluster_actor_logits(golden):
+    from paper_2506_00167_b200 import _native
+    for name in ("cfg1", "cfg2", "cfg5"):
+        cfg = golden.config(name)
+        pol = DevicePolicy(cfg.agent().actor, "fp32")
+        cap, e = cfg.meta["cap"], cfg.meta["num_embb"]
+        raw = torch.empty((cap, 2 * e), dtype=torch.float32, device="cuda")
+        alloc = torch.from_numpy(cfg["alloc"][:1]).cuda()
+        _native.check(_native.lib().cyr_actor_forward_device(
+            pol.handle, alloc.data_ptr(), 1, cfg.meta["total_scs"], cap, raw.data_ptr(),
+            _native.stream_handle()))
+        got = raw.double().cpu().numpy()
+        want = cfg["det/raw"][0].T
+        scale = np.abs(want).max(axis=1, keepdims=True)
+        assert float((np.abs(got - want) / scale).max()) <= LOGIT_TOL["fp32"]
 
 
 def test_drop_in_build_codebook_consumes_streams_like_reference(golden):
