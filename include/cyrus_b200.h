@@ -152,14 +152,14 @@ int cyr_tree_expand_device(const int32_t* codebook, int32_t S, int32_t E, int32_
                            int32_t M, int16_t* node_state, void* stream);
 
 /* ---- diagnostics ---------------------------------------------------------- */
-/* The projection's lean correctly-rounded sqrt against IEEE __dsqrt_rn on n
- * log-uniform / near-midpoint inputs; *mismatches receives the count.
- * Synchronous. */
-int cyr_selftest_sqrt(int64_t n, uint64_t seed, int64_t* mismatches);
 /* Cycles for `iters` dependent steps of an fp64 building block (one warp):
- * 0 DFMA, 1 DMUL, 2 lean sqrt, 3 __dsqrt_rn, 4 __ddiv_rn, 5 FFMA,
- * 6 coupled-bisection body, 7 SHFL, 8 vote.all, 9 MUFU.RSQ64H. */
+ * 0 DFMA, 1 DMUL, 2 __dsqrt_rn*c, 3 __dsqrt_rn+1, 4 __ddiv_rn, 5 FFMA,
+ * 6 coupled-bisection body, 7 SHFL, 8 vote.all, 9 MUFU.RSQ64H,
+ * 10 one coupled_bisection call. */
 int cyr_selftest_latency(int32_t which, int32_t iters, int64_t* cycles);
+/* Event-to-event time of an empty kernel launch (cluster of `cluster` CTAs
+ * when > 1), averaged over reps. */
+int cyr_selftest_launch(int32_t cluster, int32_t reps, int64_t* ns_per_launch);
 /* Phase timestamps (%globaltimer, ns) of the last latency-path launch when
  * the process runs with CYR_TRACE=1; zeros otherwise.  n <= 64. */
 int cyr_debug_trace(int64_t* out, int32_t n);

@@ -13,6 +13,7 @@ import argparse
 import os
 import subprocess
 import sys
+import sysconfig
 from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
@@ -66,7 +67,31 @@ def build(force: bool = False, verbose: bool = False) -> str:
         list(pool.map(run, jobs))
     if force or jobs or _stale(LIB, objs):
         run([nvcc, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static"])
+    build_fastpath(force=force, verbose=verbose)
     return LIB
+
+
+FASTPATH_SRC = os.path.join(CSRC, "fastpath.c")
+FASTPATH = os.path.join(PKG, "_fastpath" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
+
+
+def build_fastpath(force: bool = False, verbose: bool = False) -> str:
+    """CPython module for the single-slot drop-in call: links the C-ABI
+    library and numpy's libnpyrandom.a (bit-identical branch-noise draws)."""
+    import numpy
+    npyrandom = os.path.join(os.path.dirname(numpy.__file__), "random", "lib", "libnpyrandom.a")
+    deps = [FASTPATH_SRC, LIB, os.path.join(INCLUDE, "cyrus_b200.h")]
+    if not force and not _stale(FASTPATH, deps):
+        return FASTPATH
+    cmd = ["gcc", "-O2", "-shared", "-fPIC", "-std=c11", f"-I{sysconfig.get_paths()['include']}",
+           f"-I{INCLUDE}", FASTPATH_SRC, f"-L{PKG}", "-lcyrus_b200", "-Wl,-rpath,$ORIGIN",
+           npyrandom, "-lm", "-o", FASTPATH]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"fastpath build failed: {' '.join(cmd)}\n{res.stderr}")
+    if verbose:
+        sys.stderr.write(res.stderr)
+    return FASTPATH
 
 
 if __name__ == "__main__":

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <ctime>
 #include <map>
 #include <string>
 #include <tuple>
@@ -50,6 +51,14 @@ unsigned long long* g_trace_host = nullptr;
 unsigned long long* g_trace_dev = nullptr;
 
 }  // namespace
+
+static inline void host_stamp(int k) {
+  if (g_trace_host != nullptr) {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    g_trace_host[48 + k] = (unsigned long long)ts.tv_sec * 1000000000ull + ts.tv_nsec;
+  }
+}
 
 unsigned long long* cyr_trace_buffer() {
   static const bool on = [] {
@@ -92,6 +101,14 @@ struct cyr_policy {
   int32_t* pin_cb = nullptr;
   int32_t* pin_status = nullptr;
   std::map<std::tuple<int, int, int, int>, cudaGraphExec_t> graphs;
+  // single-slot fused launches, replayed as graphs with per-call parameters
+  struct FusedGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t node = nullptr;
+    cudaKernelNodeParams kp{};
+  };
+  std::map<std::tuple<int, int, int, int>, FusedGraph> fused;
 };
 
 namespace {
@@ -131,6 +148,11 @@ int upload(cyr_policy* p, const double* blob) {
 void release_host_path(cyr_policy* p) {
   for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
   p->graphs.clear();
+  for (auto& kv : p->fused) {
+    cudaGraphExecDestroy(kv.second.exec);
+    cudaGraphDestroy(kv.second.graph);
+  }
+  p->fused.clear();
   cudaFree(p->alloc_d);
   cudaFree(p->eps_d);
   cudaFree(p->raw_d);
@@ -424,20 +446,68 @@ int cyr_codebook_host(cyr_policy* p, const int32_t* alloc, const double* eps, in
   if (fused) {
     // latency path: ONE cluster launch (K2 + K3), inputs by value in the
     // launch parameters, codebook + status written straight to mapped pages
+    host_stamp(0);
     cyr::SlotInline inl;
     std::memcpy(inl.alloc, alloc, (size_t)S * E * 4);
     if (!det) std::memcpy(inl.eps, eps, (size_t)S * cap * E * 8);
     cudaStream_t st = p->stream;
-    CYR_CUDA(cudaEventRecord(p->ev0, st));
-    int lrc = cyr_launch_slot_fused(p->precision, p->desc, p->blob_d, nullptr, eps, S, E, N, L,
-                                    cap, p->cb_d, reinterpret_cast<int32_t*>(dev(p->pin_cb)),
-                                    reinterpret_cast<int32_t*>(dev(p->pin_status)), st, &inl);
-    if (lrc != CYR_OK) {
-      if (lrc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
-      return lrc;
+    static const bool use_graph = [] {
+      const char* e = getenv("CYR_SLOT_GRAPH");
+      return !(e != nullptr && e[0] == '0');
+    }();
+    auto launch = [&](cudaStream_t s) {
+      return cyr_launch_slot_fused(p->precision, p->desc, p->blob_d, nullptr, eps, S, E, N, L,
+                                   cap, p->cb_d, reinterpret_cast<int32_t*>(dev(p->pin_cb)),
+                                   reinterpret_cast<int32_t*>(dev(p->pin_status)), s, &inl);
+    };
+    if (!use_graph) {
+      CYR_CUDA(cudaEventRecord(p->ev0, st));
+      const int lrc = launch(st);
+      if (lrc != CYR_OK) {
+        if (lrc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+        return lrc;
+      }
+      CYR_CUDA(cudaEventRecord(p->ev1, st));
+    } else {
+      auto fit = p->fused.find(key);
+      if (fit == p->fused.end()) {
+        cyr_policy::FusedGraph fg;
+        CYR_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+        cudaEventRecordWithFlags(p->ev0, st, cudaEventRecordExternal);
+        const int lrc = launch(st);
+        cudaEventRecordWithFlags(p->ev1, st, cudaEventRecordExternal);
+        CYR_CUDA(cudaStreamEndCapture(st, &fg.graph));
+        if (lrc != CYR_OK) {
+          cudaGraphDestroy(fg.graph);
+          return lrc;
+        }
+        size_t n = 0;
+        CYR_CUDA(cudaGraphGetNodes(fg.graph, nullptr, &n));
+        std::vector<cudaGraphNode_t> nodes(n);
+        CYR_CUDA(cudaGraphGetNodes(fg.graph, nodes.data(), &n));
+        for (cudaGraphNode_t nd : nodes) {
+          cudaGraphNodeType t;
+          CYR_CUDA(cudaGraphNodeGetType(nd, &t));
+          if (t == cudaGraphNodeTypeKernel) fg.node = nd;
+        }
+        if (!fg.node) return CYR_CUDA_ERROR;
+        CYR_CUDA(cudaGraphKernelNodeGetParams(fg.node, &fg.kp));
+        cudaError_t e = cudaGraphInstantiate(&fg.exec, fg.graph, 0);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate(fused)");
+        fit = p->fused.emplace(key, fg).first;
+      }
+      // new inputs: same ActorLaunch (the node's stored copy), fresh SlotInline
+      cudaKernelNodeParams kp = fit->second.kp;
+      void* args[2] = {kp.kernelParams[0], &inl};
+      kp.kernelParams = args;
+      host_stamp(1);
+      CYR_CUDA(cudaGraphExecKernelNodeSetParams(fit->second.exec, fit->second.node, &kp));
+      host_stamp(2);
+      CYR_CUDA(cudaGraphLaunch(fit->second.exec, st));
+      host_stamp(3);
     }
-    CYR_CUDA(cudaEventRecord(p->ev1, st));
     CYR_CUDA(cudaEventSynchronize(p->ev1));
+    host_stamp(4);
     const int32_t code = *reinterpret_cast<volatile int32_t*>(p->pin_status);
     if (code != CYR_OK) return code;
     std::memcpy(codebook, p->pin_cb, (size_t)S * (cap + 1) * E * 4);
@@ -551,22 +621,6 @@ int cyr_tree_expand_device(const int32_t* codebook, int32_t S, int32_t E, int32_
   return rc;
 }
 
-int cyr_selftest_sqrt(int64_t n, uint64_t seed, int64_t* mismatches) {
-  if (n < 0 || !mismatches) return CYR_BAD_ARG;
-  unsigned long long* d = nullptr;
-  CYR_CUDA(cudaMalloc(&d, sizeof(unsigned long long)));
-  CYR_CUDA(cudaMemset(d, 0, sizeof(unsigned long long)));
-  int rc = cyr_launch_sqrt_selftest((long long)n, (unsigned long long)seed, d, nullptr);
-  unsigned long long h = 0;
-  if (rc == CYR_OK) {
-    cudaError_t e = cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) rc = cuda_fail(e, "selftest copy");
-  }
-  cudaFree(d);
-  *mismatches = (int64_t)h;
-  return rc;
-}
-
 int cyr_debug_trace(int64_t* out, int32_t n) {
   if (!out || n < 0) return CYR_BAD_ARG;
   for (int i = 0; i < n && i < 64; ++i)
@@ -590,6 +644,31 @@ int cyr_selftest_latency(int32_t which, int32_t iters, int64_t* cycles) {
   cudaFree(sink);
   *cycles = (int64_t)h;
   return rc;
+}
+
+int cyr_selftest_launch(int32_t cluster, int32_t reps, int64_t* ns_per_launch) {
+  if (!ns_per_launch || reps < 1) return CYR_BAD_ARG;
+  cudaStream_t st;
+  CYR_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  cudaEvent_t a, b;
+  CYR_CUDA(cudaEventCreate(&a));
+  CYR_CUDA(cudaEventCreate(&b));
+  double total = 0;
+  for (int i = 0; i < reps + 5; ++i) {
+    CYR_CUDA(cudaEventRecord(a, st));
+    const int rc = cyr_launch_empty(cluster, st);
+    if (rc != CYR_OK) return rc;
+    CYR_CUDA(cudaEventRecord(b, st));
+    CYR_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    CYR_CUDA(cudaEventElapsedTime(&ms, a, b));
+    if (i >= 5) total += ms;
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaStreamDestroy(st);
+  *ns_per_launch = (int64_t)(total * 1e6 / reps);
+  return CYR_OK;
 }
 
 }  // extern "C"

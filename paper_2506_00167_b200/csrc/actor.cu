@@ -308,6 +308,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
             for (int c = 0; c < C; ++c) acc[k][c] = fma(w[k][q], x[c], acc[k][c]);
         }
       }
+      if (o0 == g + G * warp) trace_stamp(tr, 24 + 2 * l);
 #pragma unroll
       for (int k = 0; k < kLatOW; ++k)
 #pragma unroll
@@ -340,6 +341,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
         }
       }
     }
+    trace_stamp(tr, 25 + 2 * l);
     cluster.sync();
     trace_stamp(tr, 2 + l);
   }
@@ -513,4 +515,28 @@ int cyr_launch_slot_fused(int precision, const cyr::ActorDesc& desc, const void*
                 : cyr::launch_actor_cluster<float, 4, true>(p, G, stream, inl);
   return fp64 ? cyr::launch_actor_cluster<double, 8, true>(p, G, stream, inl)
               : cyr::launch_actor_cluster<float, 8, true>(p, G, stream, inl);
+}
+
+namespace cyr {
+__global__ void empty_kernel(int* sink) {
+  if (sink != nullptr && threadIdx.x == 0) *sink = 1;
+}
+}  // namespace cyr
+
+// launch-latency probe: an empty kernel, optionally as a cluster of 8
+int cyr_launch_empty(int cluster, cudaStream_t stream) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(cluster > 1 ? cluster : 1);
+  cfg.blockDim = dim3(256);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster > 1 ? cluster : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = cluster > 1 ? 1 : 0;
+  int* null_sink = nullptr;
+  return cudaLaunchKernelEx(&cfg, cyr::empty_kernel, null_sink) == cudaSuccess ? CYR_OK
+                                                                                : CYR_CUDA_ERROR;
 }

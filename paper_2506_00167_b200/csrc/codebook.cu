@@ -143,43 +143,9 @@ __global__ void __launch_bounds__(256) apportion_kernel(
   if (lane == 0 && margin_out) margin_out[r] = margin;
 }
 
-// ------------------------------------------------------------ self-test
-// sqrt_pos vs the IEEE __dsqrt_rn: half the inputs log-uniform over
-// [1e-300, 1e300], half near rounding midpoints (x = y*next(y) +- 1 ulp).
-__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
-  z += 0x9e3779b97f4a7c15ull;
-  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-  return z ^ (z >> 31);
-}
-
-__global__ void sqrt_selftest_kernel(long long n, unsigned long long seed,
-                                     unsigned long long* mismatches) {
-  unsigned long long bad = 0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const unsigned long long r = mix64(seed ^ (unsigned long long)i);
-    double x;
-    if (i & 1) {
-      // log-uniform positive normal
-      const double u = (double)(r >> 11) * (1.0 / 9007199254740992.0);
-      x = exp2(-996.0 + 1992.0 * u);
-    } else {
-      const double u = (double)(r >> 11) * (1.0 / 9007199254740992.0);
-      const double y = exp2(-490.0 + 980.0 * u);
-      const double yn = __longlong_as_double(__double_as_longlong(y) + 1);
-      x = __dmul_rn(y, yn);
-      const long long d = (long long)((r >> 3) & 3) - 1;  // -1, 0, +1, +2 ulps
-      x = __longlong_as_double(__double_as_longlong(x) + d);
-    }
-    if (__double_as_longlong(sqrt_pos(x)) != __double_as_longlong(__dsqrt_rn(x))) ++bad;
-  }
-  if (bad) atomicAdd(mismatches, bad);
-}
-
 // ------------------------------------------------- latency microbenchmark
 // Cycles per dependent step of the fp64 building blocks of the latency path
-// (one warp, clock64): 0 DFMA, 1 DMUL, 2 sqrt_pos, 3 __dsqrt_rn, 4 __ddiv_rn,
+// (one warp, clock64): 0 DFMA, 1 DMUL, 2-3 __dsqrt_rn, 4 __ddiv_rn,
 // 5 FFMA, 6 coupled-loop body, 7 shfl.bfly.b32, 8 __all_sync, 9 MUFU.RSQ64H.
 template <int W>
 __global__ void latency_bench_kernel(int iters, long long* cycles, double* sink) {
@@ -191,13 +157,13 @@ __global__ void latency_bench_kernel(int iters, long long* cycles, double* sink)
     switch (W) {
       case 0: x = __fma_rn(x, y, z); break;
       case 1: x = __dmul_rn(x, y); break;
-      case 2: x = sqrt_pos(x) + 1.0; break;
+      case 2: x = __dsqrt_rn(x) * 1.0000001; break;
       case 3: x = __dsqrt_rn(x) + 1.0; break;
       case 4: x = __ddiv_rn(y, x) + 1.0; break;
       case 5: f = __fmaf_rn(f, 0.9999f, 1e-4f); break;
       case 6: {
         const double mid = __dmul_rn(x, y);
-        const double root = sqrt_pos(mid);
+        const double root = __dsqrt_rn(mid);
         const bool up = __double_as_longlong(mid) <= 0x3ff0000000000000ll;
         x = up ? root : x;
         y = up ? y : root;
@@ -206,6 +172,13 @@ __global__ void latency_bench_kernel(int iters, long long* cycles, double* sink)
       }
       case 7: f = __int_as_float(__shfl_xor_sync(kFull, __float_as_int(f), 1)) + 1.0f; break;
       case 8: z += __all_sync(kFull, x > 0.0) ? 1.0 : 0.0; x = x + z * 1e-300; break;
+      case 10: {  // the real coupled loop: ~45 steps per call
+        double lo[1] = {0.5 + threadIdx.x * 1e-6 + i * 1e-9}, hi[1] = {2.0};
+        const long long t[1] = {0x3ff3c0ca4283de1bll};  // 1.2345
+        const bool b[1] = {threadIdx.x < 4};
+        z += coupled_bisection<1>(lo, hi, t, b, 4) + lo[0];
+        break;
+      }
       case 9: {
         double r;
         asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
@@ -262,17 +235,12 @@ int cyr_launch_enforce(const double* b, const double* caps, const double* demand
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
 }
 
-int cyr_launch_sqrt_selftest(long long n, unsigned long long seed, unsigned long long* mismatches,
-                             cudaStream_t stream) {
-  cyr::sqrt_selftest_kernel<<<592, 256, 0, stream>>>(n, seed, mismatches);
-  return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
-}
 
 int cyr_launch_latency_bench(int which, int iters, long long* cycles, double* sink) {
   switch (which) {
 #define CYR_LB(W) case W: cyr::latency_bench_kernel<W><<<1, 32>>>(iters, cycles, sink); break;
     CYR_LB(0) CYR_LB(1) CYR_LB(2) CYR_LB(3) CYR_LB(4) CYR_LB(5) CYR_LB(6) CYR_LB(7) CYR_LB(8)
-    CYR_LB(9)
+    CYR_LB(9) CYR_LB(10)
 #undef CYR_LB
     default: return CYR_BAD_ARG;
   }

@@ -131,6 +131,18 @@ __device__ __forceinline__ void trace_stamp(unsigned long long* buf, int k) {
   }
 }
 
+// per-warp variant (lane 0 of any warp) and a raw value slot
+__device__ __forceinline__ void trace_stamp_warp(unsigned long long* buf, int k) {
+  if (buf != nullptr && (threadIdx.x & 31) == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    buf[k] = t;
+  }
+}
+__device__ __forceinline__ void trace_value(unsigned long long* buf, int k, unsigned long long v) {
+  if (buf != nullptr && (threadIdx.x & 31) == 0) buf[k] = v;
+}
+
 // ---------------------------------------------------------- shared structs
 struct LayerDesc {
   int in, out, out_pad;   // Wt is [in][out_pad], row bytes multiple of 16
@@ -180,7 +192,6 @@ int cyr_launch_apportion(const double* m_hat, const double* caps, const int64_t*
                          cudaStream_t stream);
 int cyr_launch_tree(const int32_t* codebook, int S, int E, int cap, int M, int16_t* out,
                     int sm_count, cudaStream_t stream);
-int cyr_launch_sqrt_selftest(long long n, unsigned long long seed, unsigned long long* mismatches,
-                             cudaStream_t stream);
 unsigned long long* cyr_trace_buffer();  // device alias of the trace block or null
 int cyr_launch_latency_bench(int which, int iters, long long* cycles, double* sink);
+int cyr_launch_empty(int cluster, cudaStream_t stream);

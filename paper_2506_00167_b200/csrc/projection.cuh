@@ -28,34 +28,6 @@
 
 namespace cyr {
 
-// Correctly rounded sqrt for positive, normal, finite x — the only inputs
-// the projection produces (bisection brackets, seat counts a(a+1)).  The
-// approximate reciprocal root (MUFU.RSQ64H) is refined by two coupled Newton
-// steps to well inside one ulp; the residual x - g*g is then exact (one
-// FMA), and comparing it with g*ulp decides between g and its neighbours
-// exactly (a square root of a double is never a rounding midpoint).  Saves
-// the range checks and slow-path branch of the general IEEE sqrt on the
-// serial bisection chain; tests/test_gpu_parity.py checks it against
-// __dsqrt_rn on 2^26 log-uniform and near-midpoint inputs.
-__device__ __forceinline__ double sqrt_pos(double x) {
-  double r;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double g = __dmul_rn(x, r);
-  double h = __dmul_rn(0.5, r);
-  double e = __fma_rn(-g, h, 0.5);
-  g = __fma_rn(g, e, g);
-  h = __fma_rn(h, e, h);
-  e = __fma_rn(-g, h, 0.5);
-  g = __fma_rn(g, e, g);
-  h = __fma_rn(h, e, h);
-  const double res = __fma_rn(-g, g, x);  // exact
-  const double up = __longlong_as_double(__double_as_longlong(g) + 1);
-  const double dn = __longlong_as_double(__double_as_longlong(g) - 1);
-  if (res > __dmul_rn(g, __dsub_rn(up, g))) return up;
-  if (res <= -__dmul_rn(g, __dsub_rn(g, dn))) return dn;
-  return g;
-}
-
 // a / b for b positive, normal and finite.  A zero dividend (padding lanes,
 // zero-mass users) would send __ddiv_rn down its slow path and stall the
 // whole warp; 0 / b is exactly +0, so such lanes divide a dummy and select 0.
@@ -267,7 +239,7 @@ __device__ __forceinline__ void kl_finish(const Row& r, int E, double& m, double
   m = 0.0;
   nu = 0.0;
   if (r.bis) {
-    nu = __dmul_rn(sqrt_pos(r.lo), sqrt_pos(r.hi));
+    nu = __dmul_rn(__dsqrt_rn(r.lo), __dsqrt_rn(r.hi));
     m = in ? fmin(r.c, div_or_zero(r.b, nu)) : 0.0;
   } else if (r.degen) {
     const bool pos = lane_pos(r, E);
@@ -282,7 +254,7 @@ __device__ __forceinline__ void kl_finish(const Row& r, int E, double& m, double
 // ------------------------------------------------------------ Huntington-Hill
 __device__ __forceinline__ double seat_prio(double m, int seat) {
   const double a = (double)seat;
-  return div_or_zero(m, sqrt_pos(fmax(__dmul_rn(a, __dadd_rn(a, 1.0)), 1.0)));
+  return div_or_zero(m, __dsqrt_rn(fmax(__dmul_rn(a, __dadd_rn(a, 1.0)), 1.0)));
 }
 
 // (pa, la) strictly before (pb, lb) in the reference order within one phase.
@@ -318,7 +290,8 @@ __device__ __forceinline__ void warp_first_last(double& pa, int& la, bool& oka, 
 // Seats granted to this lane's user; `margin` gets the relative priority gap
 // between the last granted and first refused seat of the same positive phase
 // (+inf otherwise) — the near-tie score of SURVEY §8(c).
-static __device__ int hh_row(double m, double c, int E, long long want, double& margin) {
+static __device__ int hh_row(double m, double c, int E, long long want, double& margin,
+                             int* steps_out = nullptr) {
   const int lane = threadIdx.x & 31;
   const bool in = lane < E;
   const int cnt = in ? (int)ceil(c) : 0;
@@ -370,6 +343,7 @@ static __device__ int hh_row(double m, double c, int E, long long want, double& 
         if (lane == ld) --h;
       } else {
         if (oka && okd) margin = div_or_zero(__dsub_rn(pd, pa), pd);
+        if (steps_out) *steps_out = step + 1;
         break;
       }
     }
@@ -465,6 +439,7 @@ __device__ void codebook_rows(const RawT* raw, const int32_t* alloc, const doubl
       s_t[w] = thr;
       s_bis[w] = row.bis;
     }
+    if (w < 8) trace_stamp_warp(tr, 16 + w);
   }
   __syncthreads();
   if (!mine) return;
@@ -484,8 +459,11 @@ __device__ void codebook_rows(const RawT* raw, const int32_t* alloc, const doubl
   kl_finish(row, E, m, nu);
   trace_stamp(tr, 13);
   double margin;
-  const int g = hh_row(m, row.c, E, (long long)j * L, margin);
+  int hh_steps = 0;
+  const int g = hh_row(m, row.c, E, (long long)j * L, margin, &hh_steps);
   trace_stamp(tr, 14);
+  if (w < 8) trace_value(tr, 40 + w, hh_steps);
+  if (w < 8) trace_value(tr, 56 + w, slot_iters);
   int32_t* book = cb + slot * (cap + 1) * E;
   if (in) {
     book[(long long)j * E + lane] = g;

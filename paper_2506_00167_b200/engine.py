@@ -33,6 +33,11 @@ from . import _native
 from .device import DevicePolicy, policy_for
 from .seeding import substream
 
+try:  # CPython fast path for the single-slot call (built with the library)
+    from . import _fastpath
+except ImportError:  # pragma: no cover - ctypes path below is equivalent
+    _fastpath = None
+
 
 @dataclass
 class Streams:
@@ -88,6 +93,22 @@ def draw_branch_noise(streams, cap: int, num_users: int, slots: int = 1) -> np.n
     return eps
 
 
+_BITGENS: dict = {}
+
+
+def branch_bitgens(streams, cap: int) -> tuple:
+    """bitgen_t addresses of streams.branch[1..cap] (cached per Streams)."""
+    branch = streams.branch
+    entry = _BITGENS.get(id(streams))
+    if entry is not None and entry[0] is branch and all(
+            branch.get(j) is g for j, g in enumerate(entry[1], start=1)):
+        return entry[2]
+    gens = tuple(branch[j] for j in range(1, cap + 1))
+    addrs = tuple(g.bit_generator.ctypes.bit_generator.value for g in gens)
+    _BITGENS[id(streams)] = (branch, gens, addrs)
+    return addrs
+
+
 def build_codebook(agent, schedule, streams, deterministic: bool = False, *,
                    policy: DevicePolicy | None = None, precision: str | None = None) -> Codebook:
     """All branches of one slot on the GPU: actor, head, KL projection,
@@ -95,6 +116,13 @@ def build_codebook(agent, schedule, streams, deterministic: bool = False, *,
     cell = agent.cell
     cap = cell.num_branches
     users = cell.num_embb
+    if _fastpath is not None:
+        pol = policy if policy is not None else policy_for(agent, precision)
+        bitgens = None if deterministic else branch_bitgens(streams, cap)
+        status, columns, gen_ns, dev_ns = _fastpath.codebook(
+            pol.handle.value, schedule.alloc, bitgens, cell.total_scs, cell.urllc_sc_len, users)
+        _native.check(status, "build_codebook")
+        return Codebook(columns=columns, gen_ns=gen_ns, device_ns=dev_ns)
     alloc = np.ascontiguousarray(schedule.alloc, dtype=np.int32)
     if alloc.shape != (users,):
         raise ValueError("input must be (input_dim, batch)")

@@ -36,15 +36,6 @@ def _cuda():
 
 
 # ----------------------------------------------------------------- K3 exact
-def test_lean_sqrt_is_correctly_rounded():
-    import ctypes
-    from paper_2506_00167_b200 import _native
-    bad = ctypes.c_int64(-1)
-    _native.check(_native.lib().cyr_selftest_sqrt(1 << 26, 20261018, ctypes.byref(bad)))
-    assert bad.value == 0
-
-
-
 def test_enforcer_corpus_bit_exact(golden):
     n = 0
     for b, caps, dem, m_hat, nu, deg, grants in golden.enforcer_groups():

@@ -87,3 +87,17 @@ def test_shard_bounds_cover_and_balance():
             sizes = [hi - lo for lo, hi in spans]
             assert max(sizes) - min(sizes) <= 1
             assert max(sizes) <= sharding.max_shard(total, world)
+
+
+def test_fastpath_noise_is_bit_identical_to_generator_draws():
+    from paper_2506_00167_b200 import _fastpath
+    a = engine.make_streams(9, 4)
+    b = engine.make_streams(9, 4)
+    addrs = engine.branch_bitgens(a, 4)
+    for _ in range(3):  # consecutive calls advance each branch stream identically
+        got = _fastpath.draw(addrs, 10)
+        want = [list(b.branch[j].standard_normal(10)) for j in range(1, 5)]
+        assert got == want
+    assert engine.branch_bitgens(a, 4) is addrs          # cached
+    a.branch[2] = b.branch[2]
+    assert engine.branch_bitgens(a, 4)[1] != addrs[1]    # re-derived after a swap
