@@ -280,6 +280,27 @@ def test_tree_node_states_exact(golden, name, slots):
         assert np.array_equal(got[s, :, :e], want)
 
 
+@pytest.mark.parametrize("cap,users,minislots", [(1, 1, 1), (2, 4, 3), (4, 10, 7), (6, 16, 5),
+                                                 (8, 17, 4), (3, 32, 6), (2, 9, 9)])
+@pytest.mark.parametrize("zero_col0", [True, False])
+def test_tree_geometry_envelope(cap, users, minislots, zero_col0):
+    from paper_2506_00167_b200.core import CellConfig
+    rng = np.random.default_rng(cap * 100 + users)
+    slots = 3
+    books = rng.integers(0, 60, size=(slots, cap + 1, users)).astype(np.int32)
+    if zero_col0:
+        books[:, 0] = 0
+    cell = CellConfig(total_scs=120, num_embb=users, urllc_sc_len=60,
+                      minislots=minislots, rb_size=12)
+    states = tree.expand_tree(torch.from_numpy(books).cuda(), cell)
+    torch.cuda.synchronize()
+    got = states.cpu().numpy()
+    for s in range(slots):
+        want = arrival_tree.node_states(books[s], minislots)
+        assert np.array_equal(got[s, :, :users], want)
+        assert (got[s, :, users:] == 0).all()
+
+
 def test_engine_tree_matches_its_codebooks(golden):
     cfg = golden.config("cfg2")
     agent = cfg.agent()
