@@ -67,7 +67,8 @@ const char* cyr_last_error(void);
 
 /* ---- policy: the device-resident actor (sac.SacAgent.actor) ------------- */
 /* Replaces the actor object of sac.py:96-127 as seen by build_codebook.
- * sizes = [E+1, *hidden, 2E]; E <= 32, every width <= 1024. */
+ * sizes = [E+1, *hidden, 2E] (Mode R) or [3E+3, *hidden, 2E] (Mode T);
+ * E <= 32, every width <= 1024. */
 int cyr_policy_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
                       const double* weights_blob, int32_t precision);
 /* Re-publish after an in-place actor update (Adam, neural.py:122-141). */
@@ -150,6 +151,23 @@ int32_t cyr_tree_state_stride(int32_t E);
  * per-user sums); padding lanes are written as zero. */
 int cyr_tree_expand_device(const int32_t* codebook, int32_t S, int32_t E, int32_t cap,
                            int32_t M, int16_t* node_state, void* stream);
+
+/* ---- arrival tree, Mode T (north star: actor on every node's state) ------ */
+/* Policy created with sizes[0] = 3E+3 (a Mode-T actor).  Level tau = 1..M:
+ * for every parent node q of level tau-1 and branch k = 1..cap the actor
+ * sees [n/N (E), k/cap, cum_q/N (E), mcs/mcs_scale (E),
+ * arrivals_q/(M*cap), (tau-1)/M]; the head uses the slot's branch-k noise
+ * eps[s][k-1] (sac.py:351-353 contract); the parent's cap rows are one
+ * coupled enforcement (enforcer.py:201-207, demand k*L); child k's state is
+ * cum_q + grant (k = 0: cum_q).  node_state layout as Mode R.  A Mode-T
+ * actor whose last 2E+2 input columns are zero reproduces Mode R exactly
+ * (the zero-pad bridge).  workspace: cyr_tree_mode_t_workspace_bytes. */
+size_t cyr_tree_mode_t_workspace_bytes(const cyr_policy* policy, int32_t S, int32_t cap,
+                                       int32_t M);
+int cyr_tree_mode_t_device(const cyr_policy* policy, const int32_t* alloc, const int32_t* mcs,
+                           const double* eps, int32_t S, int32_t N, int32_t L, int32_t M,
+                           double mcs_scale, int16_t* node_state, void* workspace,
+                           int32_t* status, void* stream);
 
 /* ---- diagnostics ---------------------------------------------------------- */
 /* Cycles for `iters` dependent steps of an fp64 building block (one warp):

@@ -47,6 +47,9 @@ SIGNATURES = {
     "cyr_tree_num_nodes": (_c_i64, [_c_i32, _c_i32]),
     "cyr_tree_state_stride": (_c_i32, [_c_i32]),
     "cyr_tree_expand_device": (_c_int, [_vp, _c_i32, _c_i32, _c_i32, _c_i32, _vp, _vp]),
+    "cyr_tree_mode_t_workspace_bytes": (ctypes.c_size_t, [_vp, _c_i32, _c_i32, _c_i32]),
+    "cyr_tree_mode_t_device": (_c_int, [_vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i32, _c_i32,
+                                        ctypes.c_double, _vp, _vp, _vp, _vp]),
     "cyr_debug_trace": (_c_int, [_pi64, _c_i32]),
     "cyr_selftest_latency": (_c_int, [_c_i32, _c_i32, _pi64]),
     "cyr_selftest_launch": (_c_int, [_c_i32, _c_i32, _pi64]),

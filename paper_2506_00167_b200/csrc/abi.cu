@@ -80,6 +80,7 @@ struct cyr_policy {
   int precision = CYR_FP32;
   std::vector<int> sizes;
   int E = 0;
+  int mode_t = 0;  // inputs: 0 = [n/N, j/cap] (E+1), 1 = Mode-T node-state features (3E+3)
   size_t elem = 4;
   cyr::ActorDesc desc{};
   void* blob_d = nullptr;
@@ -251,14 +252,17 @@ int cyr_policy_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
   if (!out || !sizes || !weights_blob || n_sizes < 2 || n_sizes - 1 > cyr::kMaxLayers)
     return CYR_BAD_ARG;
   if (precision != CYR_FP32 && precision != CYR_FP64) return CYR_BAD_ARG;
-  const int E = sizes[0] - 1;
-  if (E < 1 || E > cyr::kMaxUsers || sizes[n_sizes - 1] != 2 * E) return CYR_BAD_ARG;
+  if (sizes[n_sizes - 1] % 2 != 0) return CYR_BAD_ARG;
+  const int E = sizes[n_sizes - 1] / 2;
+  if (E < 1 || E > cyr::kMaxUsers) return CYR_BAD_ARG;
+  if (sizes[0] != E + 1 && sizes[0] != 3 * E + 3) return CYR_BAD_ARG;
   for (int i = 0; i < n_sizes; ++i)
     if (sizes[i] < 1 || sizes[i] > cyr::kMaxWidth) return CYR_UNSUPPORTED;
   cyr_policy* p = new cyr_policy();
   p->precision = precision;
   p->sizes.assign(sizes, sizes + n_sizes);
   p->E = E;
+  p->mode_t = sizes[0] == 3 * E + 3;
   p->elem = precision == CYR_FP64 ? 8 : 4;
   p->sm_count = sm_count_of_current_device();
   const int vec = 16 / (int)p->elem;
@@ -366,7 +370,7 @@ int cyr_policy_info(const cyr_policy* p, int32_t* num_users, int32_t* n_sizes, i
 
 int cyr_actor_forward_device(const cyr_policy* p, const int32_t* alloc, int32_t S, int32_t N,
                              int32_t cap, void* raw, void* stream) {
-  if (!p || (S > 0 && (!alloc || !raw)) || N <= 0 || cap < 1) return CYR_BAD_ARG;
+  if (!p || p->mode_t || (S > 0 && (!alloc || !raw)) || N <= 0 || cap < 1) return CYR_BAD_ARG;
   const int rc = cyr_launch_actor(p->precision, p->desc, p->blob_d, alloc, S, p->E, N, cap, raw,
                                   p->sm_count, static_cast<cudaStream_t>(stream));
   if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
@@ -396,7 +400,7 @@ int cyr_codebook_from_raw_device(const cyr_policy* p, const void* raw, const int
 int cyr_codebook_device(const cyr_policy* p, const int32_t* alloc, const double* eps, int32_t S,
                         int32_t N, int32_t L, int32_t* codebook, void* raw_workspace,
                         int32_t* status, void* stream) {
-  if (!p) return CYR_BAD_ARG;
+  if (!p || p->mode_t) return CYR_BAD_ARG;
   int cap = 0;
   int rc = check_geometry(S, p->E, N, L, &cap);
   if (rc != CYR_OK) return rc;
@@ -414,7 +418,7 @@ int cyr_codebook_device(const cyr_policy* p, const int32_t* alloc, const double*
 
 int cyr_codebook_host(cyr_policy* p, const int32_t* alloc, const double* eps, int32_t S,
                       int32_t N, int32_t L, int32_t* codebook, int64_t* device_ns) {
-  if (!p || !alloc || !codebook) return CYR_BAD_ARG;
+  if (!p || p->mode_t || !alloc || !codebook) return CYR_BAD_ARG;
   int cap = 0;
   int rc = check_geometry(S, p->E, N, L, &cap);
   if (rc != CYR_OK) return rc;
@@ -669,6 +673,48 @@ int cyr_selftest_launch(int32_t cluster, int32_t reps, int64_t* ns_per_launch) {
   cudaStreamDestroy(st);
   *ns_per_launch = (int64_t)(total * 1e6 / reps);
   return CYR_OK;
+}
+
+// ---------------------------------------------------------------- Mode T
+size_t cyr_tree_mode_t_workspace_bytes(const cyr_policy* p, int32_t S, int32_t cap, int32_t M) {
+  if (!p || S < 0 || cap < 1 || M < 1) return 0;
+  long long widest = 1;
+  for (int t = 1; t < M; ++t) widest *= (cap + 1);  // parents of the deepest level
+  return (size_t)S * widest * cap * 2 * p->E * p->elem;
+}
+
+int cyr_tree_mode_t_device(const cyr_policy* p, const int32_t* alloc, const int32_t* mcs,
+                           const double* eps, int32_t S, int32_t N, int32_t L, int32_t M,
+                           double mcs_scale, int16_t* node_state, void* workspace,
+                           int32_t* status, void* stream) {
+  if (!p || !p->mode_t) return CYR_BAD_ARG;
+  int cap = 0;
+  int rc = check_geometry(S, p->E, N, L, &cap);
+  if (rc != CYR_OK) return rc;
+  if (M < 1 || M > 10 || mcs_scale <= 0.0) return CYR_BAD_ARG;
+  if (S == 0) return CYR_OK;
+  if (!alloc || !mcs || !node_state || !workspace) return CYR_BAD_ARG;
+  const int R = cap + 1;
+  const int epad = cyr_tree_state_stride(p->E);
+  const long long nodes = cyr_tree_num_nodes(cap, M);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  long long parents = 1, level_off = 0, prev_off = -1;
+  for (int tau = 1; tau <= M; ++tau) {
+    // K2: the actor on every (parent, branch) column of this level
+    rc = cyr_launch_actor_mode_t(p->precision, p->desc, p->blob_d, alloc, mcs, node_state, S,
+                                 p->E, N, cap, M, tau, (int)parents, nodes, prev_off, epad,
+                                 mcs_scale, workspace, p->sm_count, st);
+    if (rc != CYR_OK) break;
+    // K3: one coupled enforcement per parent; writes the children's states
+    rc = cyr_launch_tree_level(p->precision, workspace, alloc, eps, node_state, S, p->E, L, cap,
+                               (int)parents, epad, nodes, prev_off, level_off, status, st);
+    if (rc != CYR_OK) break;
+    prev_off = level_off;
+    level_off += parents * R;
+    parents *= R;
+  }
+  if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+  return rc;
 }
 
 }  // extern "C"

@@ -53,7 +53,44 @@ struct ActorLaunch {
   int32_t* status;
   unsigned long long* trace;  // CYR_TRACE phase stamps (rank 0), or null
   int inline_inputs;          // alloc / eps come from the SlotInline parameter
+  // Mode T (actor on arrival-tree node states), batch kernel only
+  int mode_t;
+  const int16_t* node;        // node states [S][nodes][epad]
+  const int32_t* mcs;         // [S][E]
+  long long nodes_per_slot;
+  long long parent_off;       // node offset of the parent level, -1 for the root
+  int parents, tau, M, epad;
+  double mcs_scale;
 };
+
+// Mode-T actor input for column (slot s, parent q, branch k) — feature i of
+// [n/N (E), k/cap, cum/N (E), mcs/mcs_scale (E), arrivals/(M*cap), (tau-1)/M].
+// With zero weights on the last 2E+2 inputs this is exactly the Mode-R
+// column [n/N, k/cap] (sac.py:344-346): the zero-pad bridge.
+__device__ __forceinline__ double mode_t_feature(const ActorLaunch& p, int col, int i) {
+  const int k = col % p.cap + 1;
+  const int g = col / p.cap;
+  const int s = g / p.parents;
+  const int q = g - s * p.parents;
+  const int E = p.E;
+  if (i < E) return (double)p.alloc[(long long)s * E + i] / (double)p.N;
+  if (i == E) return (double)k / (double)p.cap;
+  if (i <= 2 * E) {
+    if (p.parent_off < 0) return 0.0;
+    const long long rec = (long long)s * p.nodes_per_slot + p.parent_off + q;
+    return (double)p.node[rec * p.epad + (i - E - 1)] / (double)p.N;
+  }
+  if (i <= 3 * E) return (double)p.mcs[(long long)s * E + (i - 2 * E - 1)] / p.mcs_scale;
+  if (i == 3 * E + 1) {
+    int arrivals = 0, x = q;
+    for (int d = 1; d < p.tau; ++d) {
+      arrivals += x % (p.cap + 1);
+      x /= (p.cap + 1);
+    }
+    return (double)arrivals / (double)(p.M * p.cap);
+  }
+  return (double)(p.tau - 1) / (double)p.M;
+}
 
 __host__ __device__ inline int rows_per_stage(const LayerDesc& L, int elem) {
   const int r = kStageBytes / (L.out_pad * elem);
@@ -136,15 +173,20 @@ __global__ void __launch_bounds__(kActorThreads, 1) actor_kernel(const ActorLaun
   if (tid == 0)
     for (int g = 0; g < min(p.stages, total); ++g) issue(g);
 
-  // branch inputs x[:E] = alloc/N, x[E] = j/cap, built in float64 and rounded
-  const int e1 = p.E + 1;
-  for (int idx = tid; idx < e1 * TC; idx += kActorThreads) {
+  // branch inputs x[:E] = alloc/N, x[E] = j/cap (Mode T: node-state
+  // features), built in float64 and rounded to the actor precision
+  const int in0 = p.desc.layer[0].in;
+  for (int idx = tid; idx < in0 * TC; idx += kActorThreads) {
     const int i = idx / TC, c = idx % TC, col = c0 + c;
     double v = 0.0;
     if (col < p.ncols) {
-      const int s = col / p.cap, j = col % p.cap + 1;
-      v = (i < p.E) ? (double)p.alloc[(long long)s * p.E + i] / (double)p.N
-                    : (double)j / (double)p.cap;
+      if (p.mode_t) {
+        v = mode_t_feature(p, col, i);
+      } else {
+        const int s = col / p.cap, j = col % p.cap + 1;
+        v = (i < p.E) ? (double)p.alloc[(long long)s * p.E + i] / (double)p.N
+                      : (double)j / (double)p.cap;
+      }
     }
     act_a[i * TCP + c] = (T)v;
   }
@@ -539,4 +581,38 @@ int cyr_launch_empty(int cluster, cudaStream_t stream) {
   int* null_sink = nullptr;
   return cudaLaunchKernelEx(&cfg, cyr::empty_kernel, null_sink) == cudaSuccess ? CYR_OK
                                                                                 : CYR_CUDA_ERROR;
+}
+
+// Mode-T actor over every (parent, branch) column of level `tau` (batch kernel)
+int cyr_launch_actor_mode_t(int precision, const cyr::ActorDesc& desc, const void* blob,
+                            const int32_t* alloc, const int32_t* mcs, const int16_t* node,
+                            int S, int E, int N, int cap, int M, int tau, int parents,
+                            long long nodes_per_slot, long long parent_off, int epad,
+                            double mcs_scale, void* raw, int sm_count, cudaStream_t stream) {
+  if (S <= 0) return CYR_OK;
+  if (desc.max_width > cyr::kMaxWidth) return CYR_UNSUPPORTED;
+  cyr::ActorLaunch p{};
+  p.desc = desc;
+  p.blob = blob;
+  p.alloc = alloc;
+  p.raw = raw;
+  p.S = S;
+  p.E = E;
+  p.N = N;
+  p.cap = cap;
+  const long long ncols = (long long)S * parents * cap;
+  if (ncols >= (1ll << 31)) return CYR_UNSUPPORTED;
+  p.ncols = (int)ncols;
+  p.mode_t = 1;
+  p.node = node;
+  p.mcs = mcs;
+  p.nodes_per_slot = nodes_per_slot;
+  p.parent_off = parent_off;
+  p.parents = parents;
+  p.tau = tau;
+  p.M = M;
+  p.epad = epad;
+  p.mcs_scale = mcs_scale;
+  if (precision == CYR_FP64) return cyr::launch_actor_typed<double>(p, sm_count, stream);
+  return cyr::launch_actor_typed<float>(p, sm_count, stream);
 }

@@ -21,6 +21,48 @@ __global__ void __launch_bounds__(512) codebook_kernel(
                       margin_out, iters_out, status, s_lo, s_hi, s_t, s_bis);
 }
 
+// ------------------------------------------------------------ Mode-T level
+// One CTA per parent node of level tau-1, one warp per branch k: the
+// parent's cap rows are one coupled enforcement call (a per-node
+// build_codebook, engine.py:97-116, with node-state actor inputs); the
+// grants become the children's states cum_parent + g (k = 0: cum_parent).
+struct TreeIO {
+  const int32_t* alloc;
+  const double* eps;  // [S][cap][E]: the slot's branch-k noise, shared by its nodes
+  int16_t* node;
+  int E, cap, epad, parents;
+  long long nodes_per_slot, parent_off, child_off;
+  __device__ const int32_t* alloc_row(long long group) const {
+    return alloc + (group / parents) * E;
+  }
+  __device__ const double* eps_row(long long, long long group, int j) const {
+    return eps ? eps + ((group / parents) * cap + (j - 1)) * E : nullptr;
+  }
+  __device__ void emit(long long, long long group, int j, int lane, int g, double, double, double,
+                       int) const {
+    const long long s = group / parents, q = group % parents;
+    const long long base = s * nodes_per_slot;
+    int cum = 0;
+    if (lane < E && parent_off >= 0) cum = node[(base + parent_off + q) * epad + lane];
+    const long long first = (base + child_off + q * (cap + 1)) * epad;
+    if (lane < epad) {
+      node[first + (long long)j * epad + lane] = (int16_t)(lane < E ? cum + g : 0);
+      if (j == 1) node[first + lane] = (int16_t)(lane < E ? cum : 0);
+    }
+  }
+};
+
+template <typename RawT>
+__global__ void __launch_bounds__(512) tree_level_kernel(const RawT* __restrict__ raw, TreeIO io,
+                                                         int L, int32_t* __restrict__ status) {
+  __shared__ double s_lo[32], s_hi[32];
+  __shared__ long long s_t[32];
+  __shared__ int s_bis[32];
+  const long long row0 = (long long)blockIdx.x * io.cap;
+  codebook_rows_io<RawT, TreeIO>(raw + row0 * 2 * io.E, row0, io.cap, io.cap, io.E, L, io, status,
+                                 s_lo, s_hi, s_t, s_bis);
+}
+
 // ------------------------------------------------------- standalone enforcer
 // One CTA = one coupled call of up to 256 rows; warps stride over rows in
 // phases 1 and 3 (re-reading b and caps, which stay in L1), warp 0 runs the
@@ -244,5 +286,23 @@ int cyr_launch_latency_bench(int which, int iters, long long* cycles, double* si
 #undef CYR_LB
     default: return CYR_BAD_ARG;
   }
+  return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
+}
+
+int cyr_launch_tree_level(int precision, const void* raw, const int32_t* alloc, const double* eps,
+                          int16_t* node, int S, int E, int L, int cap, int parents, int epad,
+                          long long nodes_per_slot, long long parent_off, long long child_off,
+                          int32_t* status, cudaStream_t stream) {
+  if (S <= 0) return CYR_OK;
+  if (E < 1 || E > cyr::kMaxUsers || cap < 1 || cap > 16) return CYR_UNSUPPORTED;
+  cyr::TreeIO io{alloc, eps, node, E, cap, epad, parents, nodes_per_slot, parent_off, child_off};
+  const long long groups = (long long)S * parents;
+  if (groups >= (1ll << 31)) return CYR_UNSUPPORTED;
+  if (precision == CYR_FP64)
+    cyr::tree_level_kernel<double><<<(unsigned)groups, 32 * cap, 0, stream>>>(
+        static_cast<const double*>(raw), io, L, status);
+  else
+    cyr::tree_level_kernel<float><<<(unsigned)groups, 32 * cap, 0, stream>>>(
+        static_cast<const float*>(raw), io, L, status);
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
 }

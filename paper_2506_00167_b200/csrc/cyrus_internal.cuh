@@ -195,3 +195,12 @@ int cyr_launch_tree(const int32_t* codebook, int S, int E, int cap, int M, int16
 unsigned long long* cyr_trace_buffer();  // device alias of the trace block or null
 int cyr_launch_latency_bench(int which, int iters, long long* cycles, double* sink);
 int cyr_launch_empty(int cluster, cudaStream_t stream);
+int cyr_launch_actor_mode_t(int precision, const cyr::ActorDesc& desc, const void* blob,
+                            const int32_t* alloc, const int32_t* mcs, const int16_t* node,
+                            int S, int E, int N, int cap, int M, int tau, int parents,
+                            long long nodes_per_slot, long long parent_off, int epad,
+                            double mcs_scale, void* raw, int sm_count, cudaStream_t stream);
+int cyr_launch_tree_level(int precision, const void* raw, const int32_t* alloc, const double* eps,
+                          int16_t* node, int S, int E, int L, int cap, int parents, int epad,
+                          long long nodes_per_slot, long long parent_off, long long child_off,
+                          int32_t* status, cudaStream_t stream);

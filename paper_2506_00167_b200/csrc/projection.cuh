@@ -381,24 +381,25 @@ __device__ __forceinline__ void set_status(int32_t* status, int code) {
 
 // ------------------------------------------------------- slot codebooks
 // Head + coupled projection + rounding for `nrows` rows held by this CTA
-// (warp w < nrows owns local row w = global row row0 + w); rows come in
-// whole slots of `cap` (branch j = row % cap + 1, demand j*L), and each slot
-// is one coupled enforcement call (engine.py:108-110).  Every thread of the
-// CTA must call this (it uses __syncthreads); blockDim.x >= 32 * nrows and
-// nrows <= 32.  raw points at local row 0's logits ([row][2E]); alloc, eps,
-// cb and the optional diagnostics are indexed by global slot / row.
-template <typename RawT>
-__device__ void codebook_rows(const RawT* raw, const int32_t* alloc, const double* eps,
-                              long long row0, int nrows, int cap, int E, int L, int32_t* cb,
-                              double* m_out, double* nu_out, double* margin_out,
-                              int32_t* iters_out, int32_t* status, double* s_lo, double* s_hi,
-                              long long* s_t, int* s_bis, unsigned long long* tr = nullptr) {
+// (warp w < nrows owns local row w = global row row0 + w).  Rows come in
+// whole groups of `cap` (branch j = row % cap + 1, demand j*L) and each
+// group is one coupled enforcement call: a slot's branch rows in Mode R
+// (engine.py:108-110), a parent node's branch rows in Mode T.  Every thread
+// of the CTA must call this (it uses __syncthreads); blockDim.x >= 32 *
+// nrows, nrows <= 32, row0 % cap == 0.  raw points at local row 0's logits
+// ([row][2E]).  IO supplies the group's allocation row and the row's noise
+// and consumes the grants (lanes < E) — see SlotIO / the Mode-T TreeIO.
+template <typename RawT, typename IO>
+__device__ void codebook_rows_io(const RawT* raw, long long row0, int nrows, int cap, int E,
+                                 int L, const IO& io, int32_t* status, double* s_lo,
+                                 double* s_hi, long long* s_t, int* s_bis,
+                                 unsigned long long* tr = nullptr) {
   const int w = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const bool in = lane < E;
   const bool mine = w < nrows;
   const long long grow = row0 + w;
-  const long long slot = grow / cap;
+  const long long group = grow / cap;
   const int j = (int)(grow % cap) + 1;
   Row row;
   row.valid = mine;
@@ -406,7 +407,9 @@ __device__ void codebook_rows(const RawT* raw, const int32_t* alloc, const doubl
   row.c = 0.0;
   row.d = 0.0;
   if (mine) {
-    const double n = in ? (double)alloc[slot * E + lane] : 0.0;
+    const int32_t* alloc = io.alloc_row(group);
+    const double* eps = io.eps_row(grow, group, j);
+    const double n = in ? (double)alloc[lane] : 0.0;
     double bval = 0.0;
     if (in) {
       const RawT* rr = raw + (long long)w * 2 * E;
@@ -414,7 +417,7 @@ __device__ void codebook_rows(const RawT* raw, const int32_t* alloc, const doubl
       const double ls = fmin(fmax((double)rr[E + lane], kLogSigmaMin), kLogSigmaMax);
       double a;
       if (eps != nullptr) {
-        const double u = __dadd_rn(mu, __dmul_rn(exp(ls), eps[grow * E + lane]));
+        const double u = __dadd_rn(mu, __dmul_rn(exp(ls), eps[lane]));
         a = tanh(u);
       } else {
         a = tanh(mu);
@@ -443,17 +446,17 @@ __device__ void codebook_rows(const RawT* raw, const int32_t* alloc, const doubl
   }
   __syncthreads();
   if (!mine) return;
-  // phase 2 (lanes = rows, redundantly in every row warp): coupled loop per slot
+  // phase 2 (lanes = rows, redundantly in every row warp): coupled loop per group
   double lo[1] = {lane < nrows ? s_lo[lane] : 0.0};
   double hi[1] = {lane < nrows ? s_hi[lane] : 0.0};
   const long long tt[1] = {lane < nrows ? s_t[lane] : 0};
   const bool bis[1] = {lane < nrows && s_bis[lane] != 0};
   trace_stamp(tr, 11);
-  const int iters = coupled_bisection<1>(lo, hi, tt, bis, cap);  // rows are slot-aligned
+  const int iters = coupled_bisection<1>(lo, hi, tt, bis, cap);  // rows are group-aligned
   trace_stamp(tr, 12);
   row.lo = shfl_d(lo[0], w);
   row.hi = shfl_d(hi[0], w);
-  const int slot_iters = __shfl_sync(kFull, iters, w);
+  const int group_iters = __shfl_sync(kFull, iters, w);
   // phase 3 (warp per row): m_hat, nu, Huntington-Hill
   double m, nu;
   kl_finish(row, E, m, nu);
@@ -463,18 +466,49 @@ __device__ void codebook_rows(const RawT* raw, const int32_t* alloc, const doubl
   const int g = hh_row(m, row.c, E, (long long)j * L, margin, &hh_steps);
   trace_stamp(tr, 14);
   if (w < 8) trace_value(tr, 40 + w, hh_steps);
-  if (w < 8) trace_value(tr, 56 + w, slot_iters);
-  int32_t* book = cb + slot * (cap + 1) * E;
-  if (in) {
-    book[(long long)j * E + lane] = g;
-    if (j == 1) book[lane] = 0;
-    if (m_out) m_out[grow * E + lane] = m;
+  if (w < 8) trace_value(tr, 56 + w, group_iters);
+  io.emit(grow, group, j, lane, g, m, nu, margin, group_iters);
+}
+
+// Mode R: the slot codebook [S][cap+1][E] plus optional diagnostics.
+struct SlotIO {
+  const int32_t* alloc;
+  const double* eps;  // [S][cap][E] or null (deterministic)
+  int32_t* cb;
+  double* m_out;
+  double* nu_out;
+  double* margin_out;
+  int32_t* iters_out;
+  int E, cap;
+  __device__ const int32_t* alloc_row(long long group) const { return alloc + group * E; }
+  __device__ const double* eps_row(long long grow, long long, int) const {
+    return eps ? eps + grow * E : nullptr;
   }
-  if (lane == 0) {
-    if (nu_out) nu_out[grow] = nu;
-    if (margin_out) margin_out[grow] = margin;
+  __device__ void emit(long long grow, long long group, int j, int lane, int g, double m,
+                       double nu, double margin, int iters) const {
+    int32_t* book = cb + group * (cap + 1) * E;
+    if (lane < E) {
+      book[(long long)j * E + lane] = g;
+      if (j == 1) book[lane] = 0;
+      if (m_out) m_out[grow * E + lane] = m;
+    }
+    if (lane == 0) {
+      if (nu_out) nu_out[grow] = nu;
+      if (margin_out) margin_out[grow] = margin;
+      if (iters_out && j == 1) iters_out[group] = iters;
+    }
   }
-  if (iters_out && j == 1 && lane == 0) iters_out[slot] = slot_iters;
+};
+
+template <typename RawT>
+__device__ void codebook_rows(const RawT* raw, const int32_t* alloc, const double* eps,
+                              long long row0, int nrows, int cap, int E, int L, int32_t* cb,
+                              double* m_out, double* nu_out, double* margin_out,
+                              int32_t* iters_out, int32_t* status, double* s_lo, double* s_hi,
+                              long long* s_t, int* s_bis, unsigned long long* tr = nullptr) {
+  const SlotIO io{alloc, eps, cb, m_out, nu_out, margin_out, iters_out, E, cap};
+  codebook_rows_io<RawT, SlotIO>(raw, row0, nrows, cap, E, L, io, status, s_lo, s_hi, s_t, s_bis,
+                                 tr);
 }
 
 }  // namespace cyr

@@ -97,7 +97,7 @@ class DevicePolicy:
     def update(self, actor) -> None:
         """Re-publish after an in-place actor change (same layer sizes)."""
         sizes, blob = flatten_actor(actor)
-        if sizes[0] != self.num_users + 1 or len(sizes) - 1 != self.depth:
+        if sizes[-1] != 2 * self.num_users or len(sizes) - 1 != self.depth:
             raise ValueError("actor shape differs from the published policy")
         _native.check(_native.lib().cyr_policy_update(self.handle, blob.ctypes.data), "update")
 

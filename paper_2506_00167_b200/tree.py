@@ -20,6 +20,11 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native
+from .policy import MlpParams, init_mlp
+
+# engine._synthetic_schedule draws MCS indices from the 6-entry
+# DEFAULT_MCS_TABLE (scheduler.py:32-39): Mode-T features use mcs / 5.
+DEFAULT_MCS_SCALE = 5.0
 
 
 def num_nodes(cap: int, minislots: int) -> int:
@@ -80,3 +85,70 @@ def arrivals(cap: int, minislots: int) -> np.ndarray:
         acc = (acc[:, None] + np.arange(cap + 1)[None, :]).ravel()
         out.append(acc)
     return np.concatenate(out)
+
+
+# ----------------------------------------------------------------- Mode T
+# North star: "walks the arrival tree level by level, and runs the SAC actor
+# network on each node's state (per-UE allocated and already-punctured
+# subcarriers, CQI/MCS, arrivals so far)".  The reference's actor sees only
+# [n/N, j/cap] (sac.py:344-346); Mode T extends the input to
+#     [n/N (E), k/cap, cum/N (E), mcs/5 (E), arrivals/(M*cap), (tau-1)/M]
+# (3E+3) for the decision of mini-slot tau at a parent node with punctured
+# totals `cum` and `arrivals` packets so far.  Each parent's cap branch rows
+# are one coupled enforcement (a per-node build_codebook), child k's state is
+# cum + grant.  A Mode-T actor whose extra 2E+2 input columns are zero is the
+# reference actor at every node (bridge_actor): Mode T then reproduces
+# Mode R exactly, which pins the Mode-T kernels against reference decisions.
+
+def mode_t_sizes(cell, hidden) -> list:
+    e = int(cell.num_embb)
+    return [3 * e + 3, *[int(h) for h in hidden], 2 * e]
+
+
+def make_mode_t_actor(cell, hidden, rng, final_scale: float = 0.01) -> MlpParams:
+    """He-normal Mode-T actor (the init of neural.py:50-63 on 3E+3 inputs)."""
+    return init_mlp(mode_t_sizes(cell, hidden), rng, final_scale=final_scale)
+
+
+def bridge_actor(actor) -> MlpParams:
+    """Mode-T actor equal to `actor` (a reference actor, inputs E+1) on the
+    reference features and blind to the node-state ones (zero columns)."""
+    w0 = np.asarray(actor.weights[0], dtype=np.float64)
+    e = w0.shape[1] - 1
+    padded = np.concatenate([w0, np.zeros((w0.shape[0], 2 * e + 2))], axis=1)
+    return MlpParams([padded] + [np.array(w, dtype=np.float64) for w in actor.weights[1:]],
+                     [np.array(b, dtype=np.float64) for b in actor.biases])
+
+
+def build_tree_mode_t(policy, cell, allocs, mcs, eps=None, mcs_scale: float = DEFAULT_MCS_SCALE,
+                      out=None, workspace=None, status=None, stream=None):
+    """Mode-T arrival tree for S slots on the current stream.
+
+    policy: a DevicePolicy of a Mode-T actor; allocs, mcs: CUDA int32 (S, E);
+    eps: CUDA float64 (S, cap, E) or None.  Returns node states int16
+    (S, nodes, Epad) in the Mode-R layout.
+    """
+    import torch
+    check_tree_geometry(cell)
+    lib = _native.lib()
+    s, e = int(allocs.shape[0]), int(allocs.shape[1])
+    cap, m = cell.num_branches, cell.minislots
+    nodes = num_nodes(cap, m)
+    dev = allocs.device
+    if out is None:
+        out = torch.empty((s, nodes, state_stride(e)), dtype=torch.int16, device=dev)
+    if workspace is None:
+        nbytes = lib.cyr_tree_mode_t_workspace_bytes(policy.handle, s, cap, m)
+        workspace = torch.empty(max(1, nbytes), dtype=torch.uint8, device=dev)
+    own_status = status is None
+    if own_status:
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+    _native.check(lib.cyr_tree_mode_t_device(
+        policy.handle, allocs.data_ptr(), mcs.data_ptr(), None if eps is None else eps.data_ptr(),
+        s, cell.total_scs, cell.urllc_sc_len, m, float(mcs_scale), out.data_ptr(),
+        workspace.data_ptr(), status.data_ptr(), _native.stream_handle(stream)), "mode-T tree")
+    if own_status:
+        code = int(status.item())
+        if code:
+            _native.check(code, "mode-T tree")
+    return out

@@ -317,3 +317,76 @@ def test_engine_tree_matches_its_codebooks(golden):
     assert np.array_equal(leaves.sum(axis=2), np.broadcast_to(arr * 195, leaves.shape[:2]))
     for s in range(16):
         assert np.array_equal(states[s, :, :10], arrival_tree.node_states(books[s], 7))
+
+
+# ------------------------------------------------------------------- Mode T
+def _mode_t_inputs(cfg, slots):
+    alloc = torch.from_numpy(cfg["alloc"][:slots]).cuda()
+    mcs = torch.from_numpy(cfg["mcs"][:slots]).cuda()
+    eps = torch.from_numpy(cfg["eps"][:slots]).cuda()
+    return alloc, mcs, eps
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "desk"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_mode_t_zero_pad_bridge_is_mode_r(golden, name, precision):
+    """Bridge: the Mode-T kernels with a zero-padded
+    reference actor reproduce the Mode-R tree of the Mode-R codebooks exactly."""
+    cfg = golden.config(name)
+    agent = cfg.agent()
+    slots = 6
+    alloc, mcs, eps = _mode_t_inputs(cfg, slots)
+    pol_r = DevicePolicy(agent.actor, precision)
+    pol_t = DevicePolicy(tree.bridge_actor(agent.actor), precision)
+    eng = CodebookEngine(pol_r, cfg.cell, max_slots=slots, with_tree=True)
+    eng.run(alloc, eps)
+    eng.check()
+    got = tree.build_tree_mode_t(pol_t, cfg.cell, alloc, mcs, eps)
+    torch.cuda.synchronize()
+    assert torch.equal(got, eng.node_state[:slots])
+    # and against the reference's own codebooks (punctsim golden), near-tie aside
+    e = cfg.meta["num_embb"]
+    got = got.cpu().numpy()
+    for s in range(slots):
+        want = arrival_tree.node_states(cfg["sto/codebook"][s], cfg.meta["minislots"])
+        if not np.array_equal(got[s, :, :e], want):
+            flagged = _near_tie_rows(cfg, "sto", NEAR_TIE[precision])
+            assert any(fs == s for fs, _ in flagged), f"slot {s} differs without a near-tie"
+
+
+def _taint(margins, cap, threshold):
+    """Per level, nodes whose path crosses a near-tie decision."""
+    r = cap + 1
+    taint, out = np.zeros(1, dtype=bool), []
+    for lvl in margins:
+        child = np.repeat(taint, r).reshape(-1, r)
+        child[:, 1:] |= lvl < threshold
+        taint = child.ravel()
+        out.append(taint)
+    return np.concatenate(out)
+
+
+@pytest.mark.parametrize("name,minislots,precision", [("desk", 3, "fp64"), ("cfg1", 5, "fp64"),
+                                                      ("cfg1", 5, "fp32"), ("cfg2", 3, "fp32")])
+def test_mode_t_matches_oracle(golden, name, minislots, precision):
+    from dataclasses import replace
+    from oracle import mode_t
+    from paper_2506_00167_b200 import substream
+    cfg = golden.config(name)
+    cell = replace(cfg.cell, minislots=minislots)
+    actor = tree.make_mode_t_actor(cell, (64, 64), substream(11, "mode-t"), final_scale=1.0)
+    pol = DevicePolicy(actor, precision)
+    slots = 3
+    alloc, mcs, eps = _mode_t_inputs(cfg, slots)
+    got = tree.build_tree_mode_t(pol, cell, alloc, mcs, eps).cpu().numpy()
+    e = cfg.meta["num_embb"]
+    flagged = 0
+    for s in range(slots):
+        want, margins = mode_t.mode_t_tree(actor.weights, actor.biases, cfg["alloc"][s],
+                                           cfg["mcs"][s], cell.total_scs, cell.urllc_sc_len,
+                                           minislots, cfg["eps"][s], details=True)
+        taint = _taint(margins, cell.num_branches, NEAR_TIE[precision])
+        diff = (got[s, :, :e] != want).any(axis=1)
+        assert not (diff & ~taint).any(), f"slot {s}: nodes differ outside near-tie subtrees"
+        flagged += int(taint.sum())
+    print(f"[mode-T] {name} M={minislots} {precision}: {flagged} nodes under near-ties")

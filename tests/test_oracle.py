@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 from hypothesis import given, settings, strategies as st
 
-from oracle import arrival_tree, mlp, projection, slot
+from oracle import arrival_tree, mlp, mode_t, projection, slot
 
 
 def test_pairwise8_is_numpys_row_sum():
@@ -133,3 +133,22 @@ def test_head_matches_reference_formula():
     eps = np.array([[0.7], [-1.1]])
     a = mlp.head(raw, 2, eps)
     assert np.array_equal(a, np.tanh(raw[:2] + np.exp(np.array([[-20.0], [2.0]])) * eps))
+
+
+@pytest.mark.parametrize("name,minislots", [("desk", 3), ("cfg1", 4)])
+def test_mode_t_oracle_bridge_equals_mode_r(golden, name, minislots):
+    """A Mode-T actor with zero node-state columns is the reference actor at
+    every node, so the Mode-T tree equals the Mode-R tree of the reference's
+    own codebook (golden, from punctsim)."""
+    from paper_2506_00167_b200.tree import bridge_actor
+    cfg = golden.config(name)
+    agent = cfg.agent()
+    bridged = bridge_actor(agent.actor)
+    for s in range(3):
+        for mode in ("det", "sto"):
+            eps = None if mode == "det" else cfg["eps"][s]
+            got = mode_t.mode_t_tree(bridged.weights, bridged.biases, cfg["alloc"][s],
+                                     cfg["mcs"][s], cfg.meta["total_scs"],
+                                     cfg.meta["urllc_sc_len"], minislots, eps)
+            want = arrival_tree.node_states(cfg[f"{mode}/codebook"][s], minislots)
+            assert np.array_equal(got, want)
