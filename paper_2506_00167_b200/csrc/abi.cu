@@ -127,6 +127,11 @@ void pack_blob(const cyr_policy& p, const double* src, std::vector<T>& dst) {
     for (int o = 0; o < L.out; ++o)
       for (int i = 0; i < L.in; ++i)
         dst[L.wr_off + (size_t)o * L.in_pad + i] = (T)src[off + (size_t)o * L.in + i];
+    if (L.wp_off != L.w_off)
+      for (int o = 0; o < L.out; ++o)
+        for (int i = 0; i < L.in; ++i)
+          dst[L.wp_off + ((size_t)(o / 256) * L.in + i) * 256 + o % 256] =
+              (T)src[off + (size_t)o * L.in + i];
     off += (size_t)L.out * L.in;
     for (int o = 0; o < L.out; ++o) dst[L.b_off + o] = (T)src[off + o];
     off += L.out;
@@ -282,6 +287,14 @@ int cyr_policy_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
     off += (size_t)(L.out + vec - 1) / vec * vec;
     L.wr_off = (long long)off;
     off += (size_t)L.out * L.in_pad;
+    L.pw = std::min(L.out_pad, 256);
+    if (L.out_pad > 256) {  // paneled copy for the tiled batch kernel
+      L.pw = 256;
+      L.wp_off = (long long)off;
+      off += (size_t)((L.out_pad + 255) / 256) * L.in * 256;
+    } else {
+      L.wp_off = L.w_off;
+    }
     p->desc.max_width = std::max(p->desc.max_width, std::max(L.in, L.out_pad));
     p->desc.max_rows = std::max(p->desc.max_rows, std::max(L.in_pad, L.out));
   }

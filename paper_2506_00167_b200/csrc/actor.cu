@@ -390,11 +390,9 @@ __global__ void __launch_bounds__(kLatThreads, 1)
   if constexpr (FUSE) {
     // K3 for the slot(s) on rank 0: logits never leave shared memory
     if (g != 0) return;
-    __shared__ double s_lo[32], s_hi[32];
-    __shared__ long long s_t[32];
-    __shared__ int s_bis[32];
+    __shared__ RowScratch sc;
     codebook_rows<T>(raw_s, alloc, eps, 0, p.ncols, p.cap, p.E, p.L, p.cb, nullptr, nullptr,
-                     nullptr, nullptr, p.status, s_lo, s_hi, s_t, s_bis, tr);
+                     nullptr, nullptr, p.status, sc, tr);
     if (p.cb_host != nullptr) {
       __syncthreads();
       const int n = p.S * (p.cap + 1) * p.E;
@@ -435,6 +433,248 @@ int launch_actor_cluster(const ActorLaunch& p, int G, cudaStream_t stream,
   static SlotInline empty{};
   return cudaLaunchKernelEx(&cfg, kern, p, inl ? *inl : empty) == cudaSuccess ? CYR_OK
                                                                               : CYR_CUDA_ERROR;
+}
+
+// ------------------------------------------------------ tiled batch K2
+// Register-blocked SIMT GEMM chain for large column batches (Mode R over
+// many slots, Mode T levels).  Thread (og, cg) of a 256-thread CTA owns an
+// 8-output x TC/8-column micro-tile of a 256-output panel: per input row it
+// reads 8 weights (128-bit, conflict-free: the warp covers one contiguous
+// 1 KB panel row) and TC/8 activations (warp broadcast) and issues
+// 8*TC/8 FMAs.  Weights stream through a 4-stage TMA bulk-copy ring
+// (paneled layout [panel][in][pw]); activations stay in shared memory.
+constexpr int kTileThreads = 256;
+constexpr int kTileStageBytes = 16 * 1024;
+constexpr int kTileStages = 4;
+
+__host__ __device__ inline int tile_rows(const LayerDesc& L, int elem) {
+  const int r = kTileStageBytes / (L.pw * elem);
+  return r < 1 ? 1 : r;
+}
+__host__ __device__ inline int tile_panels(const LayerDesc& L) {
+  return (L.out_pad + L.pw - 1) / L.pw;
+}
+
+template <typename T, int N>
+__device__ __forceinline__ void ld_vec(const T* src, T (&dst)[N]) {
+  if constexpr (sizeof(T) == 4) {
+    static_assert(N % 4 == 0 || N < 4, "");
+    if constexpr (N >= 4) {
+#pragma unroll
+      for (int i = 0; i < N / 4; ++i) {
+        const float4 t = reinterpret_cast<const float4*>(src)[i];
+        dst[4 * i] = t.x; dst[4 * i + 1] = t.y; dst[4 * i + 2] = t.z; dst[4 * i + 3] = t.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < N; ++i) dst[i] = src[i];
+    }
+  } else {
+    if constexpr (N >= 2) {
+#pragma unroll
+      for (int i = 0; i < N / 2; ++i) {
+        const double2 t = reinterpret_cast<const double2*>(src)[i];
+        dst[2 * i] = t.x; dst[2 * i + 1] = t.y;
+      }
+    } else {
+      dst[0] = src[0];
+    }
+  }
+}
+
+template <typename T, int TC>
+__global__ void __launch_bounds__(kTileThreads, 1) actor_tiled_kernel(const ActorLaunch p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int CPT = TC / 8;
+  constexpr int TCP = TC + 16 / (int)sizeof(T);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  unsigned char* ring = smem + 128;
+  T* act_a = reinterpret_cast<T*>(ring + (size_t)kTileStages * kTileStageBytes);
+  T* act_b = act_a + (size_t)p.desc.max_width * TCP;
+  const int tid = threadIdx.x;
+  const int og = tid & 31, cg = tid >> 5;
+  const int c0 = blockIdx.x * TC;
+  const T* blob = static_cast<const T*>(p.blob);
+  const int nl = p.desc.n_layers;
+
+  int total = 0;
+  for (int l = 0; l < nl; ++l) {
+    const LayerDesc& L = p.desc.layer[l];
+    const int r = tile_rows(L, sizeof(T));
+    total += tile_panels(L) * ((L.in + r - 1) / r);
+  }
+  auto issue = [&](int g) {  // single thread: stage g = (layer, panel, chunk)
+    int l = 0, first = 0;
+    for (;; ++l) {
+      const LayerDesc& L = p.desc.layer[l];
+      const int r = tile_rows(L, sizeof(T));
+      const int n = tile_panels(L) * ((L.in + r - 1) / r);
+      if (g < first + n) break;
+      first += n;
+    }
+    const LayerDesc& L = p.desc.layer[l];
+    const int r = tile_rows(L, sizeof(T));
+    const int chunks = (L.in + r - 1) / r;
+    const int panel = (g - first) / chunks, chunk = (g - first) % chunks;
+    const int i0 = chunk * r;
+    const int nr = min(r, L.in - i0);
+    const uint32_t bytes = (uint32_t)nr * L.pw * sizeof(T);
+    const int buf = g % kTileStages;
+    mbar_expect_tx(&full[buf], bytes);
+    bulk_g2s(ring + (size_t)buf * kTileStageBytes,
+             blob + L.wp_off + ((long long)panel * L.in + i0) * L.pw, bytes, &full[buf]);
+  };
+
+  if (tid == 0) {
+    for (int st = 0; st < kTileStages; ++st) mbar_init(&full[st], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int g = 0; g < min(kTileStages, total); ++g) issue(g);
+
+  const int in0 = p.desc.layer[0].in;
+  for (int idx = tid; idx < in0 * TC; idx += kTileThreads) {
+    const int i = idx / TC, c = idx % TC, col = c0 + c;
+    double v = 0.0;
+    if (col < p.ncols) {
+      if (p.mode_t) {
+        v = mode_t_feature(p, col, i);
+      } else {
+        const int s = col / p.cap, j = col % p.cap + 1;
+        v = (i < p.E) ? (double)p.alloc[(long long)s * p.E + i] / (double)p.N
+                      : (double)j / (double)p.cap;
+      }
+    }
+    act_a[i * TCP + c] = (T)v;
+  }
+  __syncthreads();
+
+  T* cur = act_a;
+  T* nxt = act_b;
+  int g = 0;
+  for (int l = 0; l < nl; ++l) {
+    const LayerDesc L = p.desc.layer[l];
+    const int rows = tile_rows(L, sizeof(T));
+    const bool last = (l == nl - 1);
+    const int npan = tile_panels(L);
+    // narrow panels (the 2E-output head layer): 8 outputs x 2 columns per
+    // thread so every lane works instead of ceil(pw/8) lanes per warp
+    const bool narrow = L.pw <= 64;
+    const int ogn = (L.pw + 7) / 8;
+    for (int panel = 0; panel < npan; ++panel) {
+      T acc[8][CPT];
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < CPT; ++b) acc[a][b] = T(0);
+      constexpr int kNc = CPT > 1 ? 2 : 1;  // columns per thread in the narrow mapping
+      const int my_og = narrow ? tid % ogn : og;
+      const int my_c = narrow ? (tid / ogn) * kNc : cg * CPT;  // first column of this thread
+      const bool active = narrow ? my_c < TC : og * 8 < L.pw;
+      for (int i0 = 0; i0 < L.in; i0 += rows, ++g) {
+        const int buf = g % kTileStages;
+        mbar_wait(&full[buf], (uint32_t)((g / kTileStages) & 1));
+        const T* W = reinterpret_cast<const T*>(ring + (size_t)buf * kTileStageBytes);
+        const int nr = min(rows, L.in - i0);
+        if (active && !narrow) {
+#pragma unroll 4
+          for (int r = 0; r < nr; ++r) {
+            T w[8], x[CPT];
+            ld_vec<T, 8>(W + r * L.pw + og * 8, w);
+            ld_vec<T, CPT>(cur + (size_t)(i0 + r) * TCP + cg * CPT, x);
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+#pragma unroll
+              for (int b = 0; b < CPT; ++b) acc[a][b] = fma(w[a], x[b], acc[a][b]);
+          }
+        } else if (active) {
+#pragma unroll 4
+          for (int r = 0; r < nr; ++r) {
+            T w[8];
+            ld_vec<T, 8>(W + r * L.pw + my_og * 8, w);
+            const T* xr = cur + (size_t)(i0 + r) * TCP + my_c;
+            const T x0 = xr[0], x1 = xr[kNc - 1];
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {
+              acc[a][0] = fma(w[a], x0, acc[a][0]);
+              if constexpr (CPT > 1) acc[a][1] = fma(w[a], x1, acc[a][1]);
+            }
+          }
+        }
+        __syncthreads();  // every thread is done with this stage
+        if (tid == 0 && g + kTileStages < total) issue(g + kTileStages);
+      }
+      if (active) {
+        const int ncol = narrow ? kNc : CPT;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+          const int o = panel * L.pw + my_og * 8 + a;
+          if (o >= L.out) continue;
+          const T bias = blob[L.b_off + o];
+#pragma unroll
+          for (int b = 0; b < CPT; ++b) {
+            if (b >= ncol) break;
+            const T z = acc[a][b] + bias;
+            if (!last) {
+              nxt[(size_t)o * TCP + my_c + b] = z > T(0) ? z : T(0);
+            } else {
+              const int col = c0 + my_c + b;
+              if (col < p.ncols) static_cast<T*>(p.raw)[(long long)col * L.out + o] = z;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    T* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+}
+
+template <typename T, int TC>
+int launch_actor_tiled(const ActorLaunch& p, cudaStream_t stream) {
+  constexpr int TCP = TC + 16 / (int)sizeof(T);
+  const size_t smem = 128 + (size_t)kTileStages * kTileStageBytes +
+                      2ull * p.desc.max_width * TCP * sizeof(T);
+  if (smem > (size_t)kSmemLimit) return CYR_UNSUPPORTED;
+  auto kern = actor_tiled_kernel<T, TC>;
+  static int configured = -1;
+  if ((int)smem > configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return CYR_CUDA_ERROR;
+    configured = (int)smem;
+  }
+  const int blocks = (p.ncols + TC - 1) / TC;
+  kern<<<blocks, kTileThreads, smem, stream>>>(p);
+  return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
+}
+
+// largest tile that fits shared memory and still gives every SM a CTA
+template <typename T>
+int launch_actor_tiled_auto(const ActorLaunch& p, int sm_count, cudaStream_t stream) {
+  auto fits = [&](int tc) {
+    const int tcp = tc + 16 / (int)sizeof(T);
+    return 128 + (size_t)kTileStages * kTileStageBytes +
+               2ull * p.desc.max_width * tcp * sizeof(T) <= (size_t)kSmemLimit;
+  };
+  constexpr int kMax = sizeof(T) == 4 ? 64 : 32;
+  int tc = 8;
+  for (int cand = kMax; cand >= 8; cand >>= 1) {
+    if (!fits(cand)) continue;
+    tc = cand;
+    if ((p.ncols + cand - 1) / cand >= sm_count) break;
+  }
+  if (!fits(tc)) return CYR_UNSUPPORTED;
+  switch (tc) {
+    case 64: if constexpr (sizeof(T) == 4) return launch_actor_tiled<T, 64>(p, stream);
+             else return CYR_UNSUPPORTED;
+    case 32: return launch_actor_tiled<T, 32>(p, stream);
+    case 16: return launch_actor_tiled<T, 16>(p, stream);
+    default: return launch_actor_tiled<T, 8>(p, stream);
+  }
 }
 
 template <typename T, int TC, int OPT>
@@ -488,6 +728,15 @@ int launch_actor_typed(const ActorLaunch& p, int sm_count, cudaStream_t stream) 
 
 }  // namespace cyr
 
+// CYR_ACTOR_TILED=0 selects the first-generation per-output kernel (A/B)
+static bool cyr_use_tiled() {
+  static const bool on = [] {
+    const char* e = getenv("CYR_ACTOR_TILED");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
 int cyr_launch_actor(int precision, const cyr::ActorDesc& desc, const void* blob,
                      const int32_t* alloc, int S, int E, int N, int cap, void* raw,
                      int sm_count, cudaStream_t stream) {
@@ -514,6 +763,10 @@ int cyr_launch_actor(int precision, const cyr::ActorDesc& desc, const void* blob
       return fp64 ? cyr::launch_actor_cluster<double, 8, false>(p, G, stream)
                   : cyr::launch_actor_cluster<float, 8, false>(p, G, stream);
     }
+  }
+  if (cyr_use_tiled()) {
+    if (precision == CYR_FP64) return cyr::launch_actor_tiled_auto<double>(p, sm_count, stream);
+    return cyr::launch_actor_tiled_auto<float>(p, sm_count, stream);
   }
   if (precision == CYR_FP64) return cyr::launch_actor_typed<double>(p, sm_count, stream);
   return cyr::launch_actor_typed<float>(p, sm_count, stream);
@@ -613,6 +866,10 @@ int cyr_launch_actor_mode_t(int precision, const cyr::ActorDesc& desc, const voi
   p.M = M;
   p.epad = epad;
   p.mcs_scale = mcs_scale;
+  if (cyr_use_tiled()) {
+    if (precision == CYR_FP64) return cyr::launch_actor_tiled_auto<double>(p, sm_count, stream);
+    return cyr::launch_actor_tiled_auto<float>(p, sm_count, stream);
+  }
   if (precision == CYR_FP64) return cyr::launch_actor_typed<double>(p, sm_count, stream);
   return cyr::launch_actor_typed<float>(p, sm_count, stream);
 }

@@ -6,19 +6,21 @@
 namespace cyr {
 
 // ------------------------------------------------------------ codebook K3
-// One CTA per slot, one warp per branch row.
+// A CTA holds `spc` whole slots (<= 32 rows); 8 warps stride over the rows
+// in the per-row phases and warp 0 runs every slot's coupled loop at once.
 template <typename RawT>
-__global__ void __launch_bounds__(512) codebook_kernel(
+__global__ void __launch_bounds__(256) codebook_kernel(
     const RawT* __restrict__ raw, const int32_t* __restrict__ alloc,
-    const double* __restrict__ eps, int E, int L, int cap, int32_t* __restrict__ cb,
-    double* __restrict__ m_out, double* __restrict__ nu_out, double* __restrict__ margin_out,
-    int32_t* __restrict__ iters_out, int32_t* __restrict__ status) {
-  __shared__ double s_lo[32], s_hi[32];
-  __shared__ long long s_t[32];
-  __shared__ int s_bis[32];
-  const long long row0 = (long long)blockIdx.x * cap;
-  codebook_rows<RawT>(raw + row0 * 2 * E, alloc, eps, row0, cap, cap, E, L, cb, m_out, nu_out,
-                      margin_out, iters_out, status, s_lo, s_hi, s_t, s_bis);
+    const double* __restrict__ eps, int S, int spc, int E, int L, int cap,
+    int32_t* __restrict__ cb, double* __restrict__ m_out, double* __restrict__ nu_out,
+    double* __restrict__ margin_out, int32_t* __restrict__ iters_out,
+    int32_t* __restrict__ status) {
+  __shared__ RowScratch sc;
+  const long long s0 = (long long)blockIdx.x * spc;
+  const int slots = (int)min((long long)spc, S - s0);
+  const long long row0 = s0 * cap;
+  codebook_rows<RawT>(raw + row0 * 2 * E, alloc, eps, row0, slots * cap, cap, E, L, cb, m_out,
+                      nu_out, margin_out, iters_out, status, sc);
 }
 
 // ------------------------------------------------------------ Mode-T level
@@ -53,14 +55,15 @@ struct TreeIO {
 };
 
 template <typename RawT>
-__global__ void __launch_bounds__(512) tree_level_kernel(const RawT* __restrict__ raw, TreeIO io,
-                                                         int L, int32_t* __restrict__ status) {
-  __shared__ double s_lo[32], s_hi[32];
-  __shared__ long long s_t[32];
-  __shared__ int s_bis[32];
-  const long long row0 = (long long)blockIdx.x * io.cap;
-  codebook_rows_io<RawT, TreeIO>(raw + row0 * 2 * io.E, row0, io.cap, io.cap, io.E, L, io, status,
-                                 s_lo, s_hi, s_t, s_bis);
+__global__ void __launch_bounds__(256) tree_level_kernel(const RawT* __restrict__ raw, TreeIO io,
+                                                         long long groups, int gpc, int L,
+                                                         int32_t* __restrict__ status) {
+  __shared__ RowScratch sc;
+  const long long g0 = (long long)blockIdx.x * gpc;
+  const int n = (int)min((long long)gpc, groups - g0);
+  const long long row0 = g0 * io.cap;
+  codebook_rows_io<RawT, TreeIO>(raw + row0 * 2 * io.E, row0, n * io.cap, io.cap, io.E, L, io,
+                                 status, sc);
 }
 
 // ------------------------------------------------------- standalone enforcer
@@ -253,15 +256,17 @@ int cyr_launch_codebook(int precision, const void* raw, const int32_t* alloc, co
   (void)N;
   if (S <= 0) return CYR_OK;
   if (E < 1 || E > cyr::kMaxUsers || cap < 1 || cap > 16) return CYR_UNSUPPORTED;
-  const dim3 grid(S), block(32 * cap);
+  // small batches: one slot per CTA (latency); large: as many slots as fit 32 rows
+  const int spc = S < 1184 ? 1 : 32 / cap;
+  const dim3 grid((S + spc - 1) / spc), block(S < 1184 ? 32 * cap : 256);
   if (precision == CYR_FP64)
     cyr::codebook_kernel<double><<<grid, block, 0, stream>>>(
-        static_cast<const double*>(raw), alloc, eps, E, L, cap, codebook, m_hat, nu, margin, iters,
-        status);
+        static_cast<const double*>(raw), alloc, eps, S, spc, E, L, cap, codebook, m_hat, nu,
+        margin, iters, status);
   else
     cyr::codebook_kernel<float><<<grid, block, 0, stream>>>(
-        static_cast<const float*>(raw), alloc, eps, E, L, cap, codebook, m_hat, nu, margin, iters,
-        status);
+        static_cast<const float*>(raw), alloc, eps, S, spc, E, L, cap, codebook, m_hat, nu,
+        margin, iters, status);
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
 }
 
@@ -297,12 +302,14 @@ int cyr_launch_tree_level(int precision, const void* raw, const int32_t* alloc, 
   if (E < 1 || E > cyr::kMaxUsers || cap < 1 || cap > 16) return CYR_UNSUPPORTED;
   cyr::TreeIO io{alloc, eps, node, E, cap, epad, parents, nodes_per_slot, parent_off, child_off};
   const long long groups = (long long)S * parents;
-  if (groups >= (1ll << 31)) return CYR_UNSUPPORTED;
+  const int gpc = 32 / cap;  // whole groups per CTA (<= 32 rows)
+  const long long blocks = (groups + gpc - 1) / gpc;
+  if (blocks >= (1ll << 31)) return CYR_UNSUPPORTED;
   if (precision == CYR_FP64)
-    cyr::tree_level_kernel<double><<<(unsigned)groups, 32 * cap, 0, stream>>>(
-        static_cast<const double*>(raw), io, L, status);
+    cyr::tree_level_kernel<double><<<(unsigned)blocks, 256, 0, stream>>>(
+        static_cast<const double*>(raw), io, groups, gpc, L, status);
   else
-    cyr::tree_level_kernel<float><<<(unsigned)groups, 32 * cap, 0, stream>>>(
-        static_cast<const float*>(raw), io, L, status);
+    cyr::tree_level_kernel<float><<<(unsigned)blocks, 256, 0, stream>>>(
+        static_cast<const float*>(raw), io, groups, gpc, L, status);
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
 }

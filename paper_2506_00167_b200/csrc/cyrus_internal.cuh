@@ -150,6 +150,8 @@ struct LayerDesc {
   long long w_off;        // element offset of Wt in the blob
   long long b_off;        // element offset of the bias
   long long wr_off;       // element offset of the row-major W copy
+  int pw;                 // panel width of the tiled K2 layout (<= 256 outputs)
+  long long wp_off;       // paneled Wt: [ceil(out_pad/pw)][in][pw] (== w_off if one panel)
 };
 
 // Single-slot inputs passed BY VALUE in the kernel launch (param space, read

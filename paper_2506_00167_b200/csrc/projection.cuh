@@ -389,30 +389,37 @@ __device__ __forceinline__ void set_status(int32_t* status, int code) {
 // nrows, nrows <= 32, row0 % cap == 0.  raw points at local row 0's logits
 // ([row][2E]).  IO supplies the group's allocation row and the row's noise
 // and consumes the grants (lanes < E) — see SlotIO / the Mode-T TreeIO.
+// Shared-memory scratch of one codebook_rows_io call (<= 32 rows).
+struct RowScratch {
+  double lo[32], hi[32];
+  long long t[32];
+  int flags[32];      // bit 0 bis, bit 1 degen
+  int iters[32];
+  double b[32][32];   // [row][user] raw actions from phase 1 (head computed once)
+};
+
 template <typename RawT, typename IO>
 __device__ void codebook_rows_io(const RawT* raw, long long row0, int nrows, int cap, int E,
-                                 int L, const IO& io, int32_t* status, double* s_lo,
-                                 double* s_hi, long long* s_t, int* s_bis,
+                                 int L, const IO& io, int32_t* status, RowScratch& sc,
                                  unsigned long long* tr = nullptr) {
   const int w = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   const bool in = lane < E;
-  const bool mine = w < nrows;
-  const long long grow = row0 + w;
-  const long long group = grow / cap;
-  const int j = (int)(grow % cap) + 1;
-  Row row;
-  row.valid = mine;
-  row.b = 0.0;
-  row.c = 0.0;
-  row.d = 0.0;
-  if (mine) {
+  // phase 1 (warp per row, warps stride over the rows): head, bracket,
+  // water level, exact fill threshold
+  for (int lr = w; lr < nrows; lr += nw) {
+    const long long grow = row0 + lr;
+    const long long group = grow / cap;
+    const int j = (int)(grow % cap) + 1;
     const int32_t* alloc = io.alloc_row(group);
     const double* eps = io.eps_row(grow, group, j);
+    Row row;
+    row.valid = true;
     const double n = in ? (double)alloc[lane] : 0.0;
     double bval = 0.0;
     if (in) {
-      const RawT* rr = raw + (long long)w * 2 * E;
+      const RawT* rr = raw + (long long)lr * 2 * E;
       const double mu = (double)rr[lane];
       const double ls = fmin(fmax((double)rr[E + lane], kLogSigmaMin), kLogSigmaMax);
       double a;
@@ -430,44 +437,63 @@ __device__ void codebook_rows_io(const RawT* raw, long long row0, int nrows, int
     const double capsum = np_row_sum(n, E);  // enforcer.py:64 / :138
     if (lane == 0 && row.d > capsum) set_status(status, CYR_INFEASIBLE);
     trace_stamp(tr, 8);
-    // phase 1 (warp per row): bracket, water level, exact fill threshold
     kl_setup(row, E);
     trace_stamp(tr, 9);
     long long thr = 0;
     if (row.bis) thr = fill_threshold(row, E, water_level(row, E));
     trace_stamp(tr, 10);
+    sc.b[lr][lane] = bval;
     if (lane == 0) {
-      s_lo[w] = row.lo;
-      s_hi[w] = row.hi;
-      s_t[w] = thr;
-      s_bis[w] = row.bis;
+      sc.lo[lr] = row.lo;
+      sc.hi[lr] = row.hi;
+      sc.t[lr] = thr;
+      sc.flags[lr] = (row.bis ? 1 : 0) | (row.degen ? 2 : 0);
     }
-    if (w < 8) trace_stamp_warp(tr, 16 + w);
+    if (lr < 8) trace_stamp_warp(tr, 16 + lr);
   }
   __syncthreads();
-  if (!mine) return;
-  // phase 2 (lanes = rows, redundantly in every row warp): coupled loop per group
-  double lo[1] = {lane < nrows ? s_lo[lane] : 0.0};
-  double hi[1] = {lane < nrows ? s_hi[lane] : 0.0};
-  const long long tt[1] = {lane < nrows ? s_t[lane] : 0};
-  const bool bis[1] = {lane < nrows && s_bis[lane] != 0};
-  trace_stamp(tr, 11);
-  const int iters = coupled_bisection<1>(lo, hi, tt, bis, cap);  // rows are group-aligned
-  trace_stamp(tr, 12);
-  row.lo = shfl_d(lo[0], w);
-  row.hi = shfl_d(hi[0], w);
-  const int group_iters = __shfl_sync(kFull, iters, w);
+  // phase 2 (warp 0, lanes = rows): the coupled loop of every group at once
+  if (w == 0) {
+    double lo[1] = {lane < nrows ? sc.lo[lane] : 0.0};
+    double hi[1] = {lane < nrows ? sc.hi[lane] : 0.0};
+    const long long tt[1] = {lane < nrows ? sc.t[lane] : 0};
+    const bool bis[1] = {lane < nrows && (sc.flags[lane] & 1)};
+    trace_stamp(tr, 11);
+    const int iters = coupled_bisection<1>(lo, hi, tt, bis, cap);  // rows are group-aligned
+    trace_stamp(tr, 12);
+    if (lane < nrows) {
+      sc.lo[lane] = lo[0];
+      sc.hi[lane] = hi[0];
+      sc.iters[lane] = iters;
+    }
+  }
+  __syncthreads();
   // phase 3 (warp per row): m_hat, nu, Huntington-Hill
-  double m, nu;
-  kl_finish(row, E, m, nu);
-  trace_stamp(tr, 13);
-  double margin;
-  int hh_steps = 0;
-  const int g = hh_row(m, row.c, E, (long long)j * L, margin, &hh_steps);
-  trace_stamp(tr, 14);
-  if (w < 8) trace_value(tr, 40 + w, hh_steps);
-  if (w < 8) trace_value(tr, 56 + w, group_iters);
-  io.emit(grow, group, j, lane, g, m, nu, margin, group_iters);
+  for (int lr = w; lr < nrows; lr += nw) {
+    const long long grow = row0 + lr;
+    const long long group = grow / cap;
+    const int j = (int)(grow % cap) + 1;
+    const int32_t* alloc = io.alloc_row(group);
+    Row row;
+    row.valid = true;
+    row.b = sc.b[lr][lane];
+    row.c = in ? (double)alloc[lane] : 0.0;
+    row.d = (double)((long long)j * L);
+    row.bis = (sc.flags[lr] & 1) != 0;
+    row.degen = (sc.flags[lr] & 2) != 0;
+    row.lo = sc.lo[lr];
+    row.hi = sc.hi[lr];
+    double m, nu;
+    kl_finish(row, E, m, nu);
+    trace_stamp(tr, 13);
+    double margin;
+    int hh_steps = 0;
+    const int g = hh_row(m, row.c, E, (long long)j * L, margin, &hh_steps);
+    trace_stamp(tr, 14);
+    if (lr < 8) trace_value(tr, 40 + lr, hh_steps);
+    if (lr < 8) trace_value(tr, 56 + lr, sc.iters[lr]);
+    io.emit(grow, group, j, lane, g, m, nu, margin, sc.iters[lr]);
+  }
 }
 
 // Mode R: the slot codebook [S][cap+1][E] plus optional diagnostics.
@@ -504,11 +530,10 @@ template <typename RawT>
 __device__ void codebook_rows(const RawT* raw, const int32_t* alloc, const double* eps,
                               long long row0, int nrows, int cap, int E, int L, int32_t* cb,
                               double* m_out, double* nu_out, double* margin_out,
-                              int32_t* iters_out, int32_t* status, double* s_lo, double* s_hi,
-                              long long* s_t, int* s_bis, unsigned long long* tr = nullptr) {
+                              int32_t* iters_out, int32_t* status, RowScratch& sc,
+                              unsigned long long* tr = nullptr) {
   const SlotIO io{alloc, eps, cb, m_out, nu_out, margin_out, iters_out, E, cap};
-  codebook_rows_io<RawT, SlotIO>(raw, row0, nrows, cap, E, L, io, status, s_lo, s_hi, s_t, s_bis,
-                                 tr);
+  codebook_rows_io<RawT, SlotIO>(raw, row0, nrows, cap, E, L, io, status, sc, tr);
 }
 
 }  // namespace cyr
