@@ -51,8 +51,11 @@ enum cyr_status {
 };
 
 enum cyr_precision {
-  CYR_FP32 = 0, /* fp32 SIMT actor GEMM (default), fp64 head + projection  */
-  CYR_FP64 = 1  /* fp64 actor GEMM: logits within 1e-15 of the reference   */
+  CYR_FP32 = 0,    /* fp32 SIMT actor GEMM (default), fp64 head + projection */
+  CYR_FP64 = 1,    /* fp64 actor GEMM: logits within 1e-15 of the reference  */
+  CYR_BF16_TC = 2  /* bf16 tcgen05 actor for batches >= 1024 columns (Mode T
+                      levels, big Mode-R batches), fp32 SIMT below; widths
+                      <= 256; decisions NOT bit-comparable (agreement rate) */
 };
 
 typedef struct cyr_policy cyr_policy;

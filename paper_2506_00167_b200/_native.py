@@ -15,8 +15,8 @@ import threading
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcyrus_b200.so")
 
 CYR_OK, CYR_INFEASIBLE, CYR_BAD_ARG, CYR_CUDA_ERROR, CYR_UNSUPPORTED = range(5)
-CYR_FP32, CYR_FP64 = 0, 1
-PRECISIONS = {"fp32": CYR_FP32, "fp64": CYR_FP64}
+CYR_FP32, CYR_FP64, CYR_BF16_TC = 0, 1, 2
+PRECISIONS = {"fp32": CYR_FP32, "fp64": CYR_FP64, "bf16_tc": CYR_BF16_TC}
 
 _c_int, _c_i32, _c_i64 = ctypes.c_int, ctypes.c_int32, ctypes.c_int64
 _vp, _cp = ctypes.c_void_p, ctypes.c_char_p

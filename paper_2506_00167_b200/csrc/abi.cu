@@ -85,6 +85,12 @@ struct cyr_policy {
   cyr::ActorDesc desc{};
   void* blob_d = nullptr;
   size_t blob_elems = 0;
+  // CYR_BF16_TC: pre-swizzled bf16 weight images for the tcgen05 actor
+  bool tc_ok = false;
+  unsigned char* tc_blob_d = nullptr;
+  size_t tc_bytes = 0;
+  long long tc_off[cyr::kMaxLayers] = {};
+  int tc_npad[cyr::kMaxLayers] = {};
   int sm_count = 148;
   // host path
   cudaStream_t stream = nullptr;
@@ -138,7 +144,41 @@ void pack_blob(const cyr_policy& p, const double* src, std::vector<T>& dst) {
   }
 }
 
+uint16_t f32_to_bf16_rne(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fc0;
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+// per layer: ceil(in/64) K-major SWIZZLE_128B tiles of [npad x 64] bf16 —
+// the exact shared-memory image tcgen05.mma reads (actor_tc.cu)
+void pack_tc(const cyr_policy& p, const double* src, std::vector<uint8_t>& dst) {
+  dst.assign(p.tc_bytes, 0);
+  size_t off = 0;
+  for (int l = 0; l < p.desc.n_layers; ++l) {
+    const cyr::LayerDesc& L = p.desc.layer[l];
+    const size_t tile_bytes = (size_t)p.tc_npad[l] * 128;
+    for (int n = 0; n < L.out; ++n)
+      for (int k = 0; k < L.in; ++k) {
+        const int t = k / 64, kk = k % 64;
+        const int chunk = (kk * 2) >> 4;
+        const size_t byte = (size_t)p.tc_off[l] + t * tile_bytes + (size_t)(n >> 3) * 1024 +
+                            (n & 7) * 128 + ((chunk ^ (n & 7)) << 4) + ((kk * 2) & 15);
+        const uint16_t v = f32_to_bf16_rne((float)src[off + (size_t)n * L.in + k]);
+        std::memcpy(&dst[byte], &v, 2);
+      }
+    off += (size_t)L.out * L.in + L.out;
+  }
+}
+
 int upload(cyr_policy* p, const double* blob) {
+  if (p->tc_ok) {
+    std::vector<uint8_t> h;
+    pack_tc(*p, blob, h);
+    CYR_CUDA(cudaMemcpy(p->tc_blob_d, h.data(), h.size(), cudaMemcpyHostToDevice));
+  }
   if (p->precision == CYR_FP64) {
     std::vector<double> h;
     pack_blob(*p, blob, h);
@@ -206,6 +246,22 @@ int ensure_host_path(cyr_policy* p, int S, int cap) {
   return CYR_OK;
 }
 
+constexpr long long kTcMinCols = 1024;  // below: the MLP is not a dense GEMM
+
+int simt_precision(const cyr_policy* p) { return p->precision == CYR_FP64 ? CYR_FP64 : CYR_FP32; }
+
+// Mode-R actor for S slots with the policy's precision choice
+int launch_actor_policy(const cyr_policy* p, const int32_t* alloc, int S, int N, int cap, void* raw,
+                        cudaStream_t st) {
+  if (p->tc_ok && (long long)S * cap >= kTcMinCols)
+    return cyr_launch_actor_tc(p->desc, p->tc_blob_d, p->tc_off, p->tc_npad,
+                               static_cast<const float*>(p->blob_d), alloc, S, p->E, N, cap,
+                               static_cast<float*>(raw), 0, nullptr, nullptr, 0, 0, 0, 0, 0, 0,
+                               1.0, st);
+  return cyr_launch_actor(simt_precision(p), p->desc, p->blob_d, alloc, S, p->E, N, cap, raw,
+                          p->sm_count, st);
+}
+
 int check_geometry(int S, int E, int N, int L, int* cap_out) {
   if (S < 0 || E < 1 || E > cyr::kMaxUsers || N <= 0 || L <= 0 || L >= N) return CYR_BAD_ARG;
   const int cap = N / L;
@@ -256,7 +312,8 @@ int cyr_policy_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
                       const double* weights_blob, int32_t precision) {
   if (!out || !sizes || !weights_blob || n_sizes < 2 || n_sizes - 1 > cyr::kMaxLayers)
     return CYR_BAD_ARG;
-  if (precision != CYR_FP32 && precision != CYR_FP64) return CYR_BAD_ARG;
+  if (precision != CYR_FP32 && precision != CYR_FP64 && precision != CYR_BF16_TC)
+    return CYR_BAD_ARG;
   if (sizes[n_sizes - 1] % 2 != 0) return CYR_BAD_ARG;
   const int E = sizes[n_sizes - 1] / 2;
   if (E < 1 || E > cyr::kMaxUsers) return CYR_BAD_ARG;
@@ -299,6 +356,26 @@ int cyr_policy_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
     p->desc.max_rows = std::max(p->desc.max_rows, std::max(L.in_pad, L.out));
   }
   p->blob_elems = off;
+  if (precision == CYR_BF16_TC) {  // tensor-core images when every layer fits one MMA tile
+    p->tc_ok = true;
+    size_t tb = 0;
+    for (int l = 0; l < n_sizes - 1; ++l) {
+      const cyr::LayerDesc& L = p->desc.layer[l];
+      const int npad = (L.out + 15) / 16 * 16;
+      if (L.in > 256 || npad > 256) p->tc_ok = false;
+      p->tc_npad[l] = npad;
+      p->tc_off[l] = (long long)tb;
+      tb += (size_t)((L.in + 63) / 64) * npad * 128;
+    }
+    p->tc_bytes = tb;
+    if (p->tc_ok) {
+      cudaError_t e2 = cudaMalloc(&p->tc_blob_d, tb);
+      if (e2 != cudaSuccess) {
+        delete p;
+        return cuda_fail(e2, "cudaMalloc(tc images)");
+      }
+    }
+  }
   cudaError_t e = cudaMalloc(&p->blob_d, off * p->elem);
   if (e != cudaSuccess) {
     delete p;
@@ -369,6 +446,7 @@ int cyr_policy_destroy(cyr_policy* p) {
   if (p->ev0) cudaEventDestroy(p->ev0);
   if (p->ev1) cudaEventDestroy(p->ev1);
   cudaFree(p->blob_d);
+  cudaFree(p->tc_blob_d);
   delete p;
   return CYR_OK;
 }
@@ -384,8 +462,7 @@ int cyr_policy_info(const cyr_policy* p, int32_t* num_users, int32_t* n_sizes, i
 int cyr_actor_forward_device(const cyr_policy* p, const int32_t* alloc, int32_t S, int32_t N,
                              int32_t cap, void* raw, void* stream) {
   if (!p || p->mode_t || (S > 0 && (!alloc || !raw)) || N <= 0 || cap < 1) return CYR_BAD_ARG;
-  const int rc = cyr_launch_actor(p->precision, p->desc, p->blob_d, alloc, S, p->E, N, cap, raw,
-                                  p->sm_count, static_cast<cudaStream_t>(stream));
+  const int rc = launch_actor_policy(p, alloc, S, N, cap, raw, static_cast<cudaStream_t>(stream));
   if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
   return rc;
 }
@@ -548,8 +625,7 @@ int cyr_codebook_host(cyr_policy* p, const int32_t* alloc, const double* eps, in
         cudaMemcpyAsync(p->eps_d, p->pin_eps, (size_t)S * cap * E * 8, cudaMemcpyHostToDevice,
                         st);
       cudaMemsetAsync(p->status_d, 0, 4, st);
-      lrc = cyr_launch_actor(p->precision, p->desc, p->blob_d, p->alloc_d, S, E, N, cap,
-                             p->raw_d, p->sm_count, st);
+      lrc = launch_actor_policy(p, p->alloc_d, S, N, cap, p->raw_d, st);
       if (lrc == CYR_OK)
         lrc = cyr_launch_codebook(p->precision, p->raw_d, p->alloc_d, det ? nullptr : p->eps_d,
                                   S, E, N, L, cap, p->cb_d, nullptr, nullptr, nullptr, nullptr,
@@ -714,12 +790,18 @@ int cyr_tree_mode_t_device(const cyr_policy* p, const int32_t* alloc, const int3
   long long parents = 1, level_off = 0, prev_off = -1;
   for (int tau = 1; tau <= M; ++tau) {
     // K2: the actor on every (parent, branch) column of this level
-    rc = cyr_launch_actor_mode_t(p->precision, p->desc, p->blob_d, alloc, mcs, node_state, S,
-                                 p->E, N, cap, M, tau, (int)parents, nodes, prev_off, epad,
-                                 mcs_scale, workspace, p->sm_count, st);
+    if (p->tc_ok && (long long)S * parents * cap >= kTcMinCols)
+      rc = cyr_launch_actor_tc(p->desc, p->tc_blob_d, p->tc_off, p->tc_npad,
+                               static_cast<const float*>(p->blob_d), alloc, S, p->E, N, cap,
+                               static_cast<float*>(workspace), 1, mcs, node_state, M, tau,
+                               (int)parents, nodes, prev_off, epad, mcs_scale, st);
+    else
+      rc = cyr_launch_actor_mode_t(simt_precision(p), p->desc, p->blob_d, alloc, mcs, node_state,
+                                   S, p->E, N, cap, M, tau, (int)parents, nodes, prev_off, epad,
+                                   mcs_scale, workspace, p->sm_count, st);
     if (rc != CYR_OK) break;
     // K3: one coupled enforcement per parent; writes the children's states
-    rc = cyr_launch_tree_level(p->precision, workspace, alloc, eps, node_state, S, p->E, L, cap,
+    rc = cyr_launch_tree_level(simt_precision(p), workspace, alloc, eps, node_state, S, p->E, L, cap,
                                (int)parents, epad, nodes, prev_off, level_off, status, st);
     if (rc != CYR_OK) break;
     prev_off = level_off;

@@ -1,0 +1,340 @@
+// actor_tc.cu — K2-TC: the actor MLP on the 5th-generation tensor cores.
+//
+// Optional bf16 path (precision CYR_BF16_TC) for batches where the MLP is a
+// real dense GEMM — Mode-T tree levels and large Mode-R batches (SURVEY.md
+// §7 step 8, BASELINE configs[4]).  Decisions are not bit-comparable with
+// the fp32/fp64 paths (bf16 operands); tests report the agreement rate.
+//
+// One CTA (4 warps) owns M = 128 batch columns and runs every layer:
+//   D[128 x N] (fp32, TMEM) = A[128 x K] (bf16, smem) . W[N x K]^T (bf16, smem)
+// with tcgen05.mma.cta_group::1.kind::f16 issued by one thread, 16-deep K
+// steps.  Both operands are K-major SWIZZLE_128B tiles of 64 K-elements:
+//   * W tiles are pre-swizzled at publish time into exactly that smem image
+//     (cyr_policy_create), so one TMA bulk copy (cp.async.bulk, UBLKCP) per
+//     tile lands them MMA-ready; a 3-slot ring streams them across layers,
+//     slots released by tcgen05.commit on an mbarrier;
+//   * A is the activation tile: layer 1 is built from the branch / node-state
+//     features, later layers are written by the previous layer's epilogue
+//     (tcgen05.ld 32x32b -> bias, ReLU -> bf16 -> swizzled st.shared).
+// The last layer's epilogue writes fp32 logits raw[col][2E] for K3.
+// Widths <= 256 (N of one MMA, 256 TMEM columns); wider actors use SIMT.
+#include "cyrus_internal.cuh"
+#include "cyrus_b200.h"
+
+#include <cuda_bf16.h>
+
+namespace cyr {
+
+constexpr int kTcThreads = 128;
+constexpr int kTcM = 128;
+constexpr int kTcSlots = 3;
+constexpr int kTcSlotBytes = 256 * 128;  // one [256 x 64] bf16 tile
+constexpr int kTcMaxKt = 4;              // K <= 256
+
+struct TcLaunch {
+  ActorDesc desc;
+  const unsigned char* tc_blob;  // per layer: Kt tiles of [npad x 64] bf16, SW128 images
+  long long tc_off[kMaxLayers];  // byte offset of layer l's first tile
+  int tc_npad[kMaxLayers];       // N padded to a multiple of 16
+  const float* bias;             // fp32 bias per layer at desc.layer[l].b_off (fp32 blob)
+  const int32_t* alloc;
+  float* raw;
+  int S, E, N, cap, ncols;
+  // Mode T
+  int mode_t;
+  const int16_t* node;
+  const int32_t* mcs;
+  long long nodes_per_slot, parent_off;
+  int parents, tau, M, epad;
+  double mcs_scale;
+};
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);  // start address (16-B units)
+  d |= (uint64_t)1 << 16;                       // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;             // SBO: 8-row core-matrix groups
+  d |= (uint64_t)1 << 46;                       // descriptor version (sm100)
+  d |= (uint64_t)2 << 61;                       // SWIZZLE_128B
+  return d;
+}
+
+// byte offset of element (row r, k in [0,64)) in a K-major SW128 bf16 tile
+__host__ __device__ __forceinline__ uint32_t sw128_offset(int r, int k) {
+  const int chunk = (k * 2) >> 4;  // 16-byte chunk within the 128-byte row
+  return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((chunk ^ (r & 7)) << 4) + ((k * 2) & 15));
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, int accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ double tc_feature(const TcLaunch& p, int col, int i) {
+  if (!p.mode_t) {
+    const int s = col / p.cap, j = col % p.cap + 1;
+    return (i < p.E) ? (double)p.alloc[(long long)s * p.E + i] / (double)p.N
+                     : (double)j / (double)p.cap;
+  }
+  const int k = col % p.cap + 1;
+  const int g = col / p.cap;
+  const int s = g / p.parents;
+  const int q = g - s * p.parents;
+  const int E = p.E;
+  if (i < E) return (double)p.alloc[(long long)s * E + i] / (double)p.N;
+  if (i == E) return (double)k / (double)p.cap;
+  if (i <= 2 * E) {
+    if (p.parent_off < 0) return 0.0;
+    const long long rec = (long long)s * p.nodes_per_slot + p.parent_off + q;
+    return (double)p.node[rec * p.epad + (i - E - 1)] / (double)p.N;
+  }
+  if (i <= 3 * E) return (double)p.mcs[(long long)s * E + (i - 2 * E - 1)] / p.mcs_scale;
+  if (i == 3 * E + 1) {
+    int arrivals = 0, x = q;
+    for (int d = 1; d < p.tau; ++d) {
+      arrivals += x % (p.cap + 1);
+      x /= (p.cap + 1);
+    }
+    return (double)arrivals / (double)(p.M * p.cap);
+  }
+  return (double)(p.tau - 1) / (double)p.M;
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) actor_tc_kernel(const TcLaunch p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-B aligned carve-up: A tiles | B ring | barriers
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  unsigned char* a_tiles = base;                                   // kTcMaxKt x 16 KB
+  unsigned char* ring = base + kTcMaxKt * kTcM * 128;              // kTcSlots x 32 KB
+  uint64_t* bar_full = reinterpret_cast<uint64_t*>(ring + kTcSlots * kTcSlotBytes);
+  uint64_t* bar_free = bar_full + kTcSlots;
+  uint64_t* bar_mma = bar_free + kTcSlots;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_mma + 1);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int c0 = blockIdx.x * kTcM;
+  const int nl = p.desc.n_layers;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kTcSlots; ++i) {
+      mbar_init(&bar_full[i], 1);
+      mbar_init(&bar_free[i], 1);
+    }
+    mbar_init(bar_mma, 1);
+    fence_mbar_init();
+  }
+
+  // weight-tile sequence across layers: g -> (layer, k-tile)
+  int total = 0;
+  for (int l = 0; l < nl; ++l) total += (p.desc.layer[l].in + 63) / 64;
+  auto tile_of = [&](int g, int& l, int& t) {
+    l = 0;
+    int first = 0;
+    for (;; ++l) {
+      const int kt = (p.desc.layer[l].in + 63) / 64;
+      if (g < first + kt) break;
+      first += kt;
+    }
+    t = g - first;
+  };
+  auto issue = [&](int g) {  // thread 0
+    if (g >= total) return;
+    const int slot = g % kTcSlots;
+    if (g >= kTcSlots) mbar_wait(&bar_free[slot], (uint32_t)(((g / kTcSlots) - 1) & 1));
+    int l, t;
+    tile_of(g, l, t);
+    const uint32_t bytes = (uint32_t)p.tc_npad[l] * 128;
+    mbar_expect_tx(&bar_full[slot], bytes);
+    bulk_g2s(ring + (size_t)slot * kTcSlotBytes, p.tc_blob + p.tc_off[l] + (long long)t * bytes,
+             bytes, &bar_full[slot]);
+  };
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (tid == 0)
+    for (int g = 0; g < kTcSlots - 1; ++g) issue(g);
+
+  // layer-1 A tile(s): thread tid builds batch column c0 + tid
+  {
+    const int in0 = p.desc.layer[0].in;
+    const int kt0 = (in0 + 63) / 64;
+    const int col = c0 + tid;
+    for (int t = 0; t < kt0; ++t) {
+      unsigned char* a = a_tiles + t * kTcM * 128;
+      for (int k = 0; k < 64; k += 2) {
+        const int i = t * 64 + k;
+        float v0 = 0.f, v1 = 0.f;
+        if (col < p.ncols) {
+          if (i < in0) v0 = (float)tc_feature(p, col, i);
+          if (i + 1 < in0) v1 = (float)tc_feature(p, col, i + 1);
+        }
+        const __nv_bfloat162 pr = __floats2bfloat162_rn(v0, v1);
+        *reinterpret_cast<__nv_bfloat162*>(a + sw128_offset(tid, k)) = pr;
+      }
+    }
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+
+  int g = 0, mma_phase = 0;
+  for (int l = 0; l < nl; ++l) {
+    const LayerDesc& L = p.desc.layer[l];
+    const int kt = (L.in + 63) / 64;
+    const int npad = p.tc_npad[l];
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(npad >> 3) << 17) |
+                           ((uint32_t)(kTcM >> 4) << 24);
+    if (tid == 0) {
+      tc_fence_after();
+      for (int t = 0; t < kt; ++t, ++g) {
+        const int slot = g % kTcSlots;
+        mbar_wait(&bar_full[slot], (uint32_t)((g / kTcSlots) & 1));
+        tc_fence_after();
+        const uint32_t a_addr = smem_u32(a_tiles + t * kTcM * 128);
+        const uint32_t b_addr = smem_u32(ring + (size_t)slot * kTcSlotBytes);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          tc_mma(tmem, umma_desc_sw128(a_addr + ks * 32), umma_desc_sw128(b_addr + ks * 32),
+                 idesc, (t > 0 || ks > 0) ? 1 : 0);
+        tc_commit(&bar_free[slot]);  // slot reusable once these MMAs retire
+        issue(g + kTcSlots - 1);     // refill the slot freed by the previous tile
+      }
+      tc_commit(bar_mma);  // accumulator complete
+    }
+    // epilogue: TMEM lane (32*warp + lane) = batch column c0 + tid
+    mbar_wait(bar_mma, (uint32_t)(mma_phase & 1));
+    ++mma_phase;
+    tc_fence_after();
+    const bool last = l == nl - 1;
+    const int col = c0 + tid;
+    const float* bias = p.bias + L.b_off;
+    // hidden layers also zero the K padding of the next A tile (n0 < roundup(out, 64))
+    const int n_end = last ? npad : ((L.out + 63) & ~63);
+    for (int n0 = 0; n0 < n_end; n0 += 32) {
+      uint32_t r[32];
+      if (n0 < npad) tc_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)n0, r);
+      else
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = 0u;
+      if (last) {
+        if (col < p.ncols)
+          for (int j = 0; j < 32; ++j) {
+            const int o = n0 + j;
+            if (o < L.out) p.raw[(long long)col * L.out + o] = __uint_as_float(r[j]) + bias[o];
+          }
+      } else {
+        unsigned char* a = a_tiles + (n0 >> 6) * kTcM * 128;
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const int o = n0 + j;
+          float v0 = o < L.out ? __uint_as_float(r[j]) + bias[o] : 0.f;
+          float v1 = o + 1 < L.out ? __uint_as_float(r[j + 1]) + bias[o + 1] : 0.f;
+          v0 = v0 > 0.f ? v0 : 0.f;
+          v1 = v1 > 0.f ? v1 : 0.f;
+          *reinterpret_cast<__nv_bfloat162*>(a + sw128_offset(tid, (n0 & 63) + j)) =
+              __floats2bfloat162_rn(v0, v1);
+        }
+      }
+    }
+    fence_proxy_async_smem();  // new A tiles -> visible to the MMA (async proxy)
+    tc_fence_before();
+    __syncthreads();
+  }
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  }
+}
+
+}  // namespace cyr
+
+size_t cyr_tc_smem_bytes() {
+  return 1024 + (size_t)cyr::kTcMaxKt * cyr::kTcM * 128 + (size_t)cyr::kTcSlots * cyr::kTcSlotBytes +
+         (2 * cyr::kTcSlots + 1) * 8 + 16;
+}
+
+int cyr_launch_actor_tc(const cyr::ActorDesc& desc, const unsigned char* tc_blob,
+                        const long long* tc_off, const int* tc_npad, const float* bias_blob,
+                        const int32_t* alloc, int S, int E, int N, int cap, float* raw,
+                        int mode_t, const int32_t* mcs, const int16_t* node, int M, int tau,
+                        int parents, long long nodes_per_slot, long long parent_off, int epad,
+                        double mcs_scale, cudaStream_t stream) {
+  cyr::TcLaunch p{};
+  p.desc = desc;
+  for (int l = 0; l < desc.n_layers; ++l) {
+    if (desc.layer[l].in > 64 * cyr::kTcMaxKt || tc_npad[l] > 256) return CYR_UNSUPPORTED;
+    p.tc_off[l] = tc_off[l];
+    p.tc_npad[l] = tc_npad[l];
+  }
+  p.tc_blob = tc_blob;
+  p.bias = bias_blob;
+  p.alloc = alloc;
+  p.raw = raw;
+  p.S = S;
+  p.E = E;
+  p.N = N;
+  p.cap = cap;
+  const long long ncols = mode_t ? (long long)S * parents * cap : (long long)S * cap;
+  if (ncols <= 0) return CYR_OK;
+  if (ncols >= (1ll << 31)) return CYR_UNSUPPORTED;
+  p.ncols = (int)ncols;
+  p.mode_t = mode_t;
+  p.node = node;
+  p.mcs = mcs;
+  p.nodes_per_slot = nodes_per_slot;
+  p.parent_off = parent_off;
+  p.parents = parents;
+  p.tau = tau;
+  p.M = M;
+  p.epad = epad;
+  p.mcs_scale = mcs_scale;
+  const size_t smem = cyr_tc_smem_bytes();
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(cyr::actor_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return CYR_CUDA_ERROR;
+    configured = true;
+  }
+  const int blocks = (p.ncols + cyr::kTcM - 1) / cyr::kTcM;
+  cyr::actor_tc_kernel<<<blocks, cyr::kTcThreads, smem, stream>>>(p);
+  return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
+}

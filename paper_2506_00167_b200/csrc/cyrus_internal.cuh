@@ -206,3 +206,10 @@ int cyr_launch_tree_level(int precision, const void* raw, const int32_t* alloc, 
                           int16_t* node, int S, int E, int L, int cap, int parents, int epad,
                           long long nodes_per_slot, long long parent_off, long long child_off,
                           int32_t* status, cudaStream_t stream);
+size_t cyr_tc_smem_bytes();
+int cyr_launch_actor_tc(const cyr::ActorDesc& desc, const unsigned char* tc_blob,
+                        const long long* tc_off, const int* tc_npad, const float* bias_blob,
+                        const int32_t* alloc, int S, int E, int N, int cap, float* raw,
+                        int mode_t, const int32_t* mcs, const int16_t* node, int M, int tau,
+                        int parents, long long nodes_per_slot, long long parent_off, int epad,
+                        double mcs_scale, cudaStream_t stream);

@@ -92,6 +92,7 @@ class DevicePolicy:
 
     @property
     def elem_bytes(self) -> int:
+        """Element size of the raw logits (bf16_tc writes fp32 logits)."""
         return 8 if self.precision == "fp64" else 4
 
     def update(self, actor) -> None:

@@ -16,7 +16,7 @@ GEOMS = {"cfg1": (780, 4, 300, (256, 256)), "cfg2": (780, 10, 195, (256, 256)),
 ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", default="cfg2")
 ap.add_argument("--slots", type=int, default=1)
-ap.add_argument("--precision", default="fp32")
+ap.add_argument("--precision", default="fp32", choices=("fp32", "fp64", "bf16_tc"))
 ap.add_argument("--reps", type=int, default=3)
 a = ap.parse_args()
 n, e, l, hidden = GEOMS[a.cfg]

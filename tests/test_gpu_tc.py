@@ -1,0 +1,111 @@
+"""GPU: the optional bf16 tcgen05 actor (precision "bf16_tc").
+
+Not a parity path: bf16 operands change logits at the 1e-3 level, so
+decisions are compared with the fp32 SIMT path as an AGREEMENT RATE
+(BASELINE configs[4]: "fp32 SIMT vs bf16 tcgen05 path with
+decision-agreement rate").  The logits must still be close to fp32 and the
+integer outputs must satisfy every feasibility contract.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2506_00167_b200 import CodebookEngine, DevicePolicy, _native, tree
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _inputs(cfg, slots, seed=0):
+    from bench import synthetic_inputs
+    return synthetic_inputs(cfg.cell, slots, seed=seed)
+
+
+def _logits(pol, cell, allocs):
+    s = allocs.shape[0]
+    cap = cell.num_branches
+    raw = torch.empty((s * cap, 2 * cell.num_embb), dtype=torch.float32, device="cuda")
+    al = torch.from_numpy(allocs).cuda()
+    _native.check(_native.lib().cyr_actor_forward_device(
+        pol.handle, al.data_ptr(), s, cell.total_scs, cap, raw.data_ptr(), _native.stream_handle()))
+    torch.cuda.synchronize()
+    return raw.double().cpu().numpy()
+
+
+@pytest.mark.parametrize("name", ["cfg2", "stress", "cfg1"])
+def test_tc_logits_close_to_fp32(golden, name):
+    cfg = golden.config(name)
+    agent = cfg.agent()
+    allocs, _ = _inputs(cfg, 512)           # 512 slots x cap columns >= 1024: tensor-core path
+    fp32 = _logits(DevicePolicy(agent.actor, "fp32"), cfg.cell, allocs)
+    tc = _logits(DevicePolicy(agent.actor, "bf16_tc"), cfg.cell, allocs)
+    scale = np.abs(fp32).max(axis=1, keepdims=True)
+    worst = float((np.abs(tc - fp32) / scale).max())
+    print(f"[bf16_tc] {name}: worst |dlogit|/max|col| = {worst:.2e}")
+    assert worst < 3e-2
+    assert not np.array_equal(tc, fp32)     # it really ran the bf16 path
+
+
+def _record(key, value):
+    path = os.path.join(ROOT, "gpurun_out", "bf16_agreement.json")
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    data = {}
+    if os.path.exists(path):
+        data = json.load(open(path))
+    data[key] = value
+    json.dump(data, open(path, "w"), indent=1)
+
+
+@pytest.mark.parametrize("name", ["cfg2", "stress"])
+def test_tc_codebook_agreement_and_feasibility(golden, name):
+    cfg = golden.config(name)
+    agent = cfg.agent()
+    slots = 1024
+    allocs, eps = _inputs(cfg, slots, seed=5)
+    books = {}
+    for prec in ("fp32", "bf16_tc"):
+        eng = CodebookEngine(DevicePolicy(agent.actor, prec), cfg.cell, max_slots=slots)
+        out = eng.run(torch.from_numpy(allocs).cuda(), torch.from_numpy(eps).cuda())
+        eng.check()
+        books[prec] = out.cpu().numpy()
+    tc = books["bf16_tc"]
+    l = cfg.meta["urllc_sc_len"]
+    assert (tc[:, 0] == 0).all()
+    for j in range(1, tc.shape[1]):
+        assert (tc[:, j].sum(axis=1) == j * l).all()
+    assert (tc >= 0).all() and (tc <= allocs[:, None, :]).all()
+    rows = (books["fp32"][:, 1:] == tc[:, 1:]).all(axis=2)
+    rate = float(rows.mean())
+    print(f"[bf16_tc] {name}: codebook-row agreement with fp32 = {rate:.4f}")
+    _record(f"mode_r/{name}", rate)
+    assert rate > (0.95 if name == "cfg2" else 0.5)
+
+
+def test_tc_mode_t_agreement(golden):
+    cfg = golden.config("cfg2")
+    from paper_2506_00167_b200 import substream
+    actor = tree.make_mode_t_actor(cfg.cell, (256, 256), substream(0, "mode-t"))
+    slots = 2
+    allocs, eps = _inputs(cfg, slots, seed=9)
+    mcs = np.random.default_rng(1).integers(0, 6, size=allocs.shape).astype(np.int32)
+    al, mc, ep = (torch.from_numpy(x).cuda() for x in (allocs, mcs, eps))
+    states = {}
+    for prec in ("fp32", "bf16_tc"):
+        states[prec] = tree.build_tree_mode_t(DevicePolicy(actor, prec), cfg.cell, al, mc,
+                                              ep).cpu().numpy()
+    e = cfg.meta["num_embb"]
+    same = (states["fp32"][:, :, :e] == states["bf16_tc"][:, :, :e]).all(axis=2)
+    rate = float(same.mean())
+    leaves = tree.level_offsets(4, 7)[-1]
+    leaf_rate = float(same[:, leaves:].mean())
+    print(f"[bf16_tc] mode-T cfg2: node agreement {rate:.4f}, leaves {leaf_rate:.4f}")
+    _record("mode_t/cfg2_nodes", rate)
+    _record("mode_t/cfg2_leaves", leaf_rate)
+    # levels with < 1024 columns (2 slots: levels 1-4) run fp32 SIMT and agree exactly
+    four = tree.level_offsets(4, 7)[4]
+    assert same[:, :four].all()
+    assert rate > 0.5
