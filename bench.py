@@ -207,7 +207,7 @@ def run_reference(args, rank, world):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": wall * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_block(world, "none"),
+        "config": config_block(world, "none", impl="reference"),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{SLOTS} slots per step (cfg2 geometry codebook + Mode-R "
                                    "tree restatement), all host cores"},
@@ -217,12 +217,14 @@ def run_reference(args, rank, world):
     return 0
 
 
-def config_block(world, l2):
+def config_block(world, l2, impl="ours"):
     return {"workload": "cfg3: 1024 independent slots per rank (N=780, E=10, L=195, cap 4, "
                         "M=7), actor 2x256, stochastic, Mode-R arrival tree"
                         + (", NCCL codebook all-gather" if world > 1 else ""),
             "slots_per_rank": SLOTS, "global_batch": SLOTS * world, "cells": SLOTS * world,
-            "actor": "2x256", "precision": "fp32 actor / fp64 projection",
+            "actor": "2x256",
+            "precision": ("fp32 actor / fp64 projection" if impl == "ours"
+                          else "float64 numpy (oracle port of the reference)"),
             "parallelism": f"cell-sharded x{world}", "l2": l2}
 
 
@@ -317,6 +319,7 @@ def run_ours(args, rank, world, local_rank):
 
         # ---- single-slot latency through the drop-in build_codebook
         lat = latency_run(agent, cell, allocs, args.latency_slots)
+        mode_t = mode_t_run(cell) if (rank == 0 and not args.no_mode_t) else None
 
     mean_ms = float(np.mean(step_ms))
     mean_e2e = float(np.mean(e2e))
@@ -358,6 +361,7 @@ def run_ours(args, rank, world, local_rank):
                 "note": "CodebookEngine.run_host: pinned H2D of schedules+noise, K2/K3/K1, "
                         "D2H of the codebooks (node states stay in HBM)"},
         "latency_us": lat,
+        "mode_t": mode_t,
         "roofline": roofline,
         "cpu_baseline": None if cores_rate is None else {
             "value": cores_rate, "unit": UNIT, "cores": cores, "kind": "port",
@@ -369,6 +373,42 @@ def run_ours(args, rank, world, local_rank):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def mode_t_run(cell, slots=8, reps=3):
+    """North-star Mode T (actor on every arrival-tree node state, cfg2
+    geometry, 2x256 Mode-T actor): tree-batch time for fp32 SIMT and the
+    bf16 tcgen05 path, and their node-decision agreement."""
+    import torch
+    from paper_2506_00167_b200 import DevicePolicy, substream, tree
+    actor = tree.make_mode_t_actor(cell, HIDDEN, substream(0, "mode-t"))
+    allocs, eps = synthetic_inputs(cell, slots, seed=11)
+    mcs = np.random.default_rng(11).integers(0, 6, size=allocs.shape).astype(np.int32)
+    al, mc, ep = (torch.from_numpy(x).cuda() for x in (allocs, mcs, eps))
+    out, states = {}, {}
+    cols = sum((cell.num_branches + 1) ** t for t in range(cell.minislots)) * cell.num_branches
+    sizes = tree.mode_t_sizes(cell, HIDDEN)
+    flops = 2.0 * cols * slots * sum(i * o for i, o in zip(sizes[:-1], sizes[1:]))
+    for prec in ("fp32", "bf16_tc"):
+        pol = DevicePolicy(actor, prec)
+        st = tree.build_tree_mode_t(pol, cell, al, mc, ep)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            tree.build_tree_mode_t(pol, cell, al, mc, ep, out=st)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / reps
+        states[prec] = st.cpu().numpy()[:, :, :cell.num_embb]
+        out[prec] = {"ms_per_tree_batch": ms, "trees_per_s": slots / (ms * 1e-3),
+                     "actor_tflops_effective": flops / (ms * 1e-3) / 1e12}
+        pol.close()
+    same = (states["fp32"] == states["bf16_tc"]).all(axis=2)
+    out.update({"slots": slots, "nodes_per_tree": int(same.shape[1]),
+                "actor_columns_per_tree": cols,
+                "node_agreement_bf16_vs_fp32": float(same.mean())})
+    return out
 
 
 def latency_run(agent, cell, allocs, n):
@@ -413,6 +453,7 @@ def main():
     ap.add_argument("--precision", choices=("fp32", "fp64"), default="fp32")
     ap.add_argument("--no-tree", action="store_true")
     ap.add_argument("--latency-slots", type=int, default=2000)
+    ap.add_argument("--no-mode-t", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -91,6 +91,12 @@ struct cyr_policy {
   size_t tc_bytes = 0;
   long long tc_off[cyr::kMaxLayers] = {};
   int tc_npad[cyr::kMaxLayers] = {};
+  // wider actors (cfg5): per-layer GEMM kernels over HBM activation images,
+  // weight images [n tile of 256][k tile][256 x 128 B]
+  bool tc_wide = false;
+  int tc_act_k = 0;                  // widest hidden width rounded to 64
+  mutable unsigned char* wide_act_d = nullptr;  // Mode-R activation scratch (grown on demand)
+  mutable size_t wide_act_bytes = 0;
   int sm_count = 148;
   // host path
   cudaStream_t stream = nullptr;
@@ -160,12 +166,15 @@ void pack_tc(const cyr_policy& p, const double* src, std::vector<uint8_t>& dst) 
   for (int l = 0; l < p.desc.n_layers; ++l) {
     const cyr::LayerDesc& L = p.desc.layer[l];
     const size_t tile_bytes = (size_t)p.tc_npad[l] * 128;
+    const int kt = (L.in + 63) / 64;
     for (int n = 0; n < L.out; ++n)
       for (int k = 0; k < L.in; ++k) {
         const int t = k / 64, kk = k % 64;
         const int chunk = (kk * 2) >> 4;
-        const size_t byte = (size_t)p.tc_off[l] + t * tile_bytes + (size_t)(n >> 3) * 1024 +
-                            (n & 7) * 128 + ((chunk ^ (n & 7)) << 4) + ((kk * 2) & 15);
+        const int nt = p.tc_wide ? n / 256 : 0, r = p.tc_wide ? n % 256 : n;
+        const size_t tile = p.tc_wide ? ((size_t)nt * kt + t) * (256 * 128) : t * tile_bytes;
+        const size_t byte = (size_t)p.tc_off[l] + tile + (size_t)(r >> 3) * 1024 + (r & 7) * 128 +
+                            ((chunk ^ (r & 7)) << 4) + ((kk * 2) & 15);
         const uint16_t v = f32_to_bf16_rne((float)src[off + (size_t)n * L.in + k]);
         std::memcpy(&dst[byte], &v, 2);
       }
@@ -174,7 +183,7 @@ void pack_tc(const cyr_policy& p, const double* src, std::vector<uint8_t>& dst) 
 }
 
 int upload(cyr_policy* p, const double* blob) {
-  if (p->tc_ok) {
+  if (p->tc_ok || p->tc_wide) {
     std::vector<uint8_t> h;
     pack_tc(*p, blob, h);
     CYR_CUDA(cudaMemcpy(p->tc_blob_d, h.data(), h.size(), cudaMemcpyHostToDevice));
@@ -250,9 +259,47 @@ constexpr long long kTcMinCols = 1024;  // below: the MLP is not a dense GEMM
 
 int simt_precision(const cyr_policy* p) { return p->precision == CYR_FP64 ? CYR_FP64 : CYR_FP32; }
 
+// activation ping-pong bytes of the wide tensor-core actor for `cols` columns
+size_t wide_act_bytes(const cyr_policy* p, long long cols) {
+  if (!p->tc_wide) return 0;
+  return 2 * (size_t)((cols + 127) / 128) * 128 * p->tc_act_k * 2;
+}
+
+// wide actor: one tensor-core GEMM kernel per layer (actor_tc.cu)
+int launch_actor_wide(const cyr_policy* p, const int32_t* alloc, int S, int N, int cap, float* raw,
+                      unsigned char* act, long long cols, int mode_t, const int32_t* mcs,
+                      const int16_t* node, int M, int tau, int parents, long long nodes,
+                      long long parent_off, int epad, double mcs_scale, cudaStream_t st) {
+  unsigned char* buf[2] = {act, act + wide_act_bytes(p, cols) / 2};
+  for (int l = 0; l < p->desc.n_layers; ++l) {
+    const int rc = cyr_launch_actor_tc_layer(
+        p->desc, p->tc_blob_d, p->tc_off[l], p->tc_npad[l], l, static_cast<const float*>(p->blob_d),
+        alloc, S, p->E, N, cap, raw, buf[(l + 1) & 1], buf[l & 1], mode_t, mcs, node, M, tau,
+        parents, nodes, parent_off, epad, mcs_scale, st);
+    if (rc != CYR_OK) return rc;
+  }
+  return CYR_OK;
+}
+
 // Mode-R actor for S slots with the policy's precision choice
 int launch_actor_policy(const cyr_policy* p, const int32_t* alloc, int S, int N, int cap, void* raw,
                         cudaStream_t st) {
+  if (p->tc_wide && (long long)S * cap >= kTcMinCols) {
+    const long long cols = (long long)S * cap;
+    const size_t need = wide_act_bytes(p, cols);
+    if (need > p->wide_act_bytes) {  // grown outside any capture (it synchronises)
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(st, &cs);
+      if (cs != cudaStreamCaptureStatusNone) return CYR_UNSUPPORTED;
+      cudaFree(p->wide_act_d);
+      p->wide_act_d = nullptr;
+      p->wide_act_bytes = 0;
+      if (cudaMalloc(&p->wide_act_d, need) != cudaSuccess) return CYR_CUDA_ERROR;
+      p->wide_act_bytes = need;
+    }
+    return launch_actor_wide(p, alloc, S, N, cap, static_cast<float*>(raw), p->wide_act_d, cols, 0,
+                             nullptr, nullptr, 0, 0, 0, 0, 0, 0, 1.0, st);
+  }
   if (p->tc_ok && (long long)S * cap >= kTcMinCols)
     return cyr_launch_actor_tc(p->desc, p->tc_blob_d, p->tc_off, p->tc_npad,
                                static_cast<const float*>(p->blob_d), alloc, S, p->E, N, cap,
@@ -367,8 +414,18 @@ int cyr_policy_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
       p->tc_off[l] = (long long)tb;
       tb += (size_t)((L.in + 63) / 64) * npad * 128;
     }
+    if (!p->tc_ok && n_sizes >= 3 && p->desc.layer[0].in <= 64) {
+      p->tc_wide = true;  // layer-by-layer GEMMs: any hidden width
+      tb = 0;
+      for (int l = 0; l < n_sizes - 1; ++l) {
+        const cyr::LayerDesc& L = p->desc.layer[l];
+        p->tc_off[l] = (long long)tb;
+        tb += (size_t)((p->tc_npad[l] + 255) / 256) * ((L.in + 63) / 64) * 256 * 128;
+        if (l < n_sizes - 2) p->tc_act_k = std::max(p->tc_act_k, (L.out + 63) / 64 * 64);
+      }
+    }
     p->tc_bytes = tb;
-    if (p->tc_ok) {
+    if (p->tc_ok || p->tc_wide) {
       cudaError_t e2 = cudaMalloc(&p->tc_blob_d, tb);
       if (e2 != cudaSuccess) {
         delete p;
@@ -447,6 +504,7 @@ int cyr_policy_destroy(cyr_policy* p) {
   if (p->ev1) cudaEventDestroy(p->ev1);
   cudaFree(p->blob_d);
   cudaFree(p->tc_blob_d);
+  cudaFree(p->wide_act_d);
   delete p;
   return CYR_OK;
 }
@@ -769,7 +827,8 @@ size_t cyr_tree_mode_t_workspace_bytes(const cyr_policy* p, int32_t S, int32_t c
   if (!p || S < 0 || cap < 1 || M < 1) return 0;
   long long widest = 1;
   for (int t = 1; t < M; ++t) widest *= (cap + 1);  // parents of the deepest level
-  return (size_t)S * widest * cap * 2 * p->E * p->elem;
+  const size_t raw = ((size_t)S * widest * cap * 2 * p->E * p->elem + 255) / 256 * 256;
+  return raw + wide_act_bytes(p, (long long)S * widest * cap);
 }
 
 int cyr_tree_mode_t_device(const cyr_policy* p, const int32_t* alloc, const int32_t* mcs,
@@ -790,7 +849,16 @@ int cyr_tree_mode_t_device(const cyr_policy* p, const int32_t* alloc, const int3
   long long parents = 1, level_off = 0, prev_off = -1;
   for (int tau = 1; tau <= M; ++tau) {
     // K2: the actor on every (parent, branch) column of this level
-    if (p->tc_ok && (long long)S * parents * cap >= kTcMinCols)
+    const long long cols = (long long)S * parents * cap;
+    if (p->tc_wide && cols >= kTcMinCols) {
+      long long widest = 1;
+      for (int t = 1; t < M; ++t) widest *= R;
+      unsigned char* act = static_cast<unsigned char*>(workspace) +
+                           ((size_t)S * widest * cap * 2 * p->E * p->elem + 255) / 256 * 256;
+      rc = launch_actor_wide(p, alloc, S, N, cap, static_cast<float*>(workspace), act, cols, 1, mcs,
+                             node_state, M, tau, (int)parents, nodes, prev_off, epad, mcs_scale,
+                             st);
+    } else if (p->tc_ok && cols >= kTcMinCols)
       rc = cyr_launch_actor_tc(p->desc, p->tc_blob_d, p->tc_off, p->tc_npad,
                                static_cast<const float*>(p->blob_d), alloc, S, p->E, N, cap,
                                static_cast<float*>(workspace), 1, mcs, node_state, M, tau,

@@ -284,6 +284,157 @@ __global__ void __launch_bounds__(kTcThreads, 1) actor_tc_kernel(const TcLaunch 
   }
 }
 
+// ------------------------------------------------------------- wide layers
+// Actors wider than one MMA tile (cfg5: 3 x 1024) run layer by layer:
+// grid (128-column block, 256-output tile); D[128 x 256] accumulates over
+// K tiles streamed by a 3-slot ring of {activation tile 16 KB, weight tile
+// 32 KB} bulk copies.  Activations live in HBM as the same SW128 K-major
+// tile images the MMA reads ([col block][k tile][128 x 64] bf16), written by
+// the previous layer's epilogue — so every operand load is a plain TMA bulk
+// copy.  The first layer builds its A tile from the features in shared
+// memory (in0 <= 64); the last writes fp32 logits raw[col][2E].
+constexpr int kWideStageBytes = kTcM * 128 + 256 * 128;  // A + B of one K tile
+
+struct TcLayerLaunch {
+  TcLaunch base;        // features / raw / Mode-T fields (desc, tc_* unused beyond layer l)
+  int l;                // layer index
+  int in, out, npad;    // layer geometry
+  int kt;               // K tiles of this layer
+  long long w_off;      // byte offset of this layer's images: [n tile][k tile][rows x 128 B]
+  const unsigned char* act_in;   // [col blocks][kt][16 KB]   (unused for the first layer)
+  unsigned char* act_out;        // [col blocks][out/64][16 KB] (unused for the last layer)
+  int first, last;
+};
+
+template <bool FIRST, bool LAST>
+__global__ void __launch_bounds__(kTcThreads, 1) actor_tc_layer_kernel(const TcLayerLaunch q) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  unsigned char* ring = base;  // kTcSlots x (A 16 KB | B 32 KB)
+  uint64_t* bar_full = reinterpret_cast<uint64_t*>(ring + kTcSlots * kWideStageBytes);
+  uint64_t* bar_free = bar_full + kTcSlots;
+  uint64_t* bar_mma = bar_free + kTcSlots;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_mma + 1);
+  const TcLaunch& p = q.base;
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int cb = blockIdx.x, nt = blockIdx.y;
+  const int rows_n = min(256, q.npad - nt * 256);  // N of this tile (multiple of 16)
+  const uint32_t b_bytes = (uint32_t)rows_n * 128;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kTcSlots; ++i) {
+      mbar_init(&bar_full[i], 1);
+      mbar_init(&bar_free[i], 1);
+    }
+    mbar_init(bar_mma, 1);
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  auto issue = [&](int t) {  // thread 0: K tile t into slot t % kTcSlots
+    if (t >= q.kt) return;
+    const int slot = t % kTcSlots;
+    if (t >= kTcSlots) mbar_wait(&bar_free[slot], (uint32_t)(((t / kTcSlots) - 1) & 1));
+    unsigned char* a_dst = ring + (size_t)slot * kWideStageBytes;
+    unsigned char* b_dst = a_dst + kTcM * 128;
+    const uint32_t a_bytes = FIRST ? 0u : (uint32_t)(kTcM * 128);
+    mbar_expect_tx(&bar_full[slot], a_bytes + b_bytes);
+    if (!FIRST)
+      bulk_g2s(a_dst, q.act_in + ((long long)cb * q.kt + t) * (kTcM * 128), a_bytes,
+               &bar_full[slot]);
+    bulk_g2s(b_dst, p.tc_blob + q.w_off + ((long long)nt * q.kt + t) * (256 * 128), b_bytes,
+             &bar_full[slot]);
+  };
+  if (tid == 0)
+    for (int t = 0; t < kTcSlots - 1; ++t) issue(t);
+
+  if (FIRST) {  // the single A tile: features of column c0 + tid, built in slot 0
+    unsigned char* a = ring;
+    const int col = cb * kTcM + tid;
+    for (int k = 0; k < 64; k += 2) {
+      float v0 = 0.f, v1 = 0.f;
+      if (col < p.ncols) {
+        if (k < q.in) v0 = (float)tc_feature(p, col, k);
+        if (k + 1 < q.in) v1 = (float)tc_feature(p, col, k + 1);
+      }
+      *reinterpret_cast<__nv_bfloat162*>(a + sw128_offset(tid, k)) = __floats2bfloat162_rn(v0, v1);
+    }
+    fence_proxy_async_smem();
+  }
+  __syncthreads();
+
+  const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(rows_n >> 3) << 17) |
+                         ((uint32_t)(kTcM >> 4) << 24);
+  if (tid == 0) {
+    for (int t = 0; t < q.kt; ++t) {
+      const int slot = t % kTcSlots;
+      mbar_wait(&bar_full[slot], (uint32_t)((t / kTcSlots) & 1));
+      tc_fence_after();
+      const uint32_t a_addr = smem_u32(ring + (size_t)slot * kWideStageBytes);
+      const uint32_t b_addr = a_addr + kTcM * 128;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+        tc_mma(tmem, umma_desc_sw128(a_addr + ks * 32), umma_desc_sw128(b_addr + ks * 32), idesc,
+               (t > 0 || ks > 0) ? 1 : 0);
+      tc_commit(&bar_free[slot]);
+      issue(t + kTcSlots - 1);
+    }
+    tc_commit(bar_mma);
+  }
+  mbar_wait(bar_mma, 0);
+  tc_fence_after();
+  const int col = cb * kTcM + tid;
+  const float* bias = p.bias + p.desc.layer[q.l].b_off;
+  for (int n0 = 0; n0 < rows_n; n0 += 32) {
+    uint32_t r[32];
+    tc_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)n0, r);
+    const int o0 = nt * 256 + n0;
+    if (LAST) {
+      if (col < p.ncols)
+        for (int j = 0; j < 32; ++j) {
+          const int o = o0 + j;
+          if (o < q.out) p.raw[(long long)col * q.out + o] = __uint_as_float(r[j]) + bias[o];
+        }
+    } else {
+      // next layer's A image: K tile o0 / 64 of column block cb
+      const int kt_next = (q.out + 63) / 64;
+      unsigned char* img = q.act_out + ((long long)cb * kt_next + (o0 >> 6)) * (kTcM * 128);
+      uint32_t packed[16];
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const int o = o0 + j;
+        float v0 = o < q.out ? __uint_as_float(r[j]) + bias[o] : 0.f;
+        float v1 = o + 1 < q.out ? __uint_as_float(r[j + 1]) + bias[o + 1] : 0.f;
+        v0 = v0 > 0.f ? v0 : 0.f;
+        v1 = v1 > 0.f ? v1 : 0.f;
+        const __nv_bfloat162 pr = __floats2bfloat162_rn(v0, v1);
+        packed[j / 2] = *reinterpret_cast<const uint32_t*>(&pr);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c)  // four 16-byte chunks of this row
+        *reinterpret_cast<uint4*>(img + sw128_offset(tid, (o0 & 63) + c * 8)) =
+            make_uint4(packed[4 * c], packed[4 * c + 1], packed[4 * c + 2], packed[4 * c + 3]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  }
+}
+
 }  // namespace cyr
 
 size_t cyr_tc_smem_bytes() {
@@ -336,5 +487,76 @@ int cyr_launch_actor_tc(const cyr::ActorDesc& desc, const unsigned char* tc_blob
   }
   const int blocks = (p.ncols + cyr::kTcM - 1) / cyr::kTcM;
   cyr::actor_tc_kernel<<<blocks, cyr::kTcThreads, smem, stream>>>(p);
+  return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
+}
+
+size_t cyr_tc_wide_smem_bytes() {
+  return 1024 + (size_t)cyr::kTcSlots * cyr::kWideStageBytes + (2 * cyr::kTcSlots + 1) * 8 + 16;
+}
+
+// one wide layer (see actor_tc_layer_kernel); act buffers are tile images
+int cyr_launch_actor_tc_layer(const cyr::ActorDesc& desc, const unsigned char* tc_blob,
+                              long long w_off, int npad, int l, const float* bias_blob,
+                              const int32_t* alloc, int S, int E, int N, int cap, float* raw,
+                              const unsigned char* act_in, unsigned char* act_out, int mode_t,
+                              const int32_t* mcs, const int16_t* node, int M, int tau,
+                              int parents, long long nodes_per_slot, long long parent_off,
+                              int epad, double mcs_scale, cudaStream_t stream) {
+  cyr::TcLayerLaunch q{};
+  cyr::TcLaunch& p = q.base;
+  p.desc = desc;
+  p.tc_blob = tc_blob;
+  p.bias = bias_blob;
+  p.alloc = alloc;
+  p.raw = raw;
+  p.S = S;
+  p.E = E;
+  p.N = N;
+  p.cap = cap;
+  const long long ncols = mode_t ? (long long)S * parents * cap : (long long)S * cap;
+  if (ncols <= 0) return CYR_OK;
+  if (ncols >= (1ll << 31)) return CYR_UNSUPPORTED;
+  p.ncols = (int)ncols;
+  p.mode_t = mode_t;
+  p.node = node;
+  p.mcs = mcs;
+  p.nodes_per_slot = nodes_per_slot;
+  p.parent_off = parent_off;
+  p.parents = parents;
+  p.tau = tau;
+  p.M = M;
+  p.epad = epad;
+  p.mcs_scale = mcs_scale;
+  const cyr::LayerDesc& L = desc.layer[l];
+  q.l = l;
+  q.in = L.in;
+  q.out = L.out;
+  q.npad = npad;
+  q.first = l == 0;
+  q.last = l == desc.n_layers - 1;
+  q.kt = q.first ? 1 : (L.in + 63) / 64;
+  if (q.first && L.in > 64) return CYR_UNSUPPORTED;
+  q.w_off = w_off;
+  q.act_in = act_in;
+  q.act_out = act_out;
+  const size_t smem = cyr_tc_wide_smem_bytes();
+  const dim3 grid((unsigned)((ncols + cyr::kTcM - 1) / cyr::kTcM), (unsigned)((npad + 255) / 256));
+#define CYR_WIDE(F, LST)                                                                       \
+  do {                                                                                         \
+    static bool set = false;                                                                   \
+    if (!set) {                                                                                \
+      if (cudaFuncSetAttribute(cyr::actor_tc_layer_kernel<F, LST>,                             \
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=     \
+          cudaSuccess)                                                                         \
+        return CYR_CUDA_ERROR;                                                                 \
+      set = true;                                                                              \
+    }                                                                                          \
+    cyr::actor_tc_layer_kernel<F, LST><<<grid, cyr::kTcThreads, smem, stream>>>(q);            \
+  } while (0)
+  if (q.first && q.last) return CYR_UNSUPPORTED;
+  if (q.first) CYR_WIDE(true, false);
+  else if (q.last) CYR_WIDE(false, true);
+  else CYR_WIDE(false, false);
+#undef CYR_WIDE
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
 }

@@ -9,7 +9,7 @@ namespace cyr {
 // A CTA holds `spc` whole slots (<= 32 rows); 8 warps stride over the rows
 // in the per-row phases and warp 0 runs every slot's coupled loop at once.
 template <typename RawT>
-__global__ void __launch_bounds__(256) codebook_kernel(
+__global__ void __launch_bounds__(256, 4) codebook_kernel(
     const RawT* __restrict__ raw, const int32_t* __restrict__ alloc,
     const double* __restrict__ eps, int S, int spc, int E, int L, int cap,
     int32_t* __restrict__ cb, double* __restrict__ m_out, double* __restrict__ nu_out,
@@ -55,7 +55,7 @@ struct TreeIO {
 };
 
 template <typename RawT>
-__global__ void __launch_bounds__(256) tree_level_kernel(const RawT* __restrict__ raw, TreeIO io,
+__global__ void __launch_bounds__(256, 4) tree_level_kernel(const RawT* __restrict__ raw, TreeIO io,
                                                          long long groups, int gpc, int L,
                                                          int32_t* __restrict__ status) {
   __shared__ RowScratch sc;

@@ -36,7 +36,7 @@ def _logits(pol, cell, allocs):
     return raw.double().cpu().numpy()
 
 
-@pytest.mark.parametrize("name", ["cfg2", "stress", "cfg1"])
+@pytest.mark.parametrize("name", ["cfg2", "stress", "cfg1", "cfg5"])
 def test_tc_logits_close_to_fp32(golden, name):
     cfg = golden.config(name)
     agent = cfg.agent()
@@ -109,3 +109,38 @@ def test_tc_mode_t_agreement(golden):
     four = tree.level_offsets(4, 7)[4]
     assert same[:, :four].all()
     assert rate > 0.5
+
+
+def test_tc_wide_mode_t_cfg5(golden):
+    """cfg5's 3 x 1024 actor runs the per-layer tensor-core GEMMs (HBM
+    activation images); compare its Mode-T tree with fp32 SIMT."""
+    cfg = golden.config("cfg5")
+    from paper_2506_00167_b200 import substream
+    actor = tree.make_mode_t_actor(cfg.cell, (1024, 1024, 1024), substream(0, "mode-t"))
+    allocs, eps = _inputs(cfg, 1, seed=11)
+    mcs = np.random.default_rng(2).integers(0, 6, size=allocs.shape).astype(np.int32)
+    al, mc, ep = (torch.from_numpy(x).cuda() for x in (allocs, mcs, eps))
+    states = {}
+    for prec in ("fp32", "bf16_tc"):
+        states[prec] = tree.build_tree_mode_t(DevicePolicy(actor, prec), cfg.cell, al, mc,
+                                              ep).cpu().numpy()
+    e = cfg.meta["num_embb"]
+    same = (states["fp32"][:, :, :e] == states["bf16_tc"][:, :, :e]).all(axis=2)
+    rate = float(same.mean())
+    print(f"[bf16_tc] mode-T cfg5: node agreement {rate:.4f}")
+    _record("mode_t/cfg5_nodes", rate)
+    # levels 1-3 (< 1024 columns) run fp32 SIMT and agree exactly
+    four = tree.level_offsets(6, 7)[3]
+    assert same[:, :four].all()
+    assert rate > 0.5
+    # every child satisfies the per-level column contract against its parent
+    l = cfg.meta["urllc_sc_len"]
+    st = states["bf16_tc"][0, :, :e].astype(np.int64)
+    offs = tree.level_offsets(6, 7)
+    for t in range(1, 7):
+        child = st[offs[t]:offs[t] + 7 ** (t + 1)].reshape(-1, 7, e)
+        parent = st[offs[t - 1]:offs[t - 1] + 7 ** t]
+        grants = child - parent[:, None, :]
+        assert (grants[:, 0] == 0).all()
+        for k in range(1, 7):
+            assert (grants[:, k].sum(axis=1) == k * l).all()
