@@ -284,7 +284,7 @@ int launch_actor_wide(const cyr_policy* p, const int32_t* alloc, int S, int N, i
 // Mode-R actor for S slots with the policy's precision choice
 int launch_actor_policy(const cyr_policy* p, const int32_t* alloc, int S, int N, int cap, void* raw,
                         cudaStream_t st) {
-  if (p->tc_wide && (long long)S * cap >= kTcMinCols) {
+  if (p->tc_wide) {  // any width: the SIMT path streams MBs of weights per launch
     const long long cols = (long long)S * cap;
     const size_t need = wide_act_bytes(p, cols);
     if (need > p->wide_act_bytes) {  // grown outside any capture (it synchronises)
@@ -850,7 +850,7 @@ int cyr_tree_mode_t_device(const cyr_policy* p, const int32_t* alloc, const int3
   for (int tau = 1; tau <= M; ++tau) {
     // K2: the actor on every (parent, branch) column of this level
     const long long cols = (long long)S * parents * cap;
-    if (p->tc_wide && cols >= kTcMinCols) {
+    if (p->tc_wide) {
       long long widest = 1;
       for (int t = 1; t < M; ++t) widest *= R;
       unsigned char* act = static_cast<unsigned char*>(workspace) +

@@ -99,34 +99,71 @@ __device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ double tc_feature(const TcLaunch& p, int col, int i) {
-  if (!p.mode_t) {
-    const int s = col / p.cap, j = col % p.cap + 1;
-    return (i < p.E) ? (double)p.alloc[(long long)s * p.E + i] / (double)p.N
-                     : (double)j / (double)p.cap;
-  }
+
+
+// K tile t of the layer-1 A operand for batch column `col`, written as row
+// `row` of the SW128 image `a` (zeros past in0).  Feature i of the actor
+// input, rounded to bf16 from the float64 value (double)x / (double)scale:
+//   Mode R: [n/N (E), j/cap]
+//   Mode T: [n/N (E), k/cap, cum/N (E), mcs/mcs_scale (E), arrivals/(M*cap),
+//            (tau-1)/M]
+// The column's indices are decoded once and the per-user loads are issued in
+// independent batches of four, so their latencies overlap.
+__device__ __forceinline__ void tc_put(unsigned char* a, int row, int t, int i, double x) {
+  if (i >= t * 64 && i < t * 64 + 64)
+    *reinterpret_cast<__nv_bfloat16*>(a + sw128_offset(row, i - t * 64)) =
+        __float2bfloat16_rn((float)x);
+}
+
+__device__ __forceinline__ void tc_feature_tile(const TcLaunch& p, int col, int t,
+                                                unsigned char* a, int row) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    *reinterpret_cast<uint4*>(a + sw128_offset(row, c * 8)) = make_uint4(0, 0, 0, 0);
+  if (col >= p.ncols) return;
+  const int E = p.E;
   const int k = col % p.cap + 1;
   const int g = col / p.cap;
-  const int s = g / p.parents;
-  const int q = g - s * p.parents;
-  const int E = p.E;
-  if (i < E) return (double)p.alloc[(long long)s * E + i] / (double)p.N;
-  if (i == E) return (double)k / (double)p.cap;
-  if (i <= 2 * E) {
-    if (p.parent_off < 0) return 0.0;
-    const long long rec = (long long)s * p.nodes_per_slot + p.parent_off + q;
-    return (double)p.node[rec * p.epad + (i - E - 1)] / (double)p.N;
+  const int s = p.mode_t ? g / p.parents : g;
+  const int q = p.mode_t ? g - s * p.parents : 0;
+  const int32_t* al = p.alloc + (long long)s * E;
+  const int32_t* mc = p.mode_t ? p.mcs + (long long)s * E : nullptr;
+  const int16_t* nd =
+      (p.mode_t && p.parent_off >= 0)
+          ? p.node + ((long long)s * p.nodes_per_slot + p.parent_off + q) * p.epad
+          : nullptr;
+  const double inv_n = (double)p.N;
+  for (int e0 = 0; e0 < E; e0 += 4) {
+    int av[4], mv[4], nv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int e = e0 + j < E ? e0 + j : E - 1;
+      av[j] = al[e];
+      mv[j] = mc ? mc[e] : 0;
+      nv[j] = nd ? nd[e] : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int e = e0 + j;
+      if (e < E) {
+        tc_put(a, row, t, e, (double)av[j] / inv_n);
+        if (p.mode_t) {
+          tc_put(a, row, t, E + 1 + e, (double)nv[j] / inv_n);
+          tc_put(a, row, t, 2 * E + 1 + e, (double)mv[j] / p.mcs_scale);
+        }
+      }
+    }
   }
-  if (i <= 3 * E) return (double)p.mcs[(long long)s * E + (i - 2 * E - 1)] / p.mcs_scale;
-  if (i == 3 * E + 1) {
+  tc_put(a, row, t, E, (double)k / (double)p.cap);
+  if (p.mode_t) {
     int arrivals = 0, x = q;
     for (int d = 1; d < p.tau; ++d) {
       arrivals += x % (p.cap + 1);
       x /= (p.cap + 1);
     }
-    return (double)arrivals / (double)(p.M * p.cap);
+    tc_put(a, row, t, 3 * E + 1, (double)arrivals / (double)(p.M * p.cap));
+    tc_put(a, row, t, 3 * E + 2, (double)(p.tau - 1) / (double)p.M);
   }
-  return (double)(p.tau - 1) / (double)p.M;
 }
 
 __global__ void __launch_bounds__(kTcThreads, 1) actor_tc_kernel(const TcLaunch p) {
@@ -142,7 +179,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) actor_tc_kernel(const TcLaunch 
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_mma + 1);
 
   const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
+  const int warp = tid >> 5;
   const int c0 = blockIdx.x * kTcM;
   const int nl = p.desc.n_layers;
 
@@ -195,22 +232,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) actor_tc_kernel(const TcLaunch 
 
   // layer-1 A tile(s): thread tid builds batch column c0 + tid
   {
-    const int in0 = p.desc.layer[0].in;
-    const int kt0 = (in0 + 63) / 64;
-    const int col = c0 + tid;
-    for (int t = 0; t < kt0; ++t) {
-      unsigned char* a = a_tiles + t * kTcM * 128;
-      for (int k = 0; k < 64; k += 2) {
-        const int i = t * 64 + k;
-        float v0 = 0.f, v1 = 0.f;
-        if (col < p.ncols) {
-          if (i < in0) v0 = (float)tc_feature(p, col, i);
-          if (i + 1 < in0) v1 = (float)tc_feature(p, col, i + 1);
-        }
-        const __nv_bfloat162 pr = __floats2bfloat162_rn(v0, v1);
-        *reinterpret_cast<__nv_bfloat162*>(a + sw128_offset(tid, k)) = pr;
-      }
-    }
+    const int kt0 = (p.desc.layer[0].in + 63) / 64;
+    for (int t = 0; t < kt0; ++t) tc_feature_tile(p, c0 + tid, t, a_tiles + t * kTcM * 128, tid);
   }
   fence_proxy_async_smem();
   __syncthreads();
@@ -285,153 +308,242 @@ __global__ void __launch_bounds__(kTcThreads, 1) actor_tc_kernel(const TcLaunch 
 }
 
 // ------------------------------------------------------------- wide layers
-// Actors wider than one MMA tile (cfg5: 3 x 1024) run layer by layer:
-// grid (128-column block, 256-output tile); D[128 x 256] accumulates over
-// K tiles streamed by a 3-slot ring of {activation tile 16 KB, weight tile
-// 32 KB} bulk copies.  Activations live in HBM as the same SW128 K-major
-// tile images the MMA reads ([col block][k tile][128 x 64] bf16), written by
-// the previous layer's epilogue — so every operand load is a plain TMA bulk
-// copy.  The first layer builds its A tile from the features in shared
-// memory (in0 <= 64); the last writes fp32 logits raw[col][2E].
-constexpr int kWideStageBytes = kTcM * 128 + 256 * 128;  // A + B of one K tile
+// Actors wider than one MMA tile (cfg5: 3 x 1024) run layer by layer, each
+// layer a persistent warp-specialised tcgen05 GEMM:
+//   warp 4  producer: TMA bulk copies of {A tile 16 KB, B tile <= 32 KB}
+//           K-tile stages into a ring (FIRST: streams only B);
+//   warps 6-9 (FIRST only) feature builders: thread = row of the block's
+//           feature A tile, double-buffered across column blocks;
+//   warp 5  MMA issuer (one lane): D[128 x 256] per (column block, n tile)
+//           into one of two TMEM accumulators (2 x 256 columns);
+//   warps 0-3 epilogue: tcgen05.ld, bias (+ReLU), bf16, into a 16 KB
+//           staging image, TMA bulk store (LAST: fp32 logits raw[col][2E]).
+// Each CTA walks column blocks with a grid stride and every n tile of a block
+// back to back, so the block's A tiles are L2-hot for tiles 2..4 and the
+// epilogue of one tile overlaps the MMAs of the next.  With fewer blocks
+// than SMs (the top tree levels) the n tiles of a block are split over
+// `split` CTAs instead, so a small level is not one SM streaming all weights.  Activations
+// live in HBM as the SW128 K-major images the MMA reads: [col block][k tile]
+// [128 x 64] bf16, written by the previous layer's epilogue.
+constexpr int kWideThreads = 192;       // + 128 feature builders for the first layer
+constexpr int kWideFirstThreads = 320;
+constexpr int kWideImage = kTcM * 128;  // one [128 x 64] bf16 image, 16 KB
+constexpr int kWideMaxSlots = 8;
 
-struct TcLayerLaunch {
-  TcLaunch base;        // features / raw / Mode-T fields (desc, tc_* unused beyond layer l)
-  int l;                // layer index
-  int in, out, npad;    // layer geometry
-  int kt;               // K tiles of this layer
-  long long w_off;      // byte offset of this layer's images: [n tile][k tile][rows x 128 B]
-  const unsigned char* act_in;   // [col blocks][kt][16 KB]   (unused for the first layer)
-  unsigned char* act_out;        // [col blocks][out/64][16 KB] (unused for the last layer)
-  int first, last;
+struct TcWideLaunch {
+  TcLaunch base;  // features / raw / Mode-T fields
+  int l, in, out, npad;
+  int kt;          // K tiles of this layer (1 for the first)
+  int nts;         // n tiles of 256
+  int ncb;         // column blocks of 128
+  int nslots;      // ring depth
+  int split;       // CTAs per column block (n tiles divided between them)
+  uint32_t slot_bytes, a_bytes;  // per stage (a_bytes = 0 for the first layer)
+  long long w_off;  // this layer's images: [n tile][k tile][256 x 128 B]
+  const unsigned char* act_in;  // [ncb][kt][16 KB]
+  unsigned char* act_out;       // [ncb][ceil(out/64)][16 KB]
 };
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void epi_sync() {  // the 128 epilogue threads only
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
 template <bool FIRST, bool LAST>
-__global__ void __launch_bounds__(kTcThreads, 1) actor_tc_layer_kernel(const TcLayerLaunch q) {
+__global__ void __launch_bounds__(kWideFirstThreads, 1) actor_tc_wide_kernel(const TcWideLaunch q) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  unsigned char* ring = base;  // kTcSlots x (A 16 KB | B 32 KB)
-  uint64_t* bar_full = reinterpret_cast<uint64_t*>(ring + kTcSlots * kWideStageBytes);
-  uint64_t* bar_free = bar_full + kTcSlots;
-  uint64_t* bar_mma = bar_free + kTcSlots;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_mma + 1);
+  unsigned char* ring = base;
+  unsigned char* feat = ring + (size_t)q.nslots * q.slot_bytes;  // FIRST: 2 x 16 KB
+  unsigned char* stg = feat + (FIRST ? 2 * kWideImage : 0);      // !LAST: 2 x 16 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg + (LAST ? 0 : 2 * kWideImage));
+  uint64_t* full = bars;
+  uint64_t* freeb = full + kWideMaxSlots;
+  uint64_t* tfull = freeb + kWideMaxSlots;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* ffull = tempty + 2;
+  uint64_t* ffree = ffull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ffree + 2);
   const TcLaunch& p = q.base;
-
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int cb = blockIdx.x, nt = blockIdx.y;
-  const int rows_n = min(256, q.npad - nt * 256);  // N of this tile (multiple of 16)
-  const uint32_t b_bytes = (uint32_t)rows_n * 128;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NS = q.nslots;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(256));
+                 "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid == 0) {
-    for (int i = 0; i < kTcSlots; ++i) {
-      mbar_init(&bar_full[i], 1);
-      mbar_init(&bar_free[i], 1);
+  if (tid == 32) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&freeb[i], 1);
     }
-    mbar_init(bar_mma, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+      mbar_init(&ffull[i], 4);
+      mbar_init(&ffree[i], 1);
+    }
     fence_mbar_init();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int last_nt_rows = q.npad - (q.nts - 1) * 256;
+  // this CTA: column blocks cb0, cb0 + cbs, ...; n tiles [nt0, nt1) of each
+  const int sp = blockIdx.x % q.split;
+  const int cb0 = blockIdx.x / q.split, cbs = gridDim.x / q.split;
+  const int nt0 = sp * q.nts / q.split, nt1 = (sp + 1) * q.nts / q.split;
 
-  auto issue = [&](int t) {  // thread 0: K tile t into slot t % kTcSlots
-    if (t >= q.kt) return;
-    const int slot = t % kTcSlots;
-    if (t >= kTcSlots) mbar_wait(&bar_free[slot], (uint32_t)(((t / kTcSlots) - 1) & 1));
-    unsigned char* a_dst = ring + (size_t)slot * kWideStageBytes;
-    unsigned char* b_dst = a_dst + kTcM * 128;
-    const uint32_t a_bytes = FIRST ? 0u : (uint32_t)(kTcM * 128);
-    mbar_expect_tx(&bar_full[slot], a_bytes + b_bytes);
-    if (!FIRST)
-      bulk_g2s(a_dst, q.act_in + ((long long)cb * q.kt + t) * (kTcM * 128), a_bytes,
-               &bar_full[slot]);
-    bulk_g2s(b_dst, p.tc_blob + q.w_off + ((long long)nt * q.kt + t) * (256 * 128), b_bytes,
-             &bar_full[slot]);
-  };
-  if (tid == 0)
-    for (int t = 0; t < kTcSlots - 1; ++t) issue(t);
-
-  if (FIRST) {  // the single A tile: features of column c0 + tid, built in slot 0
-    unsigned char* a = ring;
-    const int col = cb * kTcM + tid;
-    for (int k = 0; k < 64; k += 2) {
-      float v0 = 0.f, v1 = 0.f;
-      if (col < p.ncols) {
-        if (k < q.in) v0 = (float)tc_feature(p, col, k);
-        if (k + 1 < q.in) v1 = (float)tc_feature(p, col, k + 1);
-      }
-      *reinterpret_cast<__nv_bfloat162*>(a + sw128_offset(tid, k)) = __floats2bfloat162_rn(v0, v1);
-    }
-    fence_proxy_async_smem();
-  }
-  __syncthreads();
-
-  const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(rows_n >> 3) << 17) |
-                         ((uint32_t)(kTcM >> 4) << 24);
-  if (tid == 0) {
-    for (int t = 0; t < q.kt; ++t) {
-      const int slot = t % kTcSlots;
-      mbar_wait(&bar_full[slot], (uint32_t)((t / kTcSlots) & 1));
-      tc_fence_after();
-      const uint32_t a_addr = smem_u32(ring + (size_t)slot * kWideStageBytes);
-      const uint32_t b_addr = a_addr + kTcM * 128;
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks)
-        tc_mma(tmem, umma_desc_sw128(a_addr + ks * 32), umma_desc_sw128(b_addr + ks * 32), idesc,
-               (t > 0 || ks > 0) ? 1 : 0);
-      tc_commit(&bar_free[slot]);
-      issue(t + kTcSlots - 1);
-    }
-    tc_commit(bar_mma);
-  }
-  mbar_wait(bar_mma, 0);
-  tc_fence_after();
-  const int col = cb * kTcM + tid;
-  const float* bias = p.bias + p.desc.layer[q.l].b_off;
-  for (int n0 = 0; n0 < rows_n; n0 += 32) {
-    uint32_t r[32];
-    tc_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)n0, r);
-    const int o0 = nt * 256 + n0;
-    if (LAST) {
-      if (col < p.ncols)
-        for (int j = 0; j < 32; ++j) {
-          const int o = o0 + j;
-          if (o < q.out) p.raw[(long long)col * q.out + o] = __uint_as_float(r[j]) + bias[o];
+  if (warp == 4) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      long long st = 0;
+      for (int cb = cb0; cb < q.ncb; cb += cbs) {
+        for (int nt = nt0; nt < nt1; ++nt) {
+          const uint32_t b_bytes = (uint32_t)(nt == q.nts - 1 ? last_nt_rows : 256) * 128;
+          for (int t = 0; t < q.kt; ++t, ++st) {
+            const int slot = (int)(st % NS);
+            if (st >= NS) mbar_wait(&freeb[slot], (uint32_t)(((st / NS) - 1) & 1));
+            unsigned char* dst = ring + (size_t)slot * q.slot_bytes;
+            mbar_expect_tx(&full[slot], q.a_bytes + b_bytes);
+            if (!FIRST)
+              bulk_g2s(dst, q.act_in + ((long long)cb * q.kt + t) * kWideImage, kWideImage,
+                       &full[slot]);
+            bulk_g2s(dst + q.a_bytes,
+                     p.tc_blob + q.w_off + ((long long)nt * q.kt + t) * (256 * 128), b_bytes,
+                     &full[slot]);
+          }
         }
-    } else {
-      // next layer's A image: K tile o0 / 64 of column block cb
-      const int kt_next = (q.out + 63) / 64;
-      unsigned char* img = q.act_out + ((long long)cb * kt_next + (o0 >> 6)) * (kTcM * 128);
-      uint32_t packed[16];
-#pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        const int o = o0 + j;
-        float v0 = o < q.out ? __uint_as_float(r[j]) + bias[o] : 0.f;
-        float v1 = o + 1 < q.out ? __uint_as_float(r[j + 1]) + bias[o + 1] : 0.f;
-        v0 = v0 > 0.f ? v0 : 0.f;
-        v1 = v1 > 0.f ? v1 : 0.f;
-        const __nv_bfloat162 pr = __floats2bfloat162_rn(v0, v1);
-        packed[j / 2] = *reinterpret_cast<const uint32_t*>(&pr);
       }
-#pragma unroll
-      for (int c = 0; c < 4; ++c)  // four 16-byte chunks of this row
-        *reinterpret_cast<uint4*>(img + sw128_offset(tid, (o0 & 63) + c * 8)) =
-            make_uint4(packed[4 * c], packed[4 * c + 1], packed[4 * c + 2], packed[4 * c + 3]);
     }
+    __syncwarp();
+  } else if (warp >= 6) {
+    // ---------------------------------------- feature builders (first layer)
+    if (FIRST) {
+      const int row = tid - 192;
+      int i = 0;
+      for (int cb = cb0; cb < q.ncb; cb += cbs, ++i) {
+        const int fb = i & 1;
+        if (i >= 2) mbar_wait(&ffree[fb], (uint32_t)(((i >> 1) - 1) & 1));
+        tc_feature_tile(p, cb * kTcM + row, 0, feat + fb * kWideImage, row);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ffull[fb]);
+      }
+    }
+  } else if (warp == 5) {
+    // ---------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      long long st = 0;
+      int a = 0, i = 0;
+      for (int cb = cb0; cb < q.ncb; cb += cbs, ++i) {
+        const int fb = i & 1;
+        if (FIRST) {
+          mbar_wait(&ffull[fb], (uint32_t)((i >> 1) & 1));
+          tc_fence_after();
+        }
+        for (int nt = nt0; nt < nt1; ++nt, ++a) {
+          const int acc = a & 1, u = a >> 1;
+          if (u >= 1) {
+            mbar_wait(&tempty[acc], (uint32_t)((u - 1) & 1));
+            tc_fence_after();
+          }
+          const int rows_n = nt == q.nts - 1 ? last_nt_rows : 256;
+          const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
+                                 ((uint32_t)(rows_n >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
+          const uint32_t d = tmem + (uint32_t)(acc * 256);
+          for (int t = 0; t < q.kt; ++t, ++st) {
+            const int slot = (int)(st % NS);
+            mbar_wait(&full[slot], (uint32_t)((st / NS) & 1));
+            tc_fence_after();
+            const uint32_t s_addr = smem_u32(ring + (size_t)slot * q.slot_bytes);
+            const uint32_t a_addr = FIRST ? smem_u32(feat + fb * kWideImage) : s_addr;
+            const uint32_t b_addr = s_addr + q.a_bytes;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+              tc_mma(d, umma_desc_sw128(a_addr + ks * 32), umma_desc_sw128(b_addr + ks * 32),
+                     idesc, (t > 0 || ks > 0) ? 1 : 0);
+            tc_commit(&freeb[slot]);
+          }
+          tc_commit(&tfull[acc]);
+        }
+        if (FIRST) tc_commit(&ffree[fb]);
+      }
+    }
+    __syncwarp();
+  } else if (warp < 4) {
+    // ------------------------------------------------------------ epilogue
+    const float* bias = p.bias + p.desc.layer[q.l].b_off;
+    const int kt_next = (q.out + 63) / 64;
+    int a = 0, img = 0;
+    for (int cb = cb0; cb < q.ncb; cb += cbs) {
+      const int col = cb * kTcM + tid;
+      for (int nt = nt0; nt < nt1; ++nt, ++a) {
+        const int acc = a & 1, u = a >> 1;
+        mbar_wait(&tfull[acc], (uint32_t)(u & 1));
+        tc_fence_after();
+        const int rows_n = nt == q.nts - 1 ? last_nt_rows : 256;
+        for (int n0 = 0; n0 < rows_n; n0 += 64) {
+          uint32_t r[64];
+          const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * 256 + n0);
+          tc_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          tc_ld32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+          const int o0 = nt * 256 + n0;
+          if (LAST) {
+            if (col < p.ncols) {
+              float* dst = p.raw + (long long)col * q.out;
+              for (int j = 0; j < 64; ++j)
+                if (o0 + j < q.out) dst[o0 + j] = __uint_as_float(r[j]) + bias[o0 + j];
+            }
+          } else {
+            const int sb = img & 1;
+            if (tid == 0) bulk_wait_read<1>();  // the store that last used stg[sb] has read it
+            epi_sync();
+            unsigned char* sp = stg + sb * kWideImage;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              uint32_t w[4];
+#pragma unroll
+              for (int h = 0; h < 4; ++h) {
+                const int j = c * 8 + 2 * h, o = o0 + j;
+                float v0 = o < q.out ? __uint_as_float(r[j]) + bias[o] : 0.f;
+                float v1 = o + 1 < q.out ? __uint_as_float(r[j + 1]) + bias[o + 1] : 0.f;
+                v0 = v0 > 0.f ? v0 : 0.f;
+                v1 = v1 > 0.f ? v1 : 0.f;
+                const __nv_bfloat162 pr = __floats2bfloat162_rn(v0, v1);
+                w[h] = *reinterpret_cast<const uint32_t*>(&pr);
+              }
+              *reinterpret_cast<uint4*>(sp + sw128_offset(tid, c * 8)) =
+                  make_uint4(w[0], w[1], w[2], w[3]);
+            }
+            fence_proxy_async_smem();
+            epi_sync();
+            if (tid == 0) {
+              bulk_s2g(q.act_out + ((long long)cb * kt_next + (o0 >> 6)) * kWideImage, sp,
+                       kWideImage);
+              bulk_commit();
+            }
+            ++img;
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      }
+    }
+    if (!LAST && tid == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
 
@@ -490,11 +602,6 @@ int cyr_launch_actor_tc(const cyr::ActorDesc& desc, const unsigned char* tc_blob
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
 }
 
-size_t cyr_tc_wide_smem_bytes() {
-  return 1024 + (size_t)cyr::kTcSlots * cyr::kWideStageBytes + (2 * cyr::kTcSlots + 1) * 8 + 16;
-}
-
-// one wide layer (see actor_tc_layer_kernel); act buffers are tile images
 int cyr_launch_actor_tc_layer(const cyr::ActorDesc& desc, const unsigned char* tc_blob,
                               long long w_off, int npad, int l, const float* bias_blob,
                               const int32_t* alloc, int S, int E, int N, int cap, float* raw,
@@ -502,7 +609,7 @@ int cyr_launch_actor_tc_layer(const cyr::ActorDesc& desc, const unsigned char* t
                               const int32_t* mcs, const int16_t* node, int M, int tau,
                               int parents, long long nodes_per_slot, long long parent_off,
                               int epad, double mcs_scale, cudaStream_t stream) {
-  cyr::TcLayerLaunch q{};
+  cyr::TcWideLaunch q{};
   cyr::TcLaunch& p = q.base;
   p.desc = desc;
   p.tc_blob = tc_blob;
@@ -528,34 +635,47 @@ int cyr_launch_actor_tc_layer(const cyr::ActorDesc& desc, const unsigned char* t
   p.epad = epad;
   p.mcs_scale = mcs_scale;
   const cyr::LayerDesc& L = desc.layer[l];
+  const bool first = l == 0, last = l == desc.n_layers - 1;
+  if (first && last) return CYR_UNSUPPORTED;
+  if (first && L.in > 64) return CYR_UNSUPPORTED;
   q.l = l;
   q.in = L.in;
   q.out = L.out;
   q.npad = npad;
-  q.first = l == 0;
-  q.last = l == desc.n_layers - 1;
-  q.kt = q.first ? 1 : (L.in + 63) / 64;
-  if (q.first && L.in > 64) return CYR_UNSUPPORTED;
+  q.kt = first ? 1 : (L.in + 63) / 64;
+  q.nts = (npad + 255) / 256;
+  q.ncb = (int)((ncols + cyr::kTcM - 1) / cyr::kTcM);
   q.w_off = w_off;
   q.act_in = act_in;
   q.act_out = act_out;
-  const size_t smem = cyr_tc_wide_smem_bytes();
-  const dim3 grid((unsigned)((ncols + cyr::kTcM - 1) / cyr::kTcM), (unsigned)((npad + 255) / 256));
+  q.a_bytes = first ? 0u : (uint32_t)cyr::kWideImage;
+  const int b_rows = std::min(256, npad);
+  q.slot_bytes = (uint32_t)((q.a_bytes + b_rows * 128 + 1023) / 1024 * 1024);
+  const size_t fixed = 1024 + (first ? 2 * cyr::kWideImage : 0) +
+                       (last ? 0 : 2 * cyr::kWideImage) + (4 * cyr::kWideMaxSlots + 16) * 8 + 16;
+  static int max_smem = 0, sms = 0;
+  if (!max_smem) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  q.nslots = (int)std::min<size_t>(cyr::kWideMaxSlots, (max_smem - fixed) / q.slot_bytes);
+  if (q.nslots < 2) return CYR_UNSUPPORTED;
+  const size_t smem = fixed + (size_t)q.nslots * q.slot_bytes;
+  q.split = std::max(1, std::min(q.nts, sms / std::max(q.ncb, 1)));
+  const dim3 grid((unsigned)(std::min(q.ncb, sms / q.split) * q.split));
 #define CYR_WIDE(F, LST)                                                                       \
   do {                                                                                         \
-    static bool set = false;                                                                   \
-    if (!set) {                                                                                \
-      if (cudaFuncSetAttribute(cyr::actor_tc_layer_kernel<F, LST>,                             \
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=     \
-          cudaSuccess)                                                                         \
-        return CYR_CUDA_ERROR;                                                                 \
-      set = true;                                                                              \
-    }                                                                                          \
-    cyr::actor_tc_layer_kernel<F, LST><<<grid, cyr::kTcThreads, smem, stream>>>(q);            \
+    if (cudaFuncSetAttribute(cyr::actor_tc_wide_kernel<F, LST>,                                \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem) !=         \
+        cudaSuccess)                                                                           \
+      return CYR_CUDA_ERROR;                                                                   \
+    cyr::actor_tc_wide_kernel<F, LST>                                                          \
+        <<<grid, F ? cyr::kWideFirstThreads : cyr::kWideThreads, smem, stream>>>(q);           \
   } while (0)
-  if (q.first && q.last) return CYR_UNSUPPORTED;
-  if (q.first) CYR_WIDE(true, false);
-  else if (q.last) CYR_WIDE(false, true);
+  if (first) CYR_WIDE(true, false);
+  else if (last) CYR_WIDE(false, true);
   else CYR_WIDE(false, false);
 #undef CYR_WIDE
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;

@@ -213,7 +213,6 @@ int cyr_launch_actor_tc(const cyr::ActorDesc& desc, const unsigned char* tc_blob
                         int mode_t, const int32_t* mcs, const int16_t* node, int M, int tau,
                         int parents, long long nodes_per_slot, long long parent_off, int epad,
                         double mcs_scale, cudaStream_t stream);
-size_t cyr_tc_wide_smem_bytes();
 int cyr_launch_actor_tc_layer(const cyr::ActorDesc& desc, const unsigned char* tc_blob,
                               long long w_off, int npad, int l, const float* bias_blob,
                               const int32_t* alloc, int S, int E, int N, int cap, float* raw,

@@ -113,7 +113,8 @@ def test_tc_mode_t_agreement(golden):
 
 def test_tc_wide_mode_t_cfg5(golden):
     """cfg5's 3 x 1024 actor runs the per-layer tensor-core GEMMs (HBM
-    activation images); compare its Mode-T tree with fp32 SIMT."""
+    activation images) at every level; compare its Mode-T tree with fp32
+    SIMT."""
     cfg = golden.config("cfg5")
     from paper_2506_00167_b200 import substream
     actor = tree.make_mode_t_actor(cfg.cell, (1024, 1024, 1024), substream(0, "mode-t"))
@@ -129,9 +130,6 @@ def test_tc_wide_mode_t_cfg5(golden):
     rate = float(same.mean())
     print(f"[bf16_tc] mode-T cfg5: node agreement {rate:.4f}")
     _record("mode_t/cfg5_nodes", rate)
-    # levels 1-3 (< 1024 columns) run fp32 SIMT and agree exactly
-    four = tree.level_offsets(6, 7)[3]
-    assert same[:, :four].all()
     assert rate > 0.5
     # every child satisfies the per-level column contract against its parent
     l = cfg.meta["urllc_sc_len"]
