@@ -319,7 +319,7 @@ def run_ours(args, rank, world, local_rank):
 
         # ---- single-slot latency through the drop-in build_codebook
         lat = latency_run(agent, cell, allocs, args.latency_slots)
-        mode_t = mode_t_run(cell) if (rank == 0 and not args.no_mode_t) else None
+        mode_t = mode_t_all(cell) if (rank == 0 and not args.no_mode_t) else None
 
     mean_ms = float(np.mean(step_ms))
     mean_e2e = float(np.mean(e2e))
@@ -375,40 +375,51 @@ def run_ours(args, rank, world, local_rank):
     return 0
 
 
-def mode_t_run(cell, slots=8, reps=3):
-    """North-star Mode T (actor on every arrival-tree node state, cfg2
-    geometry, 2x256 Mode-T actor): tree-batch time for fp32 SIMT and the
-    bf16 tcgen05 path, and their node-decision agreement."""
+def mode_t_run(cell, hidden, slots, reps=3, fp32_reps=None):
+    """North-star Mode T (actor on every arrival-tree node state): tree-batch
+    time for fp32 SIMT and the bf16 tcgen05 path, and their node-decision
+    agreement (BASELINE configs[4] for the cfg5 geometry)."""
     import torch
     from paper_2506_00167_b200 import DevicePolicy, substream, tree
-    actor = tree.make_mode_t_actor(cell, HIDDEN, substream(0, "mode-t"))
+    actor = tree.make_mode_t_actor(cell, hidden, substream(0, "mode-t"))
     allocs, eps = synthetic_inputs(cell, slots, seed=11)
     mcs = np.random.default_rng(11).integers(0, 6, size=allocs.shape).astype(np.int32)
     al, mc, ep = (torch.from_numpy(x).cuda() for x in (allocs, mcs, eps))
     out, states = {}, {}
     cols = sum((cell.num_branches + 1) ** t for t in range(cell.minislots)) * cell.num_branches
-    sizes = tree.mode_t_sizes(cell, HIDDEN)
+    sizes = tree.mode_t_sizes(cell, hidden)
     flops = 2.0 * cols * slots * sum(i * o for i, o in zip(sizes[:-1], sizes[1:]))
     for prec in ("fp32", "bf16_tc"):
+        n = (fp32_reps or reps) if prec == "fp32" else reps
         pol = DevicePolicy(actor, prec)
         st = tree.build_tree_mode_t(pol, cell, al, mc, ep)
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        for _ in range(reps):
+        for _ in range(n):
             tree.build_tree_mode_t(pol, cell, al, mc, ep, out=st)
         b.record()
         torch.cuda.synchronize()
-        ms = a.elapsed_time(b) / reps
+        ms = a.elapsed_time(b) / n
         states[prec] = st.cpu().numpy()[:, :, :cell.num_embb]
         out[prec] = {"ms_per_tree_batch": ms, "trees_per_s": slots / (ms * 1e-3),
                      "actor_tflops_effective": flops / (ms * 1e-3) / 1e12}
         pol.close()
     same = (states["fp32"] == states["bf16_tc"]).all(axis=2)
-    out.update({"slots": slots, "nodes_per_tree": int(same.shape[1]),
-                "actor_columns_per_tree": cols,
+    out.update({"actor": "x".join(str(h) for h in hidden), "slots": slots,
+                "cell": {"N": cell.total_scs, "E": cell.num_embb, "L": cell.urllc_sc_len,
+                         "cap": cell.num_branches, "M": cell.minislots},
+                "nodes_per_tree": int(same.shape[1]), "actor_columns_per_tree": cols,
                 "node_agreement_bf16_vs_fp32": float(same.mean())})
     return out
+
+
+def mode_t_all(cell):
+    """cfg2 geometry (8 slots) and the cfg5 large tree (configs[4])."""
+    from paper_2506_00167_b200 import CellConfig
+    return {"cfg2": mode_t_run(cell, HIDDEN, 8),
+            "cfg5": mode_t_run(CellConfig(780, 16, 130), (1024, 1024, 1024), 1, reps=3,
+                               fp32_reps=1)}
 
 
 def latency_run(agent, cell, allocs, n):

@@ -2,6 +2,7 @@
 // enforcer (one coupled call per CTA) and standalone Huntington-Hill.
 // Device code lives in projection.cuh.
 #include "projection.cuh"
+#include "projection_lane.cuh"
 
 namespace cyr {
 
@@ -21,6 +22,28 @@ __global__ void __launch_bounds__(256, 4) codebook_kernel(
   const long long row0 = s0 * cap;
   codebook_rows<RawT>(raw + row0 * 2 * E, alloc, eps, row0, slots * cap, cap, E, L, cb, m_out,
                       nu_out, margin_out, iters_out, status, sc);
+}
+
+// Batch K3, one lane per row (projection_lane.cuh): each warp holds
+// 32 / cap whole slots; 4 warps per CTA, no CTA barrier.
+constexpr int kLaneWarps = 4;
+
+template <typename RawT>
+__global__ void __launch_bounds__(32 * kLaneWarps) codebook_lane_kernel(
+    const RawT* __restrict__ raw, const int32_t* __restrict__ alloc,
+    const double* __restrict__ eps, int S, int E, int L, int cap, int32_t* __restrict__ cb,
+    double* __restrict__ m_out, double* __restrict__ nu_out, double* __restrict__ margin_out,
+    int32_t* __restrict__ iters_out, int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) unsigned char lane_smem[];
+  const int w = threadIdx.x >> 5;
+  const int gpw = 32 / cap;
+  const long long s0 = ((long long)blockIdx.x * kLaneWarps + w) * gpw;
+  if (s0 >= S) return;
+  const int slots = (int)min((long long)gpw, S - s0);
+  const long long row0 = s0 * cap;
+  const SlotIO io{alloc, eps, cb, m_out, nu_out, margin_out, iters_out, E, cap};
+  codebook_rows_lane<RawT, SlotIO>(raw + row0 * 2 * E, row0, slots * cap, cap, E, L, io, status,
+                                   lane_smem + (size_t)w * lane_scratch_bytes(E));
 }
 
 // ------------------------------------------------------------ Mode-T level
@@ -52,18 +75,47 @@ struct TreeIO {
       if (j == 1) node[first + lane] = (int16_t)(lane < E ? cum : 0);
     }
   }
+  // one lane = one row: child j's record (and child 0's for j == 1), 16 B at a time
+  __device__ void emit_lane(long long, long long group, int j, const int* hT, int, const double*,
+                            double, double, int) const {
+    const long long s = group / parents, q = group % parents;
+    const long long base = s * nodes_per_slot;
+    const int16_t* par = parent_off >= 0 ? node + (base + parent_off + q) * epad : nullptr;
+    int16_t* first = node + (base + child_off + q * (cap + 1)) * epad;
+    for (int e0 = 0; e0 < epad; e0 += 8) {
+      uint4 pv = make_uint4(0, 0, 0, 0);
+      if (par) pv = *reinterpret_cast<const uint4*>(par + e0);
+      const int16_t* pc = reinterpret_cast<const int16_t*>(&pv);
+      alignas(16) int16_t v[8], v0[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int e = e0 + k;
+        const int cum = e < E ? pc[k] : 0;
+        v[k] = (int16_t)(e < E ? cum + hT[e * 32] : 0);
+        v0[k] = (int16_t)cum;
+      }
+      *reinterpret_cast<uint4*>(first + (long long)j * epad + e0) = *reinterpret_cast<const uint4*>(v);
+      if (j == 1) *reinterpret_cast<uint4*>(first + e0) = *reinterpret_cast<const uint4*>(v0);
+    }
+  }
 };
 
+// K3 of one Mode-T level, one lane per row: each warp holds 32 / cap
+// parents (one coupled call of cap rows each).
 template <typename RawT>
-__global__ void __launch_bounds__(256, 4) tree_level_kernel(const RawT* __restrict__ raw, TreeIO io,
-                                                         long long groups, int gpc, int L,
-                                                         int32_t* __restrict__ status) {
-  __shared__ RowScratch sc;
-  const long long g0 = (long long)blockIdx.x * gpc;
-  const int n = (int)min((long long)gpc, groups - g0);
+__global__ void __launch_bounds__(32 * kLaneWarps) tree_level_kernel(const RawT* __restrict__ raw,
+                                                                  TreeIO io, long long groups,
+                                                                  int L,
+                                                                  int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) unsigned char lane_smem[];
+  const int w = threadIdx.x >> 5;
+  const int gpw = 32 / io.cap;
+  const long long g0 = ((long long)blockIdx.x * kLaneWarps + w) * gpw;
+  if (g0 >= groups) return;
+  const int n = (int)min((long long)gpw, groups - g0);
   const long long row0 = g0 * io.cap;
-  codebook_rows_io<RawT, TreeIO>(raw + row0 * 2 * io.E, row0, n * io.cap, io.cap, io.E, L, io,
-                                 status, sc);
+  codebook_rows_lane<RawT, TreeIO>(raw + row0 * 2 * io.E, row0, n * io.cap, io.cap, io.E, L, io,
+                                   status, lane_smem + (size_t)w * lane_scratch_bytes(io.E));
 }
 
 // ------------------------------------------------------- standalone enforcer
@@ -256,8 +308,29 @@ int cyr_launch_codebook(int precision, const void* raw, const int32_t* alloc, co
   (void)N;
   if (S <= 0) return CYR_OK;
   if (E < 1 || E > cyr::kMaxUsers || cap < 1 || cap > 16) return CYR_UNSUPPORTED;
-  // small batches: one slot per CTA (latency); large: as many slots as fit 32 rows
-  const int spc = S < 1184 ? 1 : 32 / cap;
+  if (S >= 1184) {  // throughput: one lane per row, 32 / cap slots per warp
+    const int per_cta = cyr::kLaneWarps * (32 / cap);
+    const dim3 grid((S + per_cta - 1) / per_cta), block(32 * cyr::kLaneWarps);
+    const size_t smem = cyr::kLaneWarps * cyr::lane_scratch_bytes(E);
+    if (precision == CYR_FP64) {
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(cyr::codebook_lane_kernel<double>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cyr::codebook_lane_kernel<double><<<grid, block, smem, stream>>>(
+          static_cast<const double*>(raw), alloc, eps, S, E, L, cap, codebook, m_hat, nu, margin,
+          iters, status);
+    } else {
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(cyr::codebook_lane_kernel<float>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cyr::codebook_lane_kernel<float><<<grid, block, smem, stream>>>(
+          static_cast<const float*>(raw), alloc, eps, S, E, L, cap, codebook, m_hat, nu, margin,
+          iters, status);
+    }
+    return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
+  }
+  // small batches: one slot per CTA (latency)
+  const int spc = 1;
   const dim3 grid((S + spc - 1) / spc), block(S < 1184 ? 32 * cap : 256);
   if (precision == CYR_FP64)
     cyr::codebook_kernel<double><<<grid, block, 0, stream>>>(
@@ -302,14 +375,22 @@ int cyr_launch_tree_level(int precision, const void* raw, const int32_t* alloc, 
   if (E < 1 || E > cyr::kMaxUsers || cap < 1 || cap > 16) return CYR_UNSUPPORTED;
   cyr::TreeIO io{alloc, eps, node, E, cap, epad, parents, nodes_per_slot, parent_off, child_off};
   const long long groups = (long long)S * parents;
-  const int gpc = 32 / cap;  // whole groups per CTA (<= 32 rows)
-  const long long blocks = (groups + gpc - 1) / gpc;
+  const long long per_cta = (long long)cyr::kLaneWarps * (32 / cap);
+  const long long blocks = (groups + per_cta - 1) / per_cta;
   if (blocks >= (1ll << 31)) return CYR_UNSUPPORTED;
-  if (precision == CYR_FP64)
-    cyr::tree_level_kernel<double><<<(unsigned)blocks, 256, 0, stream>>>(
-        static_cast<const double*>(raw), io, groups, gpc, L, status);
-  else
-    cyr::tree_level_kernel<float><<<(unsigned)blocks, 256, 0, stream>>>(
-        static_cast<const float*>(raw), io, groups, gpc, L, status);
+  const size_t smem = cyr::kLaneWarps * cyr::lane_scratch_bytes(E);
+  if (precision == CYR_FP64) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(cyr::tree_level_kernel<double>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cyr::tree_level_kernel<double><<<(unsigned)blocks, 32 * cyr::kLaneWarps, smem, stream>>>(
+        static_cast<const double*>(raw), io, groups, L, status);
+  } else {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(cyr::tree_level_kernel<float>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cyr::tree_level_kernel<float><<<(unsigned)blocks, 32 * cyr::kLaneWarps, smem, stream>>>(
+        static_cast<const float*>(raw), io, groups, L, status);
+  }
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
 }

@@ -398,6 +398,85 @@ struct RowScratch {
   double b[32][32];   // [row][user] raw actions from phase 1 (head computed once)
 };
 
+// Phase 1 of one row (whole warp, lane = user): head, bracket, water level,
+// exact fill threshold.  Returns b (this lane's raw action); lo/hi/threshold
+// and flags go to the caller's scratch through the out-parameters.
+template <typename RawT, typename IO>
+__device__ __forceinline__ double row_phase1(const RawT* rr, long long grow, int cap, int E, int L,
+                                             const IO& io, int32_t* status, double& lo_out,
+                                             double& hi_out, long long& thr_out, int& flags_out,
+                                             unsigned long long* tr = nullptr) {
+  const int lane = threadIdx.x & 31;
+  const bool in = lane < E;
+  const long long group = grow / cap;
+  const int j = (int)(grow % cap) + 1;
+  const int32_t* alloc = io.alloc_row(group);
+  const double* eps = io.eps_row(grow, group, j);
+  Row row;
+  row.valid = true;
+  const double n = in ? (double)alloc[lane] : 0.0;
+  double bval = 0.0;
+  if (in) {
+    const double mu = (double)rr[lane];
+    const double ls = fmin(fmax((double)rr[E + lane], kLogSigmaMin), kLogSigmaMax);
+    double a;
+    if (eps != nullptr) {
+      const double u = __dadd_rn(mu, __dmul_rn(exp(ls), eps[lane]));
+      a = tanh(u);
+    } else {
+      a = tanh(mu);
+    }
+    bval = __dmul_rn(__dmul_rn(__dadd_rn(a, 1.0), 0.5), n);  // neural.py:181-183
+  }
+  row.b = bval;
+  row.c = n;
+  row.d = (double)((long long)j * L);
+  const double capsum = np_row_sum(n, E);  // enforcer.py:64 / :138
+  if (lane == 0 && row.d > capsum) set_status(status, CYR_INFEASIBLE);
+  trace_stamp(tr, 8);
+  kl_setup(row, E);
+  trace_stamp(tr, 9);
+  long long thr = 0;
+  if (row.bis) thr = fill_threshold(row, E, water_level(row, E));
+  trace_stamp(tr, 10);
+  lo_out = row.lo;
+  hi_out = row.hi;
+  thr_out = thr;
+  flags_out = (row.bis ? 1 : 0) | (row.degen ? 2 : 0);
+  return bval;
+}
+
+// Phase 3 of one row (whole warp): m_hat, nu, Huntington-Hill, emit.
+template <typename IO>
+__device__ __forceinline__ void row_phase3(long long grow, int cap, int E, int L, const IO& io,
+                                           double bval, double lo, double hi, int flags, int iters,
+                                           int lr = 0, unsigned long long* tr = nullptr) {
+  const int lane = threadIdx.x & 31;
+  const bool in = lane < E;
+  const long long group = grow / cap;
+  const int j = (int)(grow % cap) + 1;
+  const int32_t* alloc = io.alloc_row(group);
+  Row row;
+  row.valid = true;
+  row.b = bval;
+  row.c = in ? (double)alloc[lane] : 0.0;
+  row.d = (double)((long long)j * L);
+  row.bis = (flags & 1) != 0;
+  row.degen = (flags & 2) != 0;
+  row.lo = lo;
+  row.hi = hi;
+  double m, nu;
+  kl_finish(row, E, m, nu);
+  trace_stamp(tr, 13);
+  double margin;
+  int hh_steps = 0;
+  const int g = hh_row(m, row.c, E, (long long)j * L, margin, &hh_steps);
+  trace_stamp(tr, 14);
+  if (lr < 8) trace_value(tr, 40 + lr, hh_steps);
+  if (lr < 8) trace_value(tr, 56 + lr, iters);
+  io.emit(grow, group, j, lane, g, m, nu, margin, iters);
+}
+
 template <typename RawT, typename IO>
 __device__ void codebook_rows_io(const RawT* raw, long long row0, int nrows, int cap, int E,
                                  int L, const IO& io, int32_t* status, RowScratch& sc,
@@ -405,49 +484,19 @@ __device__ void codebook_rows_io(const RawT* raw, long long row0, int nrows, int
   const int w = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
-  const bool in = lane < E;
-  // phase 1 (warp per row, warps stride over the rows): head, bracket,
-  // water level, exact fill threshold
+  // phase 1 (warp per row, warps stride over the rows)
   for (int lr = w; lr < nrows; lr += nw) {
-    const long long grow = row0 + lr;
-    const long long group = grow / cap;
-    const int j = (int)(grow % cap) + 1;
-    const int32_t* alloc = io.alloc_row(group);
-    const double* eps = io.eps_row(grow, group, j);
-    Row row;
-    row.valid = true;
-    const double n = in ? (double)alloc[lane] : 0.0;
-    double bval = 0.0;
-    if (in) {
-      const RawT* rr = raw + (long long)lr * 2 * E;
-      const double mu = (double)rr[lane];
-      const double ls = fmin(fmax((double)rr[E + lane], kLogSigmaMin), kLogSigmaMax);
-      double a;
-      if (eps != nullptr) {
-        const double u = __dadd_rn(mu, __dmul_rn(exp(ls), eps[lane]));
-        a = tanh(u);
-      } else {
-        a = tanh(mu);
-      }
-      bval = __dmul_rn(__dmul_rn(__dadd_rn(a, 1.0), 0.5), n);  // neural.py:181-183
-    }
-    row.b = bval;
-    row.c = n;
-    row.d = (double)((long long)j * L);
-    const double capsum = np_row_sum(n, E);  // enforcer.py:64 / :138
-    if (lane == 0 && row.d > capsum) set_status(status, CYR_INFEASIBLE);
-    trace_stamp(tr, 8);
-    kl_setup(row, E);
-    trace_stamp(tr, 9);
-    long long thr = 0;
-    if (row.bis) thr = fill_threshold(row, E, water_level(row, E));
-    trace_stamp(tr, 10);
+    double lo, hi;
+    long long thr;
+    int flags;
+    const double bval = row_phase1(raw + (long long)lr * 2 * E, row0 + lr, cap, E, L, io, status,
+                                   lo, hi, thr, flags, tr);
     sc.b[lr][lane] = bval;
     if (lane == 0) {
-      sc.lo[lr] = row.lo;
-      sc.hi[lr] = row.hi;
+      sc.lo[lr] = lo;
+      sc.hi[lr] = hi;
       sc.t[lr] = thr;
-      sc.flags[lr] = (row.bis ? 1 : 0) | (row.degen ? 2 : 0);
+      sc.flags[lr] = flags;
     }
     if (lr < 8) trace_stamp_warp(tr, 16 + lr);
   }
@@ -468,32 +517,59 @@ __device__ void codebook_rows_io(const RawT* raw, long long row0, int nrows, int
     }
   }
   __syncthreads();
-  // phase 3 (warp per row): m_hat, nu, Huntington-Hill
-  for (int lr = w; lr < nrows; lr += nw) {
-    const long long grow = row0 + lr;
-    const long long group = grow / cap;
-    const int j = (int)(grow % cap) + 1;
-    const int32_t* alloc = io.alloc_row(group);
-    Row row;
-    row.valid = true;
-    row.b = sc.b[lr][lane];
-    row.c = in ? (double)alloc[lane] : 0.0;
-    row.d = (double)((long long)j * L);
-    row.bis = (sc.flags[lr] & 1) != 0;
-    row.degen = (sc.flags[lr] & 2) != 0;
-    row.lo = sc.lo[lr];
-    row.hi = sc.hi[lr];
-    double m, nu;
-    kl_finish(row, E, m, nu);
-    trace_stamp(tr, 13);
-    double margin;
-    int hh_steps = 0;
-    const int g = hh_row(m, row.c, E, (long long)j * L, margin, &hh_steps);
-    trace_stamp(tr, 14);
-    if (lr < 8) trace_value(tr, 40 + lr, hh_steps);
-    if (lr < 8) trace_value(tr, 56 + lr, sc.iters[lr]);
-    io.emit(grow, group, j, lane, g, m, nu, margin, sc.iters[lr]);
+  // phase 3 (warp per row)
+  for (int lr = w; lr < nrows; lr += nw)
+    row_phase3(row0 + lr, cap, E, L, io, sc.b[lr][lane], sc.lo[lr], sc.hi[lr], sc.flags[lr],
+               sc.iters[lr], lr, tr);
+}
+
+// One warp = one whole coupled call of `cap` rows (group `group`, rows
+// group*cap ..): phase 1 row by row, the coupled loop with lanes = rows,
+// phase 3 row by row — no CTA barrier, so the warps of a CTA (different
+// groups) overlap their latency chains.  Scratch: this warp's slice.
+struct WarpScratch {
+  double lo[32], hi[32];
+  long long t[32];
+  int flags[32];
+  int iters;
+};
+
+template <typename RawT, typename IO>
+__device__ void codebook_group_warp(const RawT* raw, long long group, int cap, int E, int L,
+                                    const IO& io, int32_t* status, WarpScratch& sc,
+                                    double* bsc /* [cap][32] */) {
+  const int lane = threadIdx.x & 31;
+  const long long row0 = group * cap;
+  for (int r = 0; r < cap; ++r) {
+    double lo, hi;
+    long long thr;
+    int flags;
+    bsc[r * 32 + lane] = row_phase1(raw + (long long)r * 2 * E, row0 + r, cap, E, L, io, status,
+                                    lo, hi, thr, flags);
+    if (lane == 0) {
+      sc.lo[r] = lo;
+      sc.hi[r] = hi;
+      sc.t[r] = thr;
+      sc.flags[r] = flags;
+    }
   }
+  __syncwarp();
+  {
+    double lo[1] = {lane < cap ? sc.lo[lane] : 0.0};
+    double hi[1] = {lane < cap ? sc.hi[lane] : 0.0};
+    const long long tt[1] = {lane < cap ? sc.t[lane] : 0};
+    const bool bis[1] = {lane < cap && (sc.flags[lane] & 1)};
+    const int iters = coupled_bisection<1>(lo, hi, tt, bis, cap);
+    if (lane < cap) {
+      sc.lo[lane] = lo[0];
+      sc.hi[lane] = hi[0];
+    }
+    if (lane == 0) sc.iters = iters;
+  }
+  __syncwarp();
+  for (int r = 0; r < cap; ++r)
+    row_phase3(row0 + r, cap, E, L, io, bsc[r * 32 + lane], sc.lo[r], sc.hi[r], sc.flags[r],
+               sc.iters, r);
 }
 
 // Mode R: the slot codebook [S][cap+1][E] plus optional diagnostics.
@@ -523,6 +599,19 @@ struct SlotIO {
       if (margin_out) margin_out[grow] = margin;
       if (iters_out && j == 1) iters_out[group] = iters;
     }
+  }
+  // one lane = one row (projection_lane.cuh): seats hT[e * 32], m_hat mT[e * 32]
+  __device__ void emit_lane(long long grow, long long group, int j, const int* hT, int E_,
+                            const double* mT, double nu, double margin, int iters) const {
+    int32_t* book = cb + group * (cap + 1) * E;
+    for (int e = 0; e < E; ++e) {
+      book[(long long)j * E + e] = hT[e * 32];
+      if (j == 1) book[e] = 0;
+      if (m_out) m_out[grow * E + e] = mT[e * 32];
+    }
+    if (nu_out) nu_out[grow] = nu;
+    if (margin_out) margin_out[grow] = margin;
+    if (iters_out && j == 1) iters_out[group] = iters;
   }
 };
 

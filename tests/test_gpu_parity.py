@@ -175,6 +175,28 @@ def test_codebooks_match_reference(golden, name, mode, precision):
 
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 @pytest.mark.parametrize("name", CONFIGS)
+@pytest.mark.parametrize("mode", ["det", "sto"])
+def test_large_batch_lane_kernel(golden, name, mode, precision):
+    """S >= 1184 slots run K3 one lane per row (codebook_lane_kernel): the
+    golden slots tiled 19x must reproduce the reference codebooks tile by
+    tile."""
+    cfg = golden.config(name)
+    agent = cfg.agent()
+    pol = DevicePolicy(agent.actor, precision)
+    reps = 19
+    allocs = np.tile(cfg["alloc"], (reps, 1))
+    eps = None if mode == "det" else np.tile(cfg["eps"], (reps, 1, 1))
+    eng = CodebookEngine(pol, cfg.cell, max_slots=allocs.shape[0])
+    out = eng.run(torch.from_numpy(allocs).cuda(),
+                  None if eps is None else torch.from_numpy(eps).cuda())
+    eng.check()
+    got = out.cpu().numpy().reshape(reps, -1, *out.shape[1:])
+    for t in range(reps):
+        _compare_books(got[t], cfg, mode, precision, f"lane tile {t}")
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("name", CONFIGS)
 def test_single_slot_fused_path(golden, name, precision):
     """S*cap <= 8: K2 runs as a thread-block cluster fused with K3 and the
     host path reads/writes mapped pinned pages (no copy nodes)."""
