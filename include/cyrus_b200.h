@@ -47,7 +47,8 @@ enum cyr_status {
   CYR_INFEASIBLE = 1,  /* demand > total capacity  (InfeasibleDemandError) */
   CYR_BAD_ARG = 2,     /* shape / range / negative input (ValueError)       */
   CYR_CUDA_ERROR = 3,  /* CUDA runtime failure                             */
-  CYR_UNSUPPORTED = 4  /* geometry outside the kernels' compiled envelope   */
+  CYR_UNSUPPORTED = 4, /* geometry outside the kernels' compiled envelope   */
+  CYR_INTERNAL = 5     /* an internal invariant failed (result withheld)     */
 };
 
 enum cyr_precision {
@@ -125,14 +126,16 @@ int cyr_codebook_host(cyr_policy* policy, const int32_t* alloc, const double* ep
  * (enforcer.py:201-207).  b, caps [R][E] float64; demand [R] int64.
  * Outputs (NULL to skip except grants): m_hat [R][E], nu [R],
  * degenerate [R] (uint8), grants [R][E] int64, margin [R].
- * R <= 256, E <= 32. */
+ * Any R (one CTA up to 256 rows; above, a two-pass multi-CTA call with the
+ * same coupled stop, e.g. critic_targets' 1,536 rows, sac.py:202-205);
+ * E <= 32. */
 int cyr_enforce_batch_device(const double* b, const double* caps, const int64_t* demand,
                              int32_t R, int32_t E, double* m_hat, double* nu,
                              uint8_t* degenerate, int64_t* grants, double* margin,
                              int32_t* status, void* stream);
 
 /* kl_project_batch(b, caps, demand) alone (enforcer.py:49-115): float64
- * demand, one coupled call, R <= 256.  Outputs m_hat [R][E], nu [R] and
+ * demand, one coupled call, any R.  Outputs m_hat [R][E], nu [R] and
  * degenerate [R] (the last two may be NULL). */
 int cyr_kl_project_batch_device(const double* b, const double* caps, const double* demand,
                                 int32_t R, int32_t E, double* m_hat, double* nu,
@@ -171,6 +174,21 @@ int cyr_tree_mode_t_device(const cyr_policy* policy, const int32_t* alloc, const
                            const double* eps, int32_t S, int32_t N, int32_t L, int32_t M,
                            double mcs_scale, int16_t* node_state, void* workspace,
                            int32_t* status, void* stream);
+
+/* Subtree shard of the Mode-T tree (north star "shards by
+ * ... first-mini-slot branch across the 8 GPUs"): levels 1..shard_level are
+ * built in full (replicated on every shard: (cap+1)^shard_level - 1 nodes),
+ * deeper levels only below the level-shard_level nodes [first, first+count)
+ * — contiguous BFS ranges per level, first*(cap+1)^(tau-shard_level) ... —
+ * with results identical to the same nodes of cyr_tree_mode_t_device.
+ * Records outside the shard are not written.  shard_level = 1 shards by the
+ * first mini-slot's arrival count; 2 or 3 balance 8 GPUs better.
+ * The whole tree is the shard (shard_level 0, first 0, count 1). */
+int cyr_tree_mode_t_shard_device(const cyr_policy* policy, const int32_t* alloc,
+                                 const int32_t* mcs, const double* eps, int32_t S, int32_t N,
+                                 int32_t L, int32_t M, double mcs_scale, int32_t shard_level,
+                                 int64_t first, int64_t count, int16_t* node_state,
+                                 void* workspace, int32_t* status, void* stream);
 
 /* ---- diagnostics ---------------------------------------------------------- */
 /* Cycles for `iters` dependent steps of an fp64 building block (one warp):

@@ -14,7 +14,7 @@ import threading
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcyrus_b200.so")
 
-CYR_OK, CYR_INFEASIBLE, CYR_BAD_ARG, CYR_CUDA_ERROR, CYR_UNSUPPORTED = range(5)
+CYR_OK, CYR_INFEASIBLE, CYR_BAD_ARG, CYR_CUDA_ERROR, CYR_UNSUPPORTED, CYR_INTERNAL = range(6)
 CYR_FP32, CYR_FP64, CYR_BF16_TC = 0, 1, 2
 PRECISIONS = {"fp32": CYR_FP32, "fp64": CYR_FP64, "bf16_tc": CYR_BF16_TC}
 
@@ -50,6 +50,9 @@ SIGNATURES = {
     "cyr_tree_mode_t_workspace_bytes": (ctypes.c_size_t, [_vp, _c_i32, _c_i32, _c_i32]),
     "cyr_tree_mode_t_device": (_c_int, [_vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i32, _c_i32,
                                         ctypes.c_double, _vp, _vp, _vp, _vp]),
+    "cyr_tree_mode_t_shard_device": (_c_int, [_vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i32, _c_i32,
+                                              ctypes.c_double, _c_i32, _c_i64, _c_i64, _vp, _vp,
+                                              _vp, _vp]),
     "cyr_debug_trace": (_c_int, [_pi64, _c_i32]),
     "cyr_selftest_latency": (_c_int, [_c_i32, _c_i32, _pi64]),
     "cyr_selftest_launch": (_c_int, [_c_i32, _c_i32, _pi64]),
@@ -108,6 +111,8 @@ def check(status: int, what: str = "") -> None:
     if status == CYR_CUDA_ERROR:
         detail = l.cyr_last_error().decode()
         raise CudaError(f"{msg} ({detail})" if detail else msg)
+    if status == CYR_INTERNAL:
+        raise RuntimeError(msg)
     raise ValueError(msg)
 
 

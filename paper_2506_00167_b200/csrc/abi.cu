@@ -139,11 +139,13 @@ void pack_blob(const cyr_policy& p, const double* src, std::vector<T>& dst) {
     for (int o = 0; o < L.out; ++o)
       for (int i = 0; i < L.in; ++i)
         dst[L.wr_off + (size_t)o * L.in_pad + i] = (T)src[off + (size_t)o * L.in + i];
-    if (L.wp_off != L.w_off)
-      for (int o = 0; o < L.out; ++o)
-        for (int i = 0; i < L.in; ++i)
-          dst[L.wp_off + ((size_t)(o / 256) * L.in + i) * 256 + o % 256] =
-              (T)src[off + (size_t)o * L.in + i];
+    for (int o = 0; o < L.out; ++o) {
+      const int oo = o % L.pw, g = L.pw / 8;
+      const int pos = L.pw > 64 ? (oo % g) * 8 + oo / g : oo;
+      for (int i = 0; i < L.in; ++i)
+        dst[L.wp_off + ((size_t)(o / L.pw) * L.in + i) * L.pw + pos] =
+            (T)src[off + (size_t)o * L.in + i];
+    }
     off += (size_t)L.out * L.in;
     for (int o = 0; o < L.out; ++o) dst[L.b_off + o] = (T)src[off + o];
     off += L.out;
@@ -269,13 +271,14 @@ size_t wide_act_bytes(const cyr_policy* p, long long cols) {
 int launch_actor_wide(const cyr_policy* p, const int32_t* alloc, int S, int N, int cap, float* raw,
                       unsigned char* act, long long cols, int mode_t, const int32_t* mcs,
                       const int16_t* node, int M, int tau, int parents, long long nodes,
-                      long long parent_off, int epad, double mcs_scale, cudaStream_t st) {
+                      long long parent_off, int epad, double mcs_scale, cudaStream_t st,
+                      int parent_base = 0) {
   unsigned char* buf[2] = {act, act + wide_act_bytes(p, cols) / 2};
   for (int l = 0; l < p->desc.n_layers; ++l) {
     const int rc = cyr_launch_actor_tc_layer(
         p->desc, p->tc_blob_d, p->tc_off[l], p->tc_npad[l], l, static_cast<const float*>(p->blob_d),
         alloc, S, p->E, N, cap, raw, buf[(l + 1) & 1], buf[l & 1], mode_t, mcs, node, M, tau,
-        parents, nodes, parent_off, epad, mcs_scale, st);
+        parents, nodes, parent_off, epad, mcs_scale, st, parent_base);
     if (rc != CYR_OK) return rc;
   }
   return CYR_OK;
@@ -330,6 +333,7 @@ const char* cyr_status_string(int status) {
     case CYR_BAD_ARG: return "invalid argument";
     case CYR_CUDA_ERROR: return "CUDA error";
     case CYR_UNSUPPORTED: return "unsupported geometry";
+    case CYR_INTERNAL: return "internal invariant violated";
     default: return "unknown status";
   }
 }
@@ -391,14 +395,13 @@ int cyr_policy_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
     off += (size_t)(L.out + vec - 1) / vec * vec;
     L.wr_off = (long long)off;
     off += (size_t)L.out * L.in_pad;
+    // paneled copy for the tiled batch kernel: panels of <= 256 outputs;
+    // wide panels (pw > 64) are rounded to 8 and stored thread-interleaved
+    // (position og*8 + a holds output og + a*pw/8, see actor_tiled_kernel)
     L.pw = std::min(L.out_pad, 256);
-    if (L.out_pad > 256) {  // paneled copy for the tiled batch kernel
-      L.pw = 256;
-      L.wp_off = (long long)off;
-      off += (size_t)((L.out_pad + 255) / 256) * L.in * 256;
-    } else {
-      L.wp_off = L.w_off;
-    }
+    if (L.pw > 64) L.pw = (L.pw + 7) / 8 * 8;
+    L.wp_off = (long long)off;
+    off += (size_t)((L.out_pad + L.pw - 1) / L.pw) * L.in * L.pw;
     p->desc.max_width = std::max(p->desc.max_width, std::max(L.in, L.out_pad));
     p->desc.max_rows = std::max(p->desc.max_rows, std::max(L.in_pad, L.out));
   }
@@ -835,19 +838,43 @@ int cyr_tree_mode_t_device(const cyr_policy* p, const int32_t* alloc, const int3
                            const double* eps, int32_t S, int32_t N, int32_t L, int32_t M,
                            double mcs_scale, int16_t* node_state, void* workspace,
                            int32_t* status, void* stream) {
+  return cyr_tree_mode_t_shard_device(p, alloc, mcs, eps, S, N, L, M, mcs_scale, 0, 0, 1,
+                                      node_state, workspace, status, stream);
+}
+
+int cyr_tree_mode_t_shard_device(const cyr_policy* p, const int32_t* alloc, const int32_t* mcs,
+                                 const double* eps, int32_t S, int32_t N, int32_t L, int32_t M,
+                                 double mcs_scale, int32_t shard_level, int64_t first,
+                                 int64_t count, int16_t* node_state, void* workspace,
+                                 int32_t* status, void* stream) {
   if (!p || !p->mode_t) return CYR_BAD_ARG;
   int cap = 0;
   int rc = check_geometry(S, p->E, N, L, &cap);
   if (rc != CYR_OK) return rc;
   if (M < 1 || M > 10 || mcs_scale <= 0.0) return CYR_BAD_ARG;
-  if (S == 0) return CYR_OK;
-  if (!alloc || !mcs || !node_state || !workspace) return CYR_BAD_ARG;
   const int R = cap + 1;
+  if (shard_level < 0 || shard_level > M) return CYR_BAD_ARG;
+  long long width = 1;  // nodes of level shard_level
+  for (int t = 0; t < shard_level; ++t) width *= R;
+  if (first < 0 || count < 0 || first + count > width) return CYR_BAD_ARG;
+  if (S == 0 || count == 0) return CYR_OK;
+  if (!alloc || !mcs || !node_state || !workspace) return CYR_BAD_ARG;
   const int epad = cyr_tree_state_stride(p->E);
   const long long nodes = cyr_tree_num_nodes(cap, M);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  long long parents = 1, level_off = 0, prev_off = -1;
+  // level tau's parents (level tau-1): all of them while tau-1 < shard_level
+  // (replicated on every shard), else the descendants of level-shard_level
+  // nodes [first, first + count): a contiguous range in BFS order
+  long long level_off = 0, prev_off = -1, level_size = 1;  // level tau-1: offset, size
   for (int tau = 1; tau <= M; ++tau) {
+    long long base = 0, parents = level_size;
+    if (tau - 1 >= shard_level) {
+      long long span = 1;
+      for (int t = shard_level; t < tau - 1; ++t) span *= R;
+      base = first * span;
+      parents = count * span;
+    }
+    const long long par_off = prev_off < 0 ? -1 : prev_off + base;
     // K2: the actor on every (parent, branch) column of this level
     const long long cols = (long long)S * parents * cap;
     if (p->tc_wide) {
@@ -856,26 +883,28 @@ int cyr_tree_mode_t_device(const cyr_policy* p, const int32_t* alloc, const int3
       unsigned char* act = static_cast<unsigned char*>(workspace) +
                            ((size_t)S * widest * cap * 2 * p->E * p->elem + 255) / 256 * 256;
       rc = launch_actor_wide(p, alloc, S, N, cap, static_cast<float*>(workspace), act, cols, 1, mcs,
-                             node_state, M, tau, (int)parents, nodes, prev_off, epad, mcs_scale,
-                             st);
+                             node_state, M, tau, (int)parents, nodes, par_off, epad, mcs_scale, st,
+                             (int)base);
     } else if (p->tc_ok && cols >= kTcMinCols)
       rc = cyr_launch_actor_tc(p->desc, p->tc_blob_d, p->tc_off, p->tc_npad,
                                static_cast<const float*>(p->blob_d), alloc, S, p->E, N, cap,
                                static_cast<float*>(workspace), 1, mcs, node_state, M, tau,
-                               (int)parents, nodes, prev_off, epad, mcs_scale, st);
+                               (int)parents, nodes, par_off, epad, mcs_scale, st, (int)base);
     else
       rc = cyr_launch_actor_mode_t(simt_precision(p), p->desc, p->blob_d, alloc, mcs, node_state,
-                                   S, p->E, N, cap, M, tau, (int)parents, nodes, prev_off, epad,
-                                   mcs_scale, workspace, p->sm_count, st);
+                                   S, p->E, N, cap, M, tau, (int)parents, nodes, par_off, epad,
+                                   mcs_scale, workspace, p->sm_count, st, (int)base);
     if (rc != CYR_OK) break;
     // K3: one coupled enforcement per parent; writes the children's states
+    const long long level_tau_off = prev_off < 0 ? 0 : prev_off + level_size;
     rc = cyr_launch_tree_level(simt_precision(p), workspace, alloc, eps, node_state, S, p->E, L, cap,
-                               (int)parents, epad, nodes, prev_off, level_off, status, st);
+                               (int)parents, epad, nodes, par_off, level_tau_off + base * R, status,
+                               st);
     if (rc != CYR_OK) break;
-    prev_off = level_off;
-    level_off += parents * R;
-    parents *= R;
+    prev_off = level_tau_off;
+    level_size *= R;
   }
+  (void)level_off;
   if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
   return rc;
 }

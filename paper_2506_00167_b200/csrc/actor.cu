@@ -58,8 +58,9 @@ struct ActorLaunch {
   const int16_t* node;        // node states [S][nodes][epad]
   const int32_t* mcs;         // [S][E]
   long long nodes_per_slot;
-  long long parent_off;       // node offset of the parent level, -1 for the root
+  long long parent_off;       // node offset of the first parent of this launch, -1 for the root
   int parents, tau, M, epad;
+  int parent_base;            // level index of the first parent (subtree shards; digits -> arrivals)
   double mcs_scale;
 };
 
@@ -82,7 +83,7 @@ __device__ __forceinline__ double mode_t_feature(const ActorLaunch& p, int col, 
   }
   if (i <= 3 * E) return (double)p.mcs[(long long)s * E + (i - 2 * E - 1)] / p.mcs_scale;
   if (i == 3 * E + 1) {
-    int arrivals = 0, x = q;
+    int arrivals = 0, x = p.parent_base + q;
     for (int d = 1; d < p.tau; ++d) {
       arrivals += x % (p.cap + 1);
       x /= (p.cap + 1);
@@ -437,13 +438,18 @@ int launch_actor_cluster(const ActorLaunch& p, int G, cudaStream_t stream,
 
 // ------------------------------------------------------ tiled batch K2
 // Register-blocked SIMT GEMM chain for large column batches (Mode R over
-// many slots, Mode T levels).  Thread (og, cg) of a 256-thread CTA owns an
+// many slots, Mode T levels).  Consumer thread (og, cg) of 8 warps owns an
 // 8-output x TC/8-column micro-tile of a 256-output panel: per input row it
 // reads 8 weights (128-bit, conflict-free: the warp covers one contiguous
 // 1 KB panel row) and TC/8 activations (warp broadcast) and issues
 // 8*TC/8 FMAs.  Weights stream through a 4-stage TMA bulk-copy ring
-// (paneled layout [panel][in][pw]); activations stay in shared memory.
-constexpr int kTileThreads = 256;
+// (paneled layout [panel][in][pw], thread-interleaved so thread og's 8
+// contiguous weights are outputs og + a*pw/8) filled by a producer warp;
+// consumer warps release a stage by arriving on its "empty" mbarrier, so no
+// CTA barrier sits inside the K loop.  Activations stay in shared memory;
+// biases are read into registers before each panel's K loop.
+constexpr int kTileThreads = 256;   // consumer threads
+constexpr int kTileProducer = 32;   // + one producer warp
 constexpr int kTileStageBytes = 16 * 1024;
 constexpr int kTileStages = 4;
 
@@ -482,57 +488,57 @@ __device__ __forceinline__ void ld_vec(const T* src, T (&dst)[N]) {
   }
 }
 
+__device__ __forceinline__ void consumer_sync() {  // the 256 consumer threads only
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+}
+
 template <typename T, int TC>
-__global__ void __launch_bounds__(kTileThreads, 1) actor_tiled_kernel(const ActorLaunch p) {
+__global__ void __launch_bounds__(kTileThreads + kTileProducer, 1)
+    actor_tiled_kernel(const ActorLaunch p) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int CPT = TC / 8;
   constexpr int TCP = TC + 16 / (int)sizeof(T);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + kTileStages;
   unsigned char* ring = smem + 128;
   T* act_a = reinterpret_cast<T*>(ring + (size_t)kTileStages * kTileStageBytes);
   T* act_b = act_a + (size_t)p.desc.max_width * TCP;
   const int tid = threadIdx.x;
-  const int og = tid & 31, cg = tid >> 5;
   const int c0 = blockIdx.x * TC;
   const T* blob = static_cast<const T*>(p.blob);
   const int nl = p.desc.n_layers;
 
-  int total = 0;
-  for (int l = 0; l < nl; ++l) {
-    const LayerDesc& L = p.desc.layer[l];
-    const int r = tile_rows(L, sizeof(T));
-    total += tile_panels(L) * ((L.in + r - 1) / r);
-  }
-  auto issue = [&](int g) {  // single thread: stage g = (layer, panel, chunk)
-    int l = 0, first = 0;
-    for (;; ++l) {
-      const LayerDesc& L = p.desc.layer[l];
-      const int r = tile_rows(L, sizeof(T));
-      const int n = tile_panels(L) * ((L.in + r - 1) / r);
-      if (g < first + n) break;
-      first += n;
-    }
-    const LayerDesc& L = p.desc.layer[l];
-    const int r = tile_rows(L, sizeof(T));
-    const int chunks = (L.in + r - 1) / r;
-    const int panel = (g - first) / chunks, chunk = (g - first) % chunks;
-    const int i0 = chunk * r;
-    const int nr = min(r, L.in - i0);
-    const uint32_t bytes = (uint32_t)nr * L.pw * sizeof(T);
-    const int buf = g % kTileStages;
-    mbar_expect_tx(&full[buf], bytes);
-    bulk_g2s(ring + (size_t)buf * kTileStageBytes,
-             blob + L.wp_off + ((long long)panel * L.in + i0) * L.pw, bytes, &full[buf]);
-  };
-
   if (tid == 0) {
-    for (int st = 0; st < kTileStages; ++st) mbar_init(&full[st], 1);
+    for (int st = 0; st < kTileStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kTileThreads / 32);
+    }
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0)
-    for (int g = 0; g < min(kTileStages, total); ++g) issue(g);
 
+  if (tid >= kTileThreads) {  // producer warp: stage g = (layer, panel, chunk) in order
+    if (tid == kTileThreads) {
+      int g = 0;
+      for (int l = 0; l < nl; ++l) {
+        const LayerDesc& L = p.desc.layer[l];
+        const int r = tile_rows(L, sizeof(T));
+        const int npan = tile_panels(L);
+        for (int panel = 0; panel < npan; ++panel)
+          for (int i0 = 0; i0 < L.in; i0 += r, ++g) {
+            const int buf = g % kTileStages;
+            if (g >= kTileStages) mbar_wait(&empty[buf], (uint32_t)((g / kTileStages - 1) & 1));
+            const uint32_t bytes = (uint32_t)min(r, L.in - i0) * L.pw * sizeof(T);
+            mbar_expect_tx(&full[buf], bytes);
+            bulk_g2s(ring + (size_t)buf * kTileStageBytes,
+                     blob + L.wp_off + ((long long)panel * L.in + i0) * L.pw, bytes, &full[buf]);
+          }
+      }
+    }
+    return;
+  }
+
+  const int og = tid & 31, cg = tid >> 5;
   const int in0 = p.desc.layer[0].in;
   for (int idx = tid; idx < in0 * TC; idx += kTileThreads) {
     const int i = idx / TC, c = idx % TC, col = c0 + c;
@@ -548,7 +554,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) actor_tiled_kernel(const Acto
     }
     act_a[i * TCP + c] = (T)v;
   }
-  __syncthreads();
+  consumer_sync();
 
   T* cur = act_a;
   T* nxt = act_b;
@@ -571,7 +577,17 @@ __global__ void __launch_bounds__(kTileThreads, 1) actor_tiled_kernel(const Acto
       constexpr int kNc = CPT > 1 ? 2 : 1;  // columns per thread in the narrow mapping
       const int my_og = narrow ? tid % ogn : og;
       const int my_c = narrow ? (tid / ogn) * kNc : cg * CPT;  // first column of this thread
-      const bool active = narrow ? my_c < TC : og * 8 < L.pw;
+      const int G = L.pw / 8;  // wide panels: thread og owns outputs og + G*a
+      const bool active = narrow ? my_c < TC : og < G;
+      // a -> output within the layer (wide: interleaved, so the epilogue's
+      // row stores of a warp hit consecutive rows: no bank conflicts)
+      auto out_of = [&](int a) { return panel * L.pw + (narrow ? my_og * 8 + a : og + G * a); };
+      T bias[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        const int o = out_of(a);
+        bias[a] = (active && o < L.out) ? blob[L.b_off + o] : T(0);
+      }
       for (int i0 = 0; i0 < L.in; i0 += rows, ++g) {
         const int buf = g % kTileStages;
         mbar_wait(&full[buf], (uint32_t)((g / kTileStages) & 1));
@@ -602,20 +618,19 @@ __global__ void __launch_bounds__(kTileThreads, 1) actor_tiled_kernel(const Acto
             }
           }
         }
-        __syncthreads();  // every thread is done with this stage
-        if (tid == 0 && g + kTileStages < total) issue(g + kTileStages);
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[buf]);  // this warp is done with the stage
       }
       if (active) {
         const int ncol = narrow ? kNc : CPT;
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
-          const int o = panel * L.pw + my_og * 8 + a;
+          const int o = out_of(a);
           if (o >= L.out) continue;
-          const T bias = blob[L.b_off + o];
 #pragma unroll
           for (int b = 0; b < CPT; ++b) {
             if (b >= ncol) break;
-            const T z = acc[a][b] + bias;
+            const T z = acc[a][b] + bias[a];
             if (!last) {
               nxt[(size_t)o * TCP + my_c + b] = z > T(0) ? z : T(0);
             } else {
@@ -626,7 +641,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) actor_tiled_kernel(const Acto
         }
       }
     }
-    __syncthreads();
+    consumer_sync();
     T* t = cur;
     cur = nxt;
     nxt = t;
@@ -648,7 +663,7 @@ int launch_actor_tiled(const ActorLaunch& p, cudaStream_t stream) {
     configured = (int)smem;
   }
   const int blocks = (p.ncols + TC - 1) / TC;
-  kern<<<blocks, kTileThreads, smem, stream>>>(p);
+  kern<<<blocks, kTileThreads + kTileProducer, smem, stream>>>(p);
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
 }
 
@@ -841,7 +856,8 @@ int cyr_launch_actor_mode_t(int precision, const cyr::ActorDesc& desc, const voi
                             const int32_t* alloc, const int32_t* mcs, const int16_t* node,
                             int S, int E, int N, int cap, int M, int tau, int parents,
                             long long nodes_per_slot, long long parent_off, int epad,
-                            double mcs_scale, void* raw, int sm_count, cudaStream_t stream) {
+                            double mcs_scale, void* raw, int sm_count, cudaStream_t stream,
+                            int parent_base) {
   if (S <= 0) return CYR_OK;
   if (desc.max_width > cyr::kMaxWidth) return CYR_UNSUPPORTED;
   cyr::ActorLaunch p{};
@@ -862,6 +878,7 @@ int cyr_launch_actor_mode_t(int precision, const cyr::ActorDesc& desc, const voi
   p.nodes_per_slot = nodes_per_slot;
   p.parent_off = parent_off;
   p.parents = parents;
+  p.parent_base = parent_base;
   p.tau = tau;
   p.M = M;
   p.epad = epad;

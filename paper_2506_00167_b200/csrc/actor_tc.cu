@@ -45,6 +45,7 @@ struct TcLaunch {
   const int16_t* node;
   const int32_t* mcs;
   long long nodes_per_slot, parent_off;
+  int parent_base;  // level index of the first parent (subtree shards)
   int parents, tau, M, epad;
   double mcs_scale;
 };
@@ -156,7 +157,7 @@ __device__ __forceinline__ void tc_feature_tile(const TcLaunch& p, int col, int 
   }
   tc_put(a, row, t, E, (double)k / (double)p.cap);
   if (p.mode_t) {
-    int arrivals = 0, x = q;
+    int arrivals = 0, x = p.parent_base + q;
     for (int d = 1; d < p.tau; ++d) {
       arrivals += x % (p.cap + 1);
       x /= (p.cap + 1);
@@ -344,9 +345,6 @@ struct TcWideLaunch {
   unsigned char* act_out;       // [ncb][ceil(out/64)][16 KB]
 };
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 __device__ __forceinline__ void epi_sync() {  // the 128 epilogue threads only
   asm volatile("bar.sync 1, 128;" ::: "memory");
 }
@@ -559,7 +557,7 @@ int cyr_launch_actor_tc(const cyr::ActorDesc& desc, const unsigned char* tc_blob
                         const int32_t* alloc, int S, int E, int N, int cap, float* raw,
                         int mode_t, const int32_t* mcs, const int16_t* node, int M, int tau,
                         int parents, long long nodes_per_slot, long long parent_off, int epad,
-                        double mcs_scale, cudaStream_t stream) {
+                        double mcs_scale, cudaStream_t stream, int parent_base) {
   cyr::TcLaunch p{};
   p.desc = desc;
   for (int l = 0; l < desc.n_layers; ++l) {
@@ -585,6 +583,7 @@ int cyr_launch_actor_tc(const cyr::ActorDesc& desc, const unsigned char* tc_blob
   p.nodes_per_slot = nodes_per_slot;
   p.parent_off = parent_off;
   p.parents = parents;
+  p.parent_base = parent_base;
   p.tau = tau;
   p.M = M;
   p.epad = epad;
@@ -608,7 +607,8 @@ int cyr_launch_actor_tc_layer(const cyr::ActorDesc& desc, const unsigned char* t
                               const unsigned char* act_in, unsigned char* act_out, int mode_t,
                               const int32_t* mcs, const int16_t* node, int M, int tau,
                               int parents, long long nodes_per_slot, long long parent_off,
-                              int epad, double mcs_scale, cudaStream_t stream) {
+                              int epad, double mcs_scale, cudaStream_t stream,
+                              int parent_base) {
   cyr::TcWideLaunch q{};
   cyr::TcLaunch& p = q.base;
   p.desc = desc;
@@ -630,6 +630,7 @@ int cyr_launch_actor_tc_layer(const cyr::ActorDesc& desc, const unsigned char* t
   p.nodes_per_slot = nodes_per_slot;
   p.parent_off = parent_off;
   p.parents = parents;
+  p.parent_base = parent_base;
   p.tau = tau;
   p.M = M;
   p.epad = epad;

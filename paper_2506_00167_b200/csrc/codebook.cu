@@ -118,6 +118,23 @@ __global__ void __launch_bounds__(32 * kLaneWarps) tree_level_kernel(const RawT*
                                    status, lane_smem + (size_t)w * lane_scratch_bytes(io.E));
 }
 
+// K3 of a SMALL Mode-T level (few rows: the lane mapping would leave the
+// machine empty and serialise E divisions per lane): one warp per row, lane
+// = eMBB user, 32 / cap parents per CTA (codebook_rows_io, the latency
+// path's mapping).
+template <typename RawT>
+__global__ void __launch_bounds__(1024) tree_level_warp_kernel(const RawT* __restrict__ raw,
+                                                             TreeIO io, long long groups, int L,
+                                                             int32_t* __restrict__ status) {
+  __shared__ RowScratch sc;
+  const int gpc = 32 / io.cap;
+  const long long g0 = (long long)blockIdx.x * gpc;
+  const int n = (int)min((long long)gpc, groups - g0);
+  const long long row0 = g0 * io.cap;
+  codebook_rows_io<RawT, TreeIO>(raw + row0 * 2 * io.E, row0, n * io.cap, io.cap, io.E, L, io,
+                                 status, sc);
+}
+
 // ------------------------------------------------------- standalone enforcer
 // One CTA = one coupled call of up to 256 rows; warps stride over rows in
 // phases 1 and 3 (re-reading b and caps, which stay in L1), warp 0 runs the
@@ -198,6 +215,104 @@ __global__ void __launch_bounds__(512) enforce_kernel(
     kl_setup(row, E);
     row.lo = s_lo[r];
     row.hi = s_hi[r];
+    double m, nu;
+    kl_finish(row, E, m, nu);
+    double margin = CUDART_INF;
+    int g = 0;
+    if (grants) g = hh_row(m, row.c, E, demand[r], margin);  // warp-uniform
+    if (in) {
+      if (m_out) m_out[(long long)r * E + lane] = m;
+      if (grants) grants[(long long)r * E + lane] = g;
+    }
+    if (lane == 0) {
+      if (nu_out) nu_out[r] = nu;
+      if (degen_out) degen_out[r] = row.degen ? 1 : 0;
+      if (margin_out) margin_out[r] = margin;
+    }
+  }
+}
+
+// ------------------------------------------ standalone enforcer, any R rows
+// A coupled call of more rows than one CTA holds (sac.critic_targets
+// enforces H*(M-1) = 1,536 rows in one call, sac.py:202-205).  Each row's
+// bracket evolves independently (enforcer.py:94-97 update every bisecting
+// row every step); only the STOP iteration is shared: the loop ends at the
+// first t with every row converged (enforcer.py:90-92).  A row stays
+// converged once it is (the bracket width at least halves each step while
+// the tolerance 1e-13*hi moves by < 1 ulp-of-width), so
+// t* = max over rows of the row's own first converged step.  Pass 1 finds
+// each row's threshold and first converged step (atomicMax -> t*); pass 2
+// replays t* steps per row, CHECKS that the row is converged there (status
+// CYR_INTERNAL otherwise: the result would not be the reference's), then
+// finishes m_hat / nu and Huntington-Hill like enforce_kernel.
+__device__ __forceinline__ bool bracket_converged(double lo, double hi) {
+  return __dsub_rn(hi, lo) <= __dmul_rn(kRelWidth, hi);  // enforcer.py:91
+}
+__device__ __forceinline__ void bracket_step(double& lo, double& hi, double& sl, double& sh,
+                                             long long T) {
+  const double mid = __dmul_rn(sl, sh);  // enforcer.py:94
+  const double root = __dsqrt_rn(mid);
+  if (__double_as_longlong(mid) <= T) {  // fill >= demand (exact threshold, §4.3)
+    lo = mid;
+    sl = root;
+  } else {
+    hi = mid;
+    sh = root;
+  }
+}
+
+__global__ void __launch_bounds__(256) enforce_wide_setup_kernel(
+    const double* __restrict__ b, const double* __restrict__ caps,
+    const double* __restrict__ demand_f, const int64_t* __restrict__ demand, int R, int E,
+    long long* __restrict__ thr_out, int* __restrict__ stop, int32_t* __restrict__ status) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  int my_stop = 0;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < R; r += nw) {
+    Row row = load_row(b, caps, demand_f, demand, r, E);
+    const bool neg = __any_sync(kFull, row.b < 0.0 || row.c < 0.0) || row.d < 0.0;
+    const double capsum = np_row_sum(row.c, E);
+    if (lane == 0) {
+      if (neg) set_status(status, CYR_BAD_ARG);
+      else if (demand_f ? row.d > __dadd_rn(capsum, 1e-9) : row.d > capsum)
+        set_status(status, CYR_INFEASIBLE);
+    }
+    kl_setup(row, E);
+    long long thr = 0;
+    if (row.bis) {
+      thr = fill_threshold(row, E, water_level(row, E));
+      double lo = row.lo, hi = row.hi, sl = __dsqrt_rn(lo), sh = __dsqrt_rn(hi);
+      int t = 0;
+      for (; t < kMaxIters && !bracket_converged(lo, hi); ++t) bracket_step(lo, hi, sl, sh, thr);
+      my_stop = max(my_stop, t);
+    }
+    if (lane == 0) thr_out[r] = thr;
+  }
+  if (lane == 0 && my_stop > 0) atomicMax(stop, my_stop);
+}
+
+__global__ void __launch_bounds__(256) enforce_wide_finish_kernel(
+    const double* __restrict__ b, const double* __restrict__ caps,
+    const double* __restrict__ demand_f, const int64_t* __restrict__ demand, int R, int E,
+    const long long* __restrict__ thr_in, const int* __restrict__ stop,
+    double* __restrict__ m_out, double* __restrict__ nu_out, uint8_t* __restrict__ degen_out,
+    int64_t* __restrict__ grants, double* __restrict__ margin_out, int32_t* __restrict__ status) {
+  const int lane = threadIdx.x & 31;
+  const bool in = lane < E;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int t_stop = *stop;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < R; r += nw) {
+    Row row = load_row(b, caps, demand_f, demand, r, E);
+    kl_setup(row, E);
+    if (row.bis) {
+      const long long thr = thr_in[r];
+      double lo = row.lo, hi = row.hi, sl = __dsqrt_rn(lo), sh = __dsqrt_rn(hi);
+      for (int t = 0; t < t_stop; ++t) bracket_step(lo, hi, sl, sh, thr);
+      if (t_stop < kMaxIters && !bracket_converged(lo, hi) && lane == 0)
+        set_status(status, CYR_INTERNAL);
+      row.lo = lo;
+      row.hi = hi;
+    }
     double m, nu;
     kl_finish(row, E, m, nu);
     double margin = CUDART_INF;
@@ -343,12 +458,31 @@ int cyr_launch_codebook(int precision, const void* raw, const int32_t* alloc, co
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
 }
 
+// rows of one coupled call that the single-CTA enforce_kernel holds
+constexpr int kOneCtaRows = 256;
+
 int cyr_launch_enforce(const double* b, const double* caps, const double* demand_f,
                        const int64_t* demand, int R, int E,
                        double* m_hat, double* nu, uint8_t* degenerate, int64_t* grants,
                        double* margin, int32_t* status, cudaStream_t stream) {
   if (R <= 0) return CYR_OK;
-  if (E < 1 || E > cyr::kMaxUsers || R > 256) return CYR_UNSUPPORTED;
+  if (E < 1 || E > cyr::kMaxUsers) return CYR_UNSUPPORTED;
+  if (R > kOneCtaRows) {  // multi-CTA coupled call (two passes, stream-ordered scratch)
+    const size_t bytes = (size_t)R * sizeof(long long) + 16;
+    void* scratch = nullptr;
+    if (cudaMallocAsync(&scratch, bytes, stream) != cudaSuccess) return CYR_CUDA_ERROR;
+    int* stop = reinterpret_cast<int*>(scratch);
+    long long* thr = reinterpret_cast<long long*>(static_cast<unsigned char*>(scratch) + 16);
+    cudaMemsetAsync(stop, 0, sizeof(int), stream);
+    const int blocks = (R + 7) / 8;
+    cyr::enforce_wide_setup_kernel<<<blocks, 256, 0, stream>>>(b, caps, demand_f, demand, R, E, thr,
+                                                               stop, status);
+    cyr::enforce_wide_finish_kernel<<<blocks, 256, 0, stream>>>(
+        b, caps, demand_f, demand, R, E, thr, stop, m_hat, nu, degenerate, grants, margin, status);
+    const cudaError_t e = cudaPeekAtLastError();
+    cudaFreeAsync(scratch, stream);
+    return e == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
+  }
   const int nw = R < 16 ? R : 16;
   cyr::enforce_kernel<<<1, 32 * nw, 0, stream>>>(b, caps, demand_f, demand, R, E, m_hat, nu,
                                                 degenerate, grants, margin, status);
@@ -367,6 +501,15 @@ int cyr_launch_latency_bench(int which, int iters, long long* cycles, double* si
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
 }
 
+// rows at or below which a Mode-T level runs warp-per-row (CYR_WARP_LEVEL_ROWS)
+static long long warp_level_rows() {
+  static const long long v = [] {
+    const char* e = getenv("CYR_WARP_LEVEL_ROWS");
+    return e ? atoll(e) : 8192ll;
+  }();
+  return v;
+}
+
 int cyr_launch_tree_level(int precision, const void* raw, const int32_t* alloc, const double* eps,
                           int16_t* node, int S, int E, int L, int cap, int parents, int epad,
                           long long nodes_per_slot, long long parent_off, long long child_off,
@@ -375,6 +518,18 @@ int cyr_launch_tree_level(int precision, const void* raw, const int32_t* alloc, 
   if (E < 1 || E > cyr::kMaxUsers || cap < 1 || cap > 16) return CYR_UNSUPPORTED;
   cyr::TreeIO io{alloc, eps, node, E, cap, epad, parents, nodes_per_slot, parent_off, child_off};
   const long long groups = (long long)S * parents;
+  if (groups * cap <= warp_level_rows()) {  // small level: warp per row (latency)
+    const int gpc = 32 / cap;
+    const long long blocks = (groups + gpc - 1) / gpc;
+    const int threads = 32 * gpc * cap;
+    if (precision == CYR_FP64)
+      cyr::tree_level_warp_kernel<double><<<(unsigned)blocks, threads, 0, stream>>>(
+          static_cast<const double*>(raw), io, groups, L, status);
+    else
+      cyr::tree_level_warp_kernel<float><<<(unsigned)blocks, threads, 0, stream>>>(
+          static_cast<const float*>(raw), io, groups, L, status);
+    return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
+  }
   const long long per_cta = (long long)cyr::kLaneWarps * (32 / cap);
   const long long blocks = (groups + per_cta - 1) / per_cta;
   if (blocks >= (1ll << 31)) return CYR_UNSUPPORTED;

@@ -94,6 +94,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // TMA bulk copy global -> shared, completion counted on an mbarrier.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -151,7 +154,7 @@ struct LayerDesc {
   long long b_off;        // element offset of the bias
   long long wr_off;       // element offset of the row-major W copy
   int pw;                 // panel width of the tiled K2 layout (<= 256 outputs)
-  long long wp_off;       // paneled Wt: [ceil(out_pad/pw)][in][pw] (== w_off if one panel)
+  long long wp_off;       // paneled Wt: [ceil(out_pad/pw)][in][pw]; pw > 64: thread-interleaved
 };
 
 // Single-slot inputs passed BY VALUE in the kernel launch (param space, read
@@ -201,7 +204,8 @@ int cyr_launch_actor_mode_t(int precision, const cyr::ActorDesc& desc, const voi
                             const int32_t* alloc, const int32_t* mcs, const int16_t* node,
                             int S, int E, int N, int cap, int M, int tau, int parents,
                             long long nodes_per_slot, long long parent_off, int epad,
-                            double mcs_scale, void* raw, int sm_count, cudaStream_t stream);
+                            double mcs_scale, void* raw, int sm_count, cudaStream_t stream,
+                            int parent_base = 0);
 int cyr_launch_tree_level(int precision, const void* raw, const int32_t* alloc, const double* eps,
                           int16_t* node, int S, int E, int L, int cap, int parents, int epad,
                           long long nodes_per_slot, long long parent_off, long long child_off,
@@ -212,11 +216,12 @@ int cyr_launch_actor_tc(const cyr::ActorDesc& desc, const unsigned char* tc_blob
                         const int32_t* alloc, int S, int E, int N, int cap, float* raw,
                         int mode_t, const int32_t* mcs, const int16_t* node, int M, int tau,
                         int parents, long long nodes_per_slot, long long parent_off, int epad,
-                        double mcs_scale, cudaStream_t stream);
+                        double mcs_scale, cudaStream_t stream, int parent_base = 0);
 int cyr_launch_actor_tc_layer(const cyr::ActorDesc& desc, const unsigned char* tc_blob,
                               long long w_off, int npad, int l, const float* bias_blob,
                               const int32_t* alloc, int S, int E, int N, int cap, float* raw,
                               const unsigned char* act_in, unsigned char* act_out, int mode_t,
                               const int32_t* mcs, const int16_t* node, int M, int tau,
                               int parents, long long nodes_per_slot, long long parent_off,
-                              int epad, double mcs_scale, cudaStream_t stream);
+                              int epad, double mcs_scale, cudaStream_t stream,
+                              int parent_base = 0);

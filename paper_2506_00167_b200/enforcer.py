@@ -7,7 +7,8 @@ demand above capacity -> InfeasibleDemandError), but compute on the GPU
 through the C ABI (K3 core):
 
 * one call == one coupled bisection (the stop test spans every bisecting
-  row of the call, enforcer.py:90-92); up to 256 rows per call;
+  row of the call, enforcer.py:90-92), any number of rows (one CTA up to
+  256, a two-pass multi-CTA call above);
 * results are bit-identical to the reference for identical float64 inputs
   (tests/test_gpu_parity.py).
 """
@@ -20,9 +21,6 @@ from . import _native
 from ._native import InfeasibleDemandError
 
 __all__ = ["InfeasibleDemandError", "kl_project_batch", "apportion_batch", "enforce_batch"]
-
-MAX_COUPLED_ROWS = 256
-
 
 def _validate_projection(b, caps, demand):
     b = np.ascontiguousarray(b, dtype=np.float64)
@@ -40,8 +38,6 @@ def _validate_projection(b, caps, demand):
 def _run(b, caps, demand_i64, want_grants=True):
     import torch
     rows, users = b.shape
-    if rows > MAX_COUPLED_ROWS:
-        raise ValueError(f"a coupled enforcement call holds at most {MAX_COUPLED_ROWS} rows")
     dev = torch.device("cuda")
     bd = torch.from_numpy(b).to(dev)
     cd = torch.from_numpy(caps).to(dev)
@@ -70,8 +66,6 @@ def kl_project_batch(b, caps, demand):
     rows, users = b.shape
     if rows == 0:
         return np.zeros_like(b), np.zeros(0), np.zeros(0, dtype=bool)
-    if rows > MAX_COUPLED_ROWS:
-        raise ValueError(f"a coupled enforcement call holds at most {MAX_COUPLED_ROWS} rows")
     dev = torch.device("cuda")
     bd, cd = torch.from_numpy(b).to(dev), torch.from_numpy(caps).to(dev)
     dd = torch.from_numpy(np.ascontiguousarray(demand)).to(dev)

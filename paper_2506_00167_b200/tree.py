@@ -121,12 +121,15 @@ def bridge_actor(actor) -> MlpParams:
 
 
 def build_tree_mode_t(policy, cell, allocs, mcs, eps=None, mcs_scale: float = DEFAULT_MCS_SCALE,
-                      out=None, workspace=None, status=None, stream=None):
+                      out=None, workspace=None, status=None, stream=None, shard=None):
     """Mode-T arrival tree for S slots on the current stream.
 
     policy: a DevicePolicy of a Mode-T actor; allocs, mcs: CUDA int32 (S, E);
     eps: CUDA float64 (S, cap, E) or None.  Returns node states int16
-    (S, nodes, Epad) in the Mode-R layout.
+    (S, nodes, Epad) in the Mode-R layout.  ``shard`` = (level, first,
+    count) builds only the subtrees below level-``level`` nodes
+    [first, first + count) (plus the replicated levels <= ``level``); other
+    records are left untouched (see subtree_ranges).
     """
     import torch
     check_tree_geometry(cell)
@@ -143,12 +146,87 @@ def build_tree_mode_t(policy, cell, allocs, mcs, eps=None, mcs_scale: float = DE
     own_status = status is None
     if own_status:
         status = torch.zeros(1, dtype=torch.int32, device=dev)
-    _native.check(lib.cyr_tree_mode_t_device(
+    level, first, count = (0, 0, 1) if shard is None else (int(v) for v in shard)
+    _native.check(lib.cyr_tree_mode_t_shard_device(
         policy.handle, allocs.data_ptr(), mcs.data_ptr(), None if eps is None else eps.data_ptr(),
-        s, cell.total_scs, cell.urllc_sc_len, m, float(mcs_scale), out.data_ptr(),
-        workspace.data_ptr(), status.data_ptr(), _native.stream_handle(stream)), "mode-T tree")
+        s, cell.total_scs, cell.urllc_sc_len, m, float(mcs_scale), level, first, count,
+        out.data_ptr(), workspace.data_ptr(), status.data_ptr(), _native.stream_handle(stream)),
+        "mode-T tree")
     if own_status:
         code = int(status.item())
         if code:
             _native.check(code, "mode-T tree")
     return out
+
+
+# ------------------------------------------------------- Mode-T subtree shards
+# SURVEY.md §8(e): below level l the subtrees are independent, so a tree is
+# split across ranks by contiguous blocks of level-l nodes (l = 1: by the
+# first mini-slot's arrival count, the north star's "first-mini-slot
+# branch"; l = 2-3 balance 8 GPUs: 49 / 343 subtrees at cap 6).  Levels
+# <= l are cheap and every rank builds them.  In BFS order the nodes of
+# level tau below level-l nodes [a, b) are [a*R^(tau-l), b*R^(tau-l)), so a
+# shard is one contiguous run per level.
+
+def subtree_ranges(cap: int, minislots: int, level: int, first: int, count: int) -> list:
+    """[(node offset, node count)] per level tau > level of the shard's
+    records, in the slot's BFS record order."""
+    r = cap + 1
+    offs = level_offsets(cap, minislots)
+    out = []
+    for tau in range(level + 1, minislots + 1):
+        span = r ** (tau - level)
+        out.append((offs[tau - 1] + first * span, count * span))
+    return out
+
+
+def shard_extent(cap: int, minislots: int, level: int, world: int, rank: int) -> tuple:
+    """(first, count) of rank's contiguous block of level-``level`` nodes."""
+    from .sharding import shard_bounds
+    lo, hi = shard_bounds((cap + 1) ** level, world, rank)
+    return lo, hi - lo
+
+
+def pack_shard(states, cap: int, minislots: int, level: int, first: int, count: int, width: int):
+    """This rank's records (S, width * sum_tau R^(tau-level), Epad): the
+    per-level runs back to back, each padded to ``width`` subtrees."""
+    import torch
+    r = cap + 1
+    runs = subtree_ranges(cap, minislots, level, first, count)
+    total = sum(width * r ** (tau - level) for tau in range(level + 1, minislots + 1))
+    out = torch.zeros((states.shape[0], total, states.shape[2]), dtype=states.dtype,
+                      device=states.device)
+    pos = 0
+    for (off, n), tau in zip(runs, range(level + 1, minislots + 1)):
+        out[:, pos:pos + n] = states[:, off:off + n]
+        pos += width * r ** (tau - level)
+    return out
+
+
+def gather_mode_t_tree(states, cap: int, minislots: int, level: int, group=None):
+    """Assemble the whole Mode-T tree on every rank with ONE all-gather
+    (NCCL over NVLink on GPUs, gloo in the CPU tests).  ``states`` is this
+    rank's (S, nodes, Epad) array holding at least its shard's records and
+    the replicated levels <= ``level``; returns the full tree."""
+    import torch
+    import torch.distributed as dist
+    from .sharding import max_shard
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    width = max_shard((cap + 1) ** level, world)
+    first, count = shard_extent(cap, minislots, level, world, rank)
+    local = pack_shard(states, cap, minislots, level, first, count, width).contiguous()
+    blocks = torch.empty((world,) + tuple(local.shape), dtype=local.dtype, device=local.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(blocks, local, group=group)
+    else:
+        dist.all_gather(list(blocks.unbind(0)), local, group=group)
+    full = states.clone()
+    r = cap + 1
+    for src in range(world):
+        f, c = shard_extent(cap, minislots, level, world, src)
+        pos = 0
+        for (off, n), tau in zip(subtree_ranges(cap, minislots, level, f, c),
+                                 range(level + 1, minislots + 1)):
+            full[:, off:off + n] = blocks[src][:, pos:pos + n]
+            pos += width * r ** (tau - level)
+    return full

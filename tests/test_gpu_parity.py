@@ -98,6 +98,39 @@ def test_enforcer_matches_oracle_property(args):
     assert got.sum() == demand and (got >= 0).all() and (got <= c2).all()
 
 
+def _critic_like_rows(rows, users, seed):
+    """critic_targets-shaped enforcement input (sac.py:194-205): per-row
+    allocations (synthetic schedules), demands k*L, b = (a+1)/2*n."""
+    rng = np.random.default_rng(seed)
+    owners = rng.integers(0, users, size=(rows, 65))
+    caps = np.stack([np.bincount(o, minlength=users) * 12 for o in owners]).astype(float)
+    a = np.tanh(rng.normal(0.0, rng.choice([0.05, 1.0, 6.0], size=(rows, 1)), size=(rows, users)))
+    b = (a + 1.0) * 0.5 * caps
+    b[rng.random((rows, users)) < 0.03] = 0.0          # zero-mass users
+    b[: rows // 50, 0] *= 1e-200                        # wide brackets: late convergence
+    k = rng.integers(1, 5, size=rows)
+    return b, caps, k * 195
+
+
+@pytest.mark.parametrize("rows", [257, 1536, 4099])
+def test_enforcer_wide_coupled_call_bit_exact(rows):
+    """More rows than one CTA holds: the two-pass multi-CTA call keeps the
+    reference's batch-coupled stop (enforcer.py:90-92) bit for bit."""
+    b, caps, dem = _critic_like_rows(rows, 10, rows)
+    got, info = enforcer.enforce_batch(b, caps, dem, with_details=True)
+    want, winfo = projection.enforce(b, caps, dem, with_details=True)
+    assert np.array_equal(info["nu"], winfo["nu"])
+    assert np.array_equal(info["m_hat"], winfo["m_hat"])
+    assert np.array_equal(info["degenerate"], winfo["degenerate"])
+    assert np.array_equal(got, want)
+    m2, nu2, _ = enforcer.kl_project_batch(b, caps, dem.astype(float))
+    assert np.array_equal(m2, winfo["m_hat"]) and np.array_equal(nu2, winfo["nu"])
+    # the coupling is exercised: rows enforced alone stop earlier (other nu bits)
+    alone = np.array([projection.enforce(b[r:r + 1], caps[r:r + 1], dem[r:r + 1],
+                                         with_details=True)[1]["nu"][0] for r in range(64)])
+    assert (alone != winfo["nu"][:64]).any()
+
+
 # ------------------------------------------------------ full pipeline K2+K3
 def _near_tie_rows(cfg, mode, threshold):
     """(slot, branch) rows whose reference HH boundary gap is below threshold."""
