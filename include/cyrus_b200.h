@@ -147,6 +147,31 @@ int cyr_apportion_batch_device(const double* m_hat, const double* caps, const in
                                int32_t R, int32_t E, int64_t* grants, double* margin,
                                int32_t* status, void* stream);
 
+/* ---- SAC critic targets: actor + enforcement on arbitrary columns -------- */
+/* The sampling block of sac.critic_targets (sac.py:190-205), SURVEY §8(f)
+ * row f1: R columns, each with its own allocation row alloc[r] (int32
+ * [R][E]) and arrival count k[r] in 1..cap; actor input [alloc/N, k/cap],
+ * forward (K2, the policy's SIMT precision), split_head, tanh-Gaussian
+ * sample with eps [R][E] (NULL: deterministic mean), action_to_scs, then ONE
+ * coupled enforce_batch over all R rows (caps = alloc[r], demand = k[r]*L).
+ * Outputs: grants [R][E] int64 (the enforced actions), log_pi [R] float64
+ * (neural.py:153-165, NULL to skip), b [R][E] float64 (the raw SC demands,
+ * NULL to skip).  Device pointers, asynchronous on `stream`. */
+int cyr_policy_actions_device(const cyr_policy* policy, const int32_t* alloc, const int32_t* k,
+                              const double* eps, int32_t R, int32_t N, int32_t L,
+                              int64_t* grants, double* log_pi, double* b, int32_t* status,
+                              void* stream);
+
+/* Any ReLU MLP (the SAC critics / target critics, sac.py:114-127: sizes
+ * [2E+1, *hidden, 1]) as a device object; free with cyr_policy_destroy,
+ * re-publish with cyr_policy_update.  precision CYR_FP32 or CYR_FP64. */
+int cyr_mlp_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
+                   const double* weights_blob, int32_t precision);
+/* neural.forward (neural.py:66-84) on explicit float64 inputs x [cols][in];
+ * out [cols][out] in the object's element type (float / double). */
+int cyr_mlp_forward_device(const cyr_policy* mlp, const double* x, int32_t cols, void* out,
+                           void* stream);
+
 /* ---- arrival tree, Mode R (K1) ------------------------------------------- */
 /* Node count excluding the root: sum_{t=1..M} (cap+1)^t. */
 int64_t cyr_tree_num_nodes(int32_t cap, int32_t M);

@@ -21,6 +21,7 @@ Modules:
   mlp          — actor forward + tanh-Gaussian head (neural.py:25-84, 144-183;
                  sac.py:334-355)
   slot         — one slot's codebook (engine.py:97-116), batched over slots
+  critic       — SAC critic targets (sac.py:167-214)
   arrival_tree — Mode-R arrival tree node states (no
                  reference counterpart: composition of engine.py:230 lookups)
 """

@@ -53,6 +53,10 @@ SIGNATURES = {
     "cyr_tree_mode_t_shard_device": (_c_int, [_vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i32, _c_i32,
                                               ctypes.c_double, _c_i32, _c_i64, _c_i64, _vp, _vp,
                                               _vp, _vp]),
+    "cyr_policy_actions_device": (_c_int, [_vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i32, _vp, _vp,
+                                           _vp, _vp, _vp]),
+    "cyr_mlp_create": (_c_int, [ctypes.POINTER(_vp), _vp, _c_i32, _vp, _c_i32]),
+    "cyr_mlp_forward_device": (_c_int, [_vp, _vp, _c_i32, _vp, _vp]),
     "cyr_debug_trace": (_c_int, [_pi64, _c_i32]),
     "cyr_selftest_latency": (_c_int, [_c_i32, _c_i32, _pi64]),
     "cyr_selftest_launch": (_c_int, [_c_i32, _c_i32, _pi64]),

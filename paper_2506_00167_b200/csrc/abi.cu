@@ -81,6 +81,7 @@ struct cyr_policy {
   std::vector<int> sizes;
   int E = 0;
   int mode_t = 0;  // inputs: 0 = [n/N, j/cap] (E+1), 1 = Mode-T node-state features (3E+3)
+  bool generic = false;  // any MLP (cyr_mlp_create): explicit feature inputs only
   size_t elem = 4;
   cyr::ActorDesc desc{};
   void* blob_d = nullptr;
@@ -130,6 +131,7 @@ namespace {
 template <typename T>
 void pack_blob(const cyr_policy& p, const double* src, std::vector<T>& dst) {
   dst.assign(p.blob_elems, T(0));
+  const int vec = 16 / (int)sizeof(T);
   size_t off = 0;
   for (int l = 0; l < p.desc.n_layers; ++l) {
     const cyr::LayerDesc& L = p.desc.layer[l];
@@ -140,8 +142,9 @@ void pack_blob(const cyr_policy& p, const double* src, std::vector<T>& dst) {
       for (int i = 0; i < L.in; ++i)
         dst[L.wr_off + (size_t)o * L.in_pad + i] = (T)src[off + (size_t)o * L.in + i];
     for (int o = 0; o < L.out; ++o) {
-      const int oo = o % L.pw, g = L.pw / 8;
-      const int pos = L.pw > 64 ? (oo % g) * 8 + oo / g : oo;
+      const int oo = o % L.pw, g = L.pw / 8, v = vec;
+      const int og = oo % g, a = oo / g;
+      const int pos = L.pw > 64 ? (a / v) * g * v + og * v + a % v : oo;
       for (int i = 0; i < L.in; ++i)
         dst[L.wp_off + ((size_t)(o / L.pw) * L.in + i) * L.pw + pos] =
             (T)src[off + (size_t)o * L.in + i];
@@ -359,23 +362,29 @@ int cyr_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor) {
   return CYR_OK;
 }
 
-int cyr_policy_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
-                      const double* weights_blob, int32_t precision) {
+namespace {
+int policy_create_impl(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
+                       const double* weights_blob, int32_t precision, bool generic) {
   if (!out || !sizes || !weights_blob || n_sizes < 2 || n_sizes - 1 > cyr::kMaxLayers)
     return CYR_BAD_ARG;
   if (precision != CYR_FP32 && precision != CYR_FP64 && precision != CYR_BF16_TC)
     return CYR_BAD_ARG;
-  if (sizes[n_sizes - 1] % 2 != 0) return CYR_BAD_ARG;
-  const int E = sizes[n_sizes - 1] / 2;
-  if (E < 1 || E > cyr::kMaxUsers) return CYR_BAD_ARG;
-  if (sizes[0] != E + 1 && sizes[0] != 3 * E + 3) return CYR_BAD_ARG;
+  if (generic && precision == CYR_BF16_TC) return CYR_BAD_ARG;
+  int E = 0;
+  if (!generic) {
+    if (sizes[n_sizes - 1] % 2 != 0) return CYR_BAD_ARG;
+    E = sizes[n_sizes - 1] / 2;
+    if (E < 1 || E > cyr::kMaxUsers) return CYR_BAD_ARG;
+    if (sizes[0] != E + 1 && sizes[0] != 3 * E + 3) return CYR_BAD_ARG;
+  }
   for (int i = 0; i < n_sizes; ++i)
     if (sizes[i] < 1 || sizes[i] > cyr::kMaxWidth) return CYR_UNSUPPORTED;
   cyr_policy* p = new cyr_policy();
   p->precision = precision;
   p->sizes.assign(sizes, sizes + n_sizes);
   p->E = E;
-  p->mode_t = sizes[0] == 3 * E + 3;
+  p->generic = generic;
+  p->mode_t = !generic && sizes[0] == 3 * E + 3;
   p->elem = precision == CYR_FP64 ? 8 : 4;
   p->sm_count = sm_count_of_current_device();
   const int vec = 16 / (int)p->elem;
@@ -396,8 +405,10 @@ int cyr_policy_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
     L.wr_off = (long long)off;
     off += (size_t)L.out * L.in_pad;
     // paneled copy for the tiled batch kernel: panels of <= 256 outputs;
-    // wide panels (pw > 64) are rounded to 8 and stored thread-interleaved
-    // (position og*8 + a holds output og + a*pw/8, see actor_tiled_kernel)
+    // wide panels (pw > 64) are rounded to 8 and stored thread-interleaved:
+    // output og + a*G (G = pw/8, a = 0..7) sits in 16-byte vector chunk
+    // a / V at position chunk*G*V + og*V + a % V (V = 16 / elem), so each
+    // of a warp's vector loads reads one contiguous run (actor_tiled_kernel)
     L.pw = std::min(L.out_pad, 256);
     if (L.pw > 64) L.pw = (L.pw + 7) / 8 * 8;
     L.wp_off = (long long)off;
@@ -449,6 +460,62 @@ int cyr_policy_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
   }
   *out = p;
   return CYR_OK;
+}
+}  // namespace
+
+int cyr_policy_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
+                      const double* weights_blob, int32_t precision) {
+  return policy_create_impl(out, sizes, n_sizes, weights_blob, precision, false);
+}
+
+int cyr_mlp_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
+                   const double* weights_blob, int32_t precision) {
+  return policy_create_impl(out, sizes, n_sizes, weights_blob, precision, true);
+}
+
+int cyr_mlp_forward_device(const cyr_policy* p, const double* x, int32_t cols, void* out,
+                           void* stream) {
+  if (!p || cols < 0 || (cols > 0 && (!x || !out))) return CYR_BAD_ARG;
+  const int rc = cyr_launch_actor_columns(simt_precision(p), p->desc, p->blob_d, nullptr, nullptr,
+                                          x, cols, p->E, 1, 1, out, p->sm_count,
+                                          static_cast<cudaStream_t>(stream));
+  if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+  return rc;
+}
+
+int cyr_policy_actions_device(const cyr_policy* p, const int32_t* alloc, const int32_t* k,
+                              const double* eps, int32_t R, int32_t N, int32_t L, int64_t* grants,
+                              double* log_pi, double* b_out, int32_t* status, void* stream) {
+  if (!p || p->generic || p->mode_t) return CYR_BAD_ARG;
+  int cap = 0;
+  int rc = check_geometry(R, p->E, N, L, &cap);
+  if (rc != CYR_OK) return rc;
+  if (R == 0) return CYR_OK;
+  if (!alloc || !k || !grants || !status) return CYR_BAD_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int E = p->E;
+  const size_t raw_b = ((size_t)R * 2 * E * p->elem + 255) / 256 * 256;
+  const size_t mat_b = ((size_t)R * E * 8 + 255) / 256 * 256;
+  unsigned char* ws = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&ws), raw_b + 3 * mat_b + (size_t)R * 8, st) !=
+      cudaSuccess)
+    return cuda_fail(cudaGetLastError(), "cudaMallocAsync(actions)");
+  void* raw = ws;
+  double* b = b_out ? b_out : reinterpret_cast<double*>(ws + raw_b);
+  double* caps = reinterpret_cast<double*>(ws + raw_b + mat_b);
+  int64_t* demand = reinterpret_cast<int64_t*>(ws + raw_b + 2 * mat_b);
+  const int prec = simt_precision(p);
+  rc = cyr_launch_actor_columns(prec, p->desc, p->blob_d, alloc, k, nullptr, R, E, N, cap, raw,
+                                p->sm_count, st);
+  if (rc == CYR_OK)
+    rc = cyr_launch_actions_head(prec, raw, alloc, k, eps, R, E, L, b, caps, demand, log_pi,
+                                 status, st);
+  if (rc == CYR_OK)
+    rc = cyr_launch_enforce(b, caps, nullptr, demand, R, E, nullptr, nullptr, nullptr, grants,
+                            nullptr, status, st);
+  cudaFreeAsync(ws, st);
+  if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+  return rc;
 }
 
 int cyr_policy_update(cyr_policy* p, const double* weights_blob) {
@@ -857,7 +924,7 @@ int cyr_tree_mode_t_shard_device(const cyr_policy* p, const int32_t* alloc, cons
   long long width = 1;  // nodes of level shard_level
   for (int t = 0; t < shard_level; ++t) width *= R;
   if (first < 0 || count < 0 || first + count > width) return CYR_BAD_ARG;
-  if (S == 0 || count == 0) return CYR_OK;
+  if (S == 0) return CYR_OK;  // count == 0 still builds the replicated levels
   if (!alloc || !mcs || !node_state || !workspace) return CYR_BAD_ARG;
   const int epad = cyr_tree_state_stride(p->E);
   const long long nodes = cyr_tree_num_nodes(cap, M);
@@ -873,6 +940,7 @@ int cyr_tree_mode_t_shard_device(const cyr_policy* p, const int32_t* alloc, cons
       for (int t = shard_level; t < tau - 1; ++t) span *= R;
       base = first * span;
       parents = count * span;
+      if (parents == 0) break;
     }
     const long long par_off = prev_off < 0 ? -1 : prev_off + base;
     // K2: the actor on every (parent, branch) column of this level

@@ -62,6 +62,10 @@ struct ActorLaunch {
   int parents, tau, M, epad;
   int parent_base;            // level index of the first parent (subtree shards; digits -> arrivals)
   double mcs_scale;
+  // column inputs (tiled kernel only): kcol -> column c is [alloc[c]/N, kcol[c]/cap]
+  // (sac.critic_targets, sac.py:190-192); x -> explicit float64 features [c][in]
+  const int32_t* kcol;
+  const double* x;
 };
 
 // Mode-T actor input for column (slot s, parent q, branch k) — feature i of
@@ -544,10 +548,13 @@ __global__ void __launch_bounds__(kTileThreads + kTileProducer, 1)
     const int i = idx / TC, c = idx % TC, col = c0 + c;
     double v = 0.0;
     if (col < p.ncols) {
-      if (p.mode_t) {
+      if (p.x) {
+        v = p.x[(long long)col * in0 + i];
+      } else if (p.mode_t) {
         v = mode_t_feature(p, col, i);
       } else {
-        const int s = col / p.cap, j = col % p.cap + 1;
+        const int s = p.kcol ? col : col / p.cap;
+        const int j = p.kcol ? p.kcol[col] : col % p.cap + 1;
         v = (i < p.E) ? (double)p.alloc[(long long)s * p.E + i] / (double)p.N
                       : (double)j / (double)p.cap;
       }
@@ -597,7 +604,14 @@ __global__ void __launch_bounds__(kTileThreads + kTileProducer, 1)
 #pragma unroll 4
           for (int r = 0; r < nr; ++r) {
             T w[8], x[CPT];
-            ld_vec<T, 8>(W + r * L.pw + og * 8, w);
+            constexpr int V = 16 / (int)sizeof(T);  // interleaved chunks: conflict-free
+#pragma unroll
+            for (int c = 0; c < 8 / V; ++c) {
+              T t[V];
+              ld_vec<T, V>(W + r * L.pw + c * G * V + og * V, t);
+#pragma unroll
+              for (int u = 0; u < V; ++u) w[c * V + u] = t[u];
+            }
             ld_vec<T, CPT>(cur + (size_t)(i0 + r) * TCP + cg * CPT, x);
 #pragma unroll
             for (int a = 0; a < 8; ++a)
@@ -785,6 +799,31 @@ int cyr_launch_actor(int precision, const cyr::ActorDesc& desc, const void* blob
   }
   if (precision == CYR_FP64) return cyr::launch_actor_typed<double>(p, sm_count, stream);
   return cyr::launch_actor_typed<float>(p, sm_count, stream);
+}
+
+// Columns with explicit inputs through the tiled batch kernel: kcol != null
+// -> [alloc[c]/N, kcol[c]/cap] (per-column allocation rows); x != null ->
+// float64 features [ncols][in] (any MLP, e.g. the SAC critics).
+int cyr_launch_actor_columns(int precision, const cyr::ActorDesc& desc, const void* blob,
+                             const int32_t* alloc, const int32_t* kcol, const double* x,
+                             int ncols, int E, int N, int cap, void* raw, int sm_count,
+                             cudaStream_t stream) {
+  if (ncols <= 0) return CYR_OK;
+  if (desc.max_width > cyr::kMaxWidth) return CYR_UNSUPPORTED;
+  cyr::ActorLaunch p{};
+  p.desc = desc;
+  p.blob = blob;
+  p.alloc = alloc;
+  p.kcol = kcol;
+  p.x = x;
+  p.raw = raw;
+  p.S = ncols;
+  p.E = E;
+  p.N = N;
+  p.cap = cap;
+  p.ncols = ncols;
+  if (precision == CYR_FP64) return cyr::launch_actor_tiled_auto<double>(p, sm_count, stream);
+  return cyr::launch_actor_tiled_auto<float>(p, sm_count, stream);
 }
 
 int cyr_cluster_size() {

@@ -330,6 +330,56 @@ __global__ void __launch_bounds__(256) enforce_wide_finish_kernel(
   }
 }
 
+// ------------------------------------------------- SAC branch actions head
+// sac.critic_targets' sampling block (sac.py:193-203) for R columns with
+// their own allocation row and arrival count k (warp per row, lane = user):
+// split_head (neural.py:144-150), sample_squashed with its log-density
+// (neural.py:153-165: a = tanh(mu + sigma*eps), log pi = sum over users, in
+// user order, of -log sigma - log(2 pi)/2 - eps^2/2 - log(1 - a^2 + 1e-6)),
+// action_to_scs (neural.py:181-183), and the enforcement inputs: caps = the
+// row's allocation, demand = k*L (sac.py:202-204).  eps == null: the
+// deterministic mean tanh(mu), log pi = 0.
+constexpr double kHalfLog2Pi = 0.9189385332046727;  // 0.5 * np.log(2.0 * np.pi)
+constexpr double kSquashEps = 1e-6;                 // neural.py:17
+
+template <typename RawT>
+__global__ void __launch_bounds__(256) actions_head_kernel(
+    const RawT* __restrict__ raw, const int32_t* __restrict__ alloc,
+    const int32_t* __restrict__ kcol, const double* __restrict__ eps, int R, int E, int L,
+    double* __restrict__ b_out, double* __restrict__ caps_out, int64_t* __restrict__ demand_out,
+    double* __restrict__ log_pi, int32_t* __restrict__ status) {
+  const int lane = threadIdx.x & 31;
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= R) return;  // warp-uniform
+  const bool in = lane < E;
+  const int k = kcol[r];
+  if (lane == 0 && k < 1) set_status(status, CYR_BAD_ARG);
+  double lp = 0.0;
+  if (in) {
+    const double n = (double)alloc[(long long)r * E + lane];
+    const double mu = (double)raw[(long long)r * 2 * E + lane];
+    const double ls =
+        fmin(fmax((double)raw[(long long)r * 2 * E + E + lane], kLogSigmaMin), kLogSigmaMax);
+    double a;
+    if (eps != nullptr) {
+      const double e = eps[(long long)r * E + lane];
+      a = tanh(__dadd_rn(mu, __dmul_rn(exp(ls), e)));
+      const double t = __dsub_rn(__dsub_rn(-ls, kHalfLog2Pi), __dmul_rn(0.5, __dmul_rn(e, e)));
+      lp = __dsub_rn(t, log(__dadd_rn(__dsub_rn(1.0, __dmul_rn(a, a)), kSquashEps)));
+    } else {
+      a = tanh(mu);
+    }
+    b_out[(long long)r * E + lane] = __dmul_rn(__dmul_rn(__dadd_rn(a, 1.0), 0.5), n);
+    caps_out[(long long)r * E + lane] = n;
+  }
+  double acc = shfl_d(lp, 0);  // numpy's axis-0 sum: user order, sequential
+  for (int e = 1; e < E; ++e) acc = __dadd_rn(acc, shfl_d(lp, e));
+  if (lane == 0) {
+    demand_out[r] = (int64_t)k * L;
+    if (log_pi) log_pi[r] = eps ? acc : 0.0;
+  }
+}
+
 // ------------------------------------------------- standalone Huntington-Hill
 // apportion_batch alone (enforcer.py:118-165): rows are independent, one
 // warp per row, any number of rows.
@@ -405,6 +455,24 @@ __global__ void latency_bench_kernel(int iters, long long* cycles, double* sink)
 }
 
 }  // namespace cyr
+
+int cyr_launch_actions_head(int precision, const void* raw, const int32_t* alloc,
+                            const int32_t* kcol, const double* eps, int R, int E, int L,
+                            double* b, double* caps, int64_t* demand, double* log_pi,
+                            int32_t* status, cudaStream_t stream) {
+  if (R <= 0) return CYR_OK;
+  if (E < 1 || E > cyr::kMaxUsers) return CYR_UNSUPPORTED;
+  const int blocks = (R + 7) / 8;
+  if (precision == CYR_FP64)
+    cyr::actions_head_kernel<double><<<blocks, 256, 0, stream>>>(
+        static_cast<const double*>(raw), alloc, kcol, eps, R, E, L, b, caps, demand, log_pi,
+        status);
+  else
+    cyr::actions_head_kernel<float><<<blocks, 256, 0, stream>>>(
+        static_cast<const float*>(raw), alloc, kcol, eps, R, E, L, b, caps, demand, log_pi,
+        status);
+  return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
+}
 
 int cyr_launch_apportion(const double* m_hat, const double* caps, const int64_t* demand, int R,
                          int E, int64_t* grants, double* margin, int32_t* status,

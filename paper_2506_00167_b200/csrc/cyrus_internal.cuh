@@ -210,6 +210,14 @@ int cyr_launch_tree_level(int precision, const void* raw, const int32_t* alloc, 
                           int16_t* node, int S, int E, int L, int cap, int parents, int epad,
                           long long nodes_per_slot, long long parent_off, long long child_off,
                           int32_t* status, cudaStream_t stream);
+int cyr_launch_actor_columns(int precision, const cyr::ActorDesc& desc, const void* blob,
+                             const int32_t* alloc, const int32_t* kcol, const double* x,
+                             int ncols, int E, int N, int cap, void* raw, int sm_count,
+                             cudaStream_t stream);
+int cyr_launch_actions_head(int precision, const void* raw, const int32_t* alloc,
+                            const int32_t* kcol, const double* eps, int R, int E, int L,
+                            double* b, double* caps, int64_t* demand, double* log_pi,
+                            int32_t* status, cudaStream_t stream);
 size_t cyr_tc_smem_bytes();
 int cyr_launch_actor_tc(const cyr::ActorDesc& desc, const unsigned char* tc_blob,
                         const long long* tc_off, const int* tc_npad, const float* bias_blob,

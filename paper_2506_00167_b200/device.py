@@ -116,6 +116,67 @@ class DevicePolicy:
             pass
 
 
+class DeviceMlp:
+    """Any published ReLU MLP (``cyr_mlp_create``): the SAC critics and
+    target critics (sac.py:114-127, sizes [2E+1, *hidden, 1]) for
+    ``sac.critic_targets``; forward only (neural.py:66-84)."""
+
+    def __init__(self, params, precision: str | None = None):
+        precision = precision or _DEFAULT_PRECISION
+        if precision == "bf16_tc":
+            precision = "fp32"  # the critics run SIMT (not a codebook decision path)
+        if precision not in ("fp32", "fp64"):
+            raise ValueError("precision must be fp32 or fp64")
+        self.precision = precision
+        sizes, blob = flatten_actor(params)
+        self.sizes = list(sizes)
+        h = ctypes.c_void_p()
+        arr = np.asarray(sizes, dtype=np.int32)
+        _native.check(_native.lib().cyr_mlp_create(ctypes.byref(h), arr.ctypes.data, len(sizes),
+                                                   blob.ctypes.data,
+                                                   _native.PRECISIONS[precision]), "mlp create")
+        self._h = h
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise ValueError("mlp is closed")
+        return self._h
+
+    def update(self, params) -> None:
+        sizes, blob = flatten_actor(params)
+        if list(sizes) != self.sizes:
+            raise ValueError("MLP shape differs from the published one")
+        _native.check(_native.lib().cyr_policy_update(self.handle, blob.ctypes.data), "update")
+
+    def forward(self, x, out=None, stream=None):
+        """x: CUDA float64 (cols, in) -> (cols, out) CUDA tensor (fp32/fp64)."""
+        import torch
+        x = x.contiguous()
+        if x.dtype != torch.float64 or x.dim() != 2 or x.shape[1] != self.sizes[0]:
+            raise ValueError("input must be float64 (cols, input_dim)")
+        dt = torch.float64 if self.precision == "fp64" else torch.float32
+        if out is None:
+            out = torch.empty((x.shape[0], self.sizes[-1]), dtype=dt, device=x.device)
+        _native.check(_native.lib().cyr_mlp_forward_device(
+            self.handle, x.data_ptr(), x.shape[0], out.data_ptr(),
+            _native.stream_handle(stream)), "mlp forward")
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None:
+            try:
+                _native.lib().cyr_policy_destroy(self._h)
+            finally:
+                self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class _Published:
     __slots__ = ("policy", "snapshot", "actor_ref")
 
@@ -152,6 +213,25 @@ def policy_for(agent, precision: str | None = None) -> DevicePolicy:
     elif _SYNC_MODE == "check" and not _same(actor, entry.snapshot):
         entry.policy.update(actor)
         entry.snapshot = _snapshot(actor)
+    return entry.policy
+
+
+_PUBLISHED_MLP: dict = {}
+
+
+def mlp_for(params, precision: str | None = None) -> DeviceMlp:
+    """Device copy of any MlpParams (e.g. ``agent.target1``), published on
+    first use and re-published after an in-place change in "check" mode."""
+    precision = precision or _DEFAULT_PRECISION
+    key = (id(params), precision)
+    entry = _PUBLISHED_MLP.get(key)
+    if entry is None or entry.actor_ref() is not params:
+        entry = _Published(params, DeviceMlp(params, precision))
+        _PUBLISHED_MLP[key] = entry
+        weakref.finalize(params, _PUBLISHED_MLP.pop, key, None)
+    elif _SYNC_MODE == "check" and not _same(params, entry.snapshot):
+        entry.policy.update(params)
+        entry.snapshot = _snapshot(params)
     return entry.policy
 
 

@@ -214,12 +214,15 @@ def gather_mode_t_tree(states, cap: int, minislots: int, level: int, group=None)
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     width = max_shard((cap + 1) ** level, world)
     first, count = shard_extent(cap, minislots, level, world, rank)
+    # int16 records travel as bytes (neither NCCL nor gloo has an int16 type)
     local = pack_shard(states, cap, minislots, level, first, count, width).contiguous()
-    blocks = torch.empty((world,) + tuple(local.shape), dtype=local.dtype, device=local.device)
+    raw = local.view(torch.uint8)
+    blocks = torch.empty((world,) + tuple(raw.shape), dtype=torch.uint8, device=local.device)
     if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(blocks, local, group=group)
+        dist.all_gather_into_tensor(blocks, raw, group=group)
     else:
-        dist.all_gather(list(blocks.unbind(0)), local, group=group)
+        dist.all_gather(list(blocks.unbind(0)), raw, group=group)
+    blocks = blocks.view(local.dtype)
     full = states.clone()
     r = cap + 1
     for src in range(world):

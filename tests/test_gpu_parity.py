@@ -445,3 +445,34 @@ def test_mode_t_matches_oracle(golden, name, minislots, precision):
         assert not (diff & ~taint).any(), f"slot {s}: nodes differ outside near-tie subtrees"
         flagged += int(taint.sum())
     print(f"[mode-T] {name} M={minislots} {precision}: {flagged} nodes under near-ties")
+
+
+@pytest.mark.parametrize("name,precision", [("cfg2", "fp32"), ("cfg1", "bf16_tc"), ("cfg2", "fp64")])
+@pytest.mark.parametrize("level,world", [(1, 2), (1, 8), (2, 3), (3, 8)])
+def test_mode_t_subtree_shards_equal_whole_tree(golden, name, precision, level, world):
+    """§8(e): a Mode-T tree built shard by shard (levels <= `level`
+    replicated, deeper levels only under each rank's block of level-`level`
+    nodes) has exactly the whole tree's records — for every kernel path
+    (fp32 SIMT, fp64, bf16 tcgen05) since the shards run the same kernels."""
+    from paper_2506_00167_b200 import substream
+    cfg = golden.config(name)
+    cell = cfg.cell
+    actor = tree.make_mode_t_actor(cell, (256, 256), substream(3, "mode-t"))
+    pol = DevicePolicy(actor, precision)
+    slots = 2
+    alloc, mcs, eps = _mode_t_inputs(cfg, slots)
+    whole = tree.build_tree_mode_t(pol, cell, alloc, mcs, eps)
+    cap, m = cell.num_branches, cell.minislots
+    covered = torch.zeros(whole.shape[1], dtype=torch.bool)
+    covered[:tree.level_offsets(cap, m)[level - 1] + (cap + 1) ** level if level else 0] = True
+    for rank in range(world):
+        first, count = tree.shard_extent(cap, m, level, world, rank)
+        part = torch.full_like(whole, -7)
+        tree.build_tree_mode_t(pol, cell, alloc, mcs, eps, out=part, shard=(level, first, count))
+        top = tree.level_offsets(cap, m)[level - 1] + (cap + 1) ** level
+        assert torch.equal(part[:, :top], whole[:, :top])     # replicated levels
+        for off, n in tree.subtree_ranges(cap, m, level, first, count):
+            assert torch.equal(part[:, off:off + n], whole[:, off:off + n])
+            covered[off:off + n] = True
+    assert covered.all()
+    pol.close()

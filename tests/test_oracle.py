@@ -152,3 +152,25 @@ def test_mode_t_oracle_bridge_equals_mode_r(golden, name, minislots):
                                      cfg.meta["urllc_sc_len"], minislots, eps)
             want = arrival_tree.node_states(cfg[f"{mode}/codebook"][s], minislots)
             assert np.array_equal(got, want)
+
+
+# ------------------------------------------------- SAC critic targets (f1)
+def test_critic_oracle_matches_reference_golden():
+    """oracle.critic restates sac.critic_targets bit for bit (fixtures from
+    the unmodified reference, tests/golden/make_critic_golden.py), including
+    the coupled enforcement of > 256 rows in one call."""
+    from oracle import critic
+    from tests.golden_util import critic_cases
+    cases = critic_cases()
+    assert max(c.meta["rows"] for c in cases) > 1000
+    for case in cases:
+        agent = case.agent()
+        details = {}
+        y = critic.critic_targets((agent.actor.weights, agent.actor.biases),
+                                  (agent.target1.weights, agent.target1.biases),
+                                  (agent.target2.weights, agent.target2.biases),
+                                  case.cell, case.meta["discount"], case.meta["zeta"],
+                                  case.arrays(), case.rng(), details)
+        assert np.array_equal(y, case["y"]), case.name
+        assert np.array_equal(details["grants"], case["grants"]), case.name
+        assert np.array_equal(details["log_pi"], case["log_pi"]), case.name

@@ -66,3 +66,46 @@ def test_two_rank_shard_and_gather(golden, cells):
         assert n_local == span[1] - span[0]
         spans[rank] = span
     assert spans[0][1] == spans[1][0] and spans[1][1] == cells
+
+
+def _tree_worker(rank, world, port, level, queue):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import arrival_tree
+        from paper_2506_00167_b200 import tree
+        from tests.golden_util import Golden
+        cfg = Golden.load().config("cfg1")
+        cap, m = cfg.cell.num_branches, cfg.meta["minislots"]
+        whole = np.stack([arrival_tree.node_states(cfg["sto/codebook"][s], m) for s in range(2)])
+        whole = torch.from_numpy(whole.astype(np.int16))
+        # this rank holds the replicated levels and its own subtrees only
+        mine = torch.full_like(whole, -1)
+        top = tree.level_offsets(cap, m)[level - 1] + (cap + 1) ** level
+        mine[:, :top] = whole[:, :top]
+        first, count = tree.shard_extent(cap, m, level, world, rank)
+        for off, n in tree.subtree_ranges(cap, m, level, first, count):
+            mine[:, off:off + n] = whole[:, off:off + n]
+        full = tree.gather_mode_t_tree(mine, cap, m, level)
+        queue.put((rank, bool(torch.equal(full, whole))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,level", [(2, 1), (3, 2)])
+def test_mode_t_subtree_gather(world, level):
+    """Mode-T subtree shards (tree.shard_extent / subtree_ranges) are
+    assembled on every rank by ONE all-gather (tree.gather_mode_t_tree)."""
+    ctx = mp.get_context("spawn")
+    queue = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tree_worker, args=(r, world, port, level, queue))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [queue.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in results), results
