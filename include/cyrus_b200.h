@@ -183,6 +183,24 @@ int32_t cyr_tree_state_stride(int32_t E);
 int cyr_tree_expand_device(const int32_t* codebook, int32_t S, int32_t E, int32_t cap,
                            int32_t M, int16_t* node_state, void* stream);
 
+/* Leaf scoring fused into K1: the node states as
+ * cyr_tree_expand_device plus, at every leaf (a full arrival pattern of the
+ * slot), the reference's threshold decoder for every user (phy.py:73-80,
+ * decode_user phy.py:196-198):
+ *   ok_e = n_e <= 0  or  cum_e <= margin[s][e] * (M * n_e)
+ * (margin = the decoder's margin, or 1 - code_rate of the user's MCS when
+ * the model's margin is None), the TTI reward r = sum_e (ok_e - 1) n_e / N
+ * (core.py:132-146) and goodput sum_e ok_e n_e (core.py:149-153).
+ * Outputs (NULL to skip): leaf_ok [S][(cap+1)^M] uint32 bitmask of decoding
+ * users (leaf q = the level-M node q, digits = admitted counts per
+ * mini-slot); expect [S][3] float64 = (E[r], E[goodput], E[lost SCs]) with
+ * leaf weight prod_tau prob[tau][k_tau] (prob: [M][cap+1] admitted-count
+ * probabilities per mini-slot).  Requires M * N <= 32767. */
+int cyr_tree_score_device(const int32_t* codebook, const int32_t* alloc, const double* margin,
+                          const double* prob, int32_t S, int32_t E, int32_t cap, int32_t M,
+                          int32_t N, int16_t* node_state, uint32_t* leaf_ok, double* expect,
+                          void* stream);
+
 /* ---- arrival tree, Mode T (north star: actor on every node's state) ------ */
 /* Policy created with sizes[0] = 3E+3 (a Mode-T actor).  Level tau = 1..M:
  * for every parent node q of level tau-1 and branch k = 1..cap the actor

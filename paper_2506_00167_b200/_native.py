@@ -57,6 +57,8 @@ SIGNATURES = {
                                            _vp, _vp, _vp]),
     "cyr_mlp_create": (_c_int, [ctypes.POINTER(_vp), _vp, _c_i32, _vp, _c_i32]),
     "cyr_mlp_forward_device": (_c_int, [_vp, _vp, _c_i32, _vp, _vp]),
+    "cyr_tree_score_device": (_c_int, [_vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32,
+                                       _vp, _vp, _vp, _vp]),
     "cyr_debug_trace": (_c_int, [_pi64, _c_i32]),
     "cyr_selftest_latency": (_c_int, [_c_i32, _c_i32, _pi64]),
     "cyr_selftest_launch": (_c_int, [_c_i32, _c_i32, _pi64]),

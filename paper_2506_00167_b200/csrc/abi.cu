@@ -901,6 +901,20 @@ size_t cyr_tree_mode_t_workspace_bytes(const cyr_policy* p, int32_t S, int32_t c
   return raw + wide_act_bytes(p, (long long)S * widest * cap);
 }
 
+int cyr_tree_score_device(const int32_t* codebook, const int32_t* alloc, const double* margin,
+                          const double* prob, int32_t S, int32_t E, int32_t cap, int32_t M,
+                          int32_t N, int16_t* node_state, uint32_t* leaf_ok, double* expect,
+                          void* stream) {
+  if (S < 0 || E < 1 || cap < 1 || M < 1) return CYR_BAD_ARG;
+  if (S > 0 && (!codebook || !alloc || !margin || !prob || !node_state)) return CYR_BAD_ARG;
+  if (M * N > 32767) return CYR_UNSUPPORTED;  // int16 cumulative punctures
+  const int rc = cyr_launch_tree_score(codebook, alloc, margin, prob, S, E, cap, M, N, node_state,
+                                       leaf_ok, expect, sm_count_of_current_device(),
+                                       static_cast<cudaStream_t>(stream));
+  if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+  return rc;
+}
+
 int cyr_tree_mode_t_device(const cyr_policy* p, const int32_t* alloc, const int32_t* mcs,
                            const double* eps, int32_t S, int32_t N, int32_t L, int32_t M,
                            double mcs_scale, int16_t* node_state, void* workspace,

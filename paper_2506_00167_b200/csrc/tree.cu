@@ -46,13 +46,33 @@ struct TreeParams {
   int level_blocks[kMaxLevels + 1];  // prefix over parent levels t = 0..M-1
   long long level_parents[kMaxLevels];
   long long child_off[kMaxLevels];   // node offset of level t+1 within a slot
+  // leaf scoring, SCORE instantiation only
+  const int32_t* alloc;              // [S][E] allocations n_e
+  const double* margin;              // [S][E] threshold-decoder margins
+  const double* prob;                // [M][R] admitted-count probabilities per mini-slot
+  int N;                             // total SCs (reward denominator)
+  uint32_t* leaf_ok;                 // [S][R^M] decoding-user bitmask, or null
+  double* partial;                   // [S][leaf items][2]: sum w*lost, sum w*goodput
 };
 
 __device__ __forceinline__ uint4 vadd16(uint4 a, uint4 b) {
   return make_uint4(__vadd2(a.x, b.x), __vadd2(a.y, b.y), __vadd2(a.z, b.z), __vadd2(a.w, b.w));
 }
 
-template <int CH, int R>  // CH: 16-byte granules per record; R = cap + 1
+// Leaf epilogue (SCORE): the threshold decoder of every user at every leaf
+// (phy.py:73-80 via decode_user, phy.py:196-198): ok_e = n_e <= 0 or
+// cum_e <= margin_e * (M * n_e).  cum is an integer, so the float64 bound
+// becomes an exact int16 bound (floor), and a packed signed compare
+// (__vcmples2) decides two users per instruction.  lost = sum of n_e over
+// failing users (core.py:132-146: r = -lost / N), goodput = sum n_e - lost.
+// Each leaf's weight is the product over mini-slots of the admitted-count
+// probability of its digit; the CTA reduces sum(w * lost) and
+// sum(w * goodput) deterministically into one partial per work item.
+__device__ __forceinline__ unsigned lane_bits(unsigned m) {  // 0xffff lanes -> 2 bits
+  return (m & 1u) | ((m >> 15) & 2u);
+}
+
+template <int CH, int R, bool SCORE>  // CH: 16-byte granules per record; R = cap + 1
 __global__ void __launch_bounds__(kTreeThreads, 2) tree_kernel(const TreeParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int NP = p.np_item;
@@ -60,6 +80,12 @@ __global__ void __launch_bounds__(kTreeThreads, 2) tree_kernel(const TreeParams 
   const int r3 = p.r3;
   uint4* t3 = reinterpret_cast<uint4*>(smem + 2 * stage_bytes);  // [r3][CH], per item
   int16_t* bookw = reinterpret_cast<int16_t*>(t3 + (size_t)r3 * CH);  // [R][CH*8]
+  // SCORE: per-user int16 bounds and allocations as packed granules, leaf-digit
+  // probabilities, and the CTA reduction scratch
+  int16_t* boundw = bookw + R * CH * 8;                 // [CH*8]
+  int16_t* allocw = boundw + CH * 8;                    // [CH*8]
+  double* probs = reinterpret_cast<double*>(allocw + CH * 8);  // [M][R]
+  double* red = probs + kMaxLevels * R;                 // [kTreeThreads / 32][2]
   const int tid = threadIdx.x;
   const int items = p.S * p.blocks_per_slot;  // host-checked to fit in int
   int it = 0;
@@ -72,6 +98,7 @@ __global__ void __launch_bounds__(kTreeThreads, 2) tree_kernel(const TreeParams 
     while (bw >= p.level_blocks[t + 1]) ++t;
     const int p0 = (bw - p.level_blocks[t]) * NP;
     const int np = (int)min((long long)NP, p.level_parents[t] - p0);
+    double acc_lost = 0.0, acc_good = 0.0;  // SCORE: this thread's weighted leaf sums
 
     if (tid == 0) bulk_wait_read<1>();  // the store issued two items ago released this stage
     // this slot's codebook as packed int16 granules: cooperative load to
@@ -80,6 +107,23 @@ __global__ void __launch_bounds__(kTreeThreads, 2) tree_kernel(const TreeParams 
     for (int idx = tid; idx < R * CH * 8; idx += NP) {
       const int k = idx / (CH * 8), e = idx % (CH * 8);
       bookw[idx] = (int16_t)((e < p.E) ? cb[k * p.E + e] : 0);
+    }
+    if constexpr (SCORE) {
+      if (t == p.M - 1) {
+        for (int e = tid; e < CH * 8; e += NP) {
+          int bound = 32767, n = 0;  // padding lanes: always "ok", no SCs
+          if (e < p.E) {
+            n = p.alloc[(long long)s * p.E + e];
+            if (n > 0) {
+              const double rhs = __dmul_rn(p.margin[(long long)s * p.E + e], (double)(p.M * n));
+              bound = rhs >= 32767.0 ? 32767 : (rhs < 0.0 ? -1 : (int)floor(rhs));
+            }
+          }
+          boundw[e] = (int16_t)bound;
+          allocw[e] = (int16_t)(n > 0 ? n : 0);
+        }
+        for (int idx = tid; idx < p.M * R; idx += NP) probs[idx] = p.prob[idx];
+      }
     }
     __syncthreads();
     uint4 col[R][CH];
@@ -147,8 +191,77 @@ __global__ void __launch_bounds__(kTreeThreads, 2) tree_kernel(const TreeParams 
       for (int k = 0; k < R; ++k)
 #pragma unroll
         for (int c = 0; c < CH; ++c) dst[k * CH + c] = vadd16(cum[c], col[k][c]);
+      if constexpr (SCORE) {
+        if (t == p.M - 1) {  // children are leaves
+          double wq = 1.0;   // parent weight: its M-1 digits, first mini-slot first
+          unsigned x = (unsigned)(p0 + tid), div = 1;
+          for (int d = 1; d < p.M - 1; ++d) div *= (unsigned)R;
+          for (int d = 0; d < p.M - 1; ++d) {
+            const unsigned dig = x / div;
+            x -= dig * div;
+            div /= (unsigned)R;
+            wq = __dmul_rn(wq, probs[d * R + dig]);
+          }
+          const uint4* bw4 = reinterpret_cast<const uint4*>(boundw);
+          const uint4* aw4 = reinterpret_cast<const uint4*>(allocw);
+          unsigned tot = 0;
+#pragma unroll
+          for (int c = 0; c < CH; ++c) {
+            const uint4 a = aw4[c];
+            tot += (a.x & 0xffffu) + (a.x >> 16) + (a.y & 0xffffu) + (a.y >> 16) +
+                   (a.z & 0xffffu) + (a.z >> 16) + (a.w & 0xffffu) + (a.w >> 16);
+          }
+          const long long leaf0 = (long long)s * p.level_parents[p.M - 1] * R +
+                                  (long long)(p0 + tid) * R;
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            unsigned okbits = 0, lost2 = 0;
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+              const uint4 v = dst[k * CH + c], b = bw4[c], a = aw4[c];
+              const unsigned m0 = __vcmples2(v.x, b.x), m1 = __vcmples2(v.y, b.y);
+              const unsigned m2 = __vcmples2(v.z, b.z), m3 = __vcmples2(v.w, b.w);
+              okbits |= (lane_bits(m0) | lane_bits(m1) << 2 | lane_bits(m2) << 4 |
+                         lane_bits(m3) << 6) << (8 * c);
+              lost2 = __vadd2(lost2, __vadd2(__vadd2(~m0 & a.x, ~m1 & a.y),
+                                             __vadd2(~m2 & a.z, ~m3 & a.w)));
+            }
+            const unsigned lost = (lost2 & 0xffffu) + (lost2 >> 16);
+            const double w = __dmul_rn(wq, probs[(p.M - 1) * R + k]);
+            acc_lost = __fma_rn(w, (double)lost, acc_lost);
+            acc_good = __fma_rn(w, (double)(tot - lost), acc_good);
+            if (p.leaf_ok) p.leaf_ok[leaf0 + k] = okbits & (p.E >= 32 ? 0xffffffffu : ((1u << p.E) - 1u));
+          }
+        }
+      }
     }
     fence_proxy_async_smem();  // generic smem writes -> visible to the bulk-copy proxy
+    if constexpr (SCORE) {
+      if (t == p.M - 1) {  // deterministic CTA reduction -> this item's partial
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          acc_lost += __shfl_down_sync(0xffffffffu, acc_lost, off);
+          acc_good += __shfl_down_sync(0xffffffffu, acc_good, off);
+        }
+        if ((tid & 31) == 0) {
+          red[(tid >> 5) * 2] = acc_lost;
+          red[(tid >> 5) * 2 + 1] = acc_good;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          double l = 0.0, g = 0.0;
+          for (int wi = 0; wi < NP / 32; ++wi) {
+            l += red[wi * 2];
+            g += red[wi * 2 + 1];
+          }
+          const long long item = (long long)s * (p.level_blocks[p.M] - p.level_blocks[p.M - 1]) +
+                                 (bw - p.level_blocks[p.M - 1]);
+          p.partial[item * 2] = l;
+          p.partial[item * 2 + 1] = g;
+        }
+        acc_lost = acc_good = 0.0;
+      }
+    }
     __syncthreads();
     if (tid == 0) {
       const long long first = (long long)s * p.nodes_per_slot + p.child_off[t] + (long long)p0 * R;
@@ -159,44 +272,70 @@ __global__ void __launch_bounds__(kTreeThreads, 2) tree_kernel(const TreeParams 
   if (tid == 0) bulk_wait_all();
 }
 
-template <int CH, int R>
+// expected values per slot from the per-item partials, in item order
+__global__ void tree_score_reduce_kernel(const double* __restrict__ partial, int items, int S,
+                                         int N, double* __restrict__ expect) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  double l = 0.0, g = 0.0;
+  for (int i = 0; i < items; ++i) {
+    l += partial[((long long)s * items + i) * 2];
+    g += partial[((long long)s * items + i) * 2 + 1];
+  }
+  expect[s * 3] = -l / (double)N;  // E[r] (core.py:132-146)
+  expect[s * 3 + 1] = g;           // E[goodput SCs] (core.py:149-153)
+  expect[s * 3 + 2] = l;           // E[lost SCs]
+}
+
+template <int CH, int R, bool SCORE>
 int launch_tree_t(const TreeParams& p, int sm_count, cudaStream_t stream) {
-  const size_t smem =
-      2 * (size_t)p.np_item * R * CH * 16 + (size_t)p.r3 * CH * 16 + (size_t)R * CH * 16;
+  const size_t smem = 2 * (size_t)p.np_item * R * CH * 16 + (size_t)p.r3 * CH * 16 +
+                      (size_t)R * CH * 16 +
+                      (SCORE ? 2 * (size_t)CH * 16 + (size_t)kMaxLevels * R * 8 +
+                                   (kTreeThreads / 32) * 16
+                             : 0);
   if (smem > 227 * 1024) return CYR_UNSUPPORTED;
-  if (cudaFuncSetAttribute(tree_kernel<CH, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem) != cudaSuccess)
+  auto kern = tree_kernel<CH, R, SCORE>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
     return CYR_CUDA_ERROR;
   const long long items = (long long)p.S * p.blocks_per_slot;
   const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (227 * 1024) / (smem + 1024)));
   const long long grid = std::min<long long>(items, (long long)sm_count * per_sm);
-  tree_kernel<CH, R><<<(unsigned)grid, p.np_item, smem, stream>>>(p);
+  kern<<<(unsigned)grid, p.np_item, smem, stream>>>(p);
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
 }
 
-template <int CH>
+template <int CH, bool SCORE>
 int launch_tree_r(const TreeParams& p, int sm_count, cudaStream_t stream) {
   switch (p.cap + 1) {
-    case 2: return launch_tree_t<CH, 2>(p, sm_count, stream);
-    case 3: return launch_tree_t<CH, 3>(p, sm_count, stream);
-    case 4: return launch_tree_t<CH, 4>(p, sm_count, stream);
-    case 5: return launch_tree_t<CH, 5>(p, sm_count, stream);
-    case 6: return launch_tree_t<CH, 6>(p, sm_count, stream);
-    case 7: return launch_tree_t<CH, 7>(p, sm_count, stream);
-    case 8: return launch_tree_t<CH, 8>(p, sm_count, stream);
-    case 9: return launch_tree_t<CH, 9>(p, sm_count, stream);
+    case 2: return launch_tree_t<CH, 2, SCORE>(p, sm_count, stream);
+    case 3: return launch_tree_t<CH, 3, SCORE>(p, sm_count, stream);
+    case 4: return launch_tree_t<CH, 4, SCORE>(p, sm_count, stream);
+    case 5: return launch_tree_t<CH, 5, SCORE>(p, sm_count, stream);
+    case 6: return launch_tree_t<CH, 6, SCORE>(p, sm_count, stream);
+    case 7: return launch_tree_t<CH, 7, SCORE>(p, sm_count, stream);
+    case 8: return launch_tree_t<CH, 8, SCORE>(p, sm_count, stream);
+    case 9: return launch_tree_t<CH, 9, SCORE>(p, sm_count, stream);
     default: return CYR_UNSUPPORTED;
   }
 }
 
-}  // namespace cyr
+template <bool SCORE>
+int launch_tree_ch(const TreeParams& p, int sm_count, cudaStream_t stream) {
+  switch (p.epad / 8) {
+    case 1: return launch_tree_r<1, SCORE>(p, sm_count, stream);
+    case 2: return launch_tree_r<2, SCORE>(p, sm_count, stream);
+    case 3: return launch_tree_r<3, SCORE>(p, sm_count, stream);
+    default: return launch_tree_r<4, SCORE>(p, sm_count, stream);
+  }
+}
 
-int cyr_launch_tree(const int32_t* codebook, int S, int E, int cap, int M, int16_t* out,
-                    int sm_count, cudaStream_t stream) {
-  if (S <= 0) return CYR_OK;
-  if (E < 1 || E > cyr::kMaxUsers || cap < 1 || M < 1 || M > 10) return CYR_BAD_ARG;
+// geometry of the level-synchronous work items (shared by both entry points)
+int tree_params(TreeParams& p, const int32_t* codebook, int S, int E, int cap, int M,
+                int16_t* out, int sm_count) {
+  if (E < 1 || E > kMaxUsers || cap < 1 || M < 1 || M > 10) return CYR_BAD_ARG;
   if (cap + 1 > 9) return CYR_UNSUPPORTED;
-  cyr::TreeParams p{};
   p.codebook = codebook;
   p.out = out;
   p.S = S;
@@ -216,7 +355,7 @@ int cyr_launch_tree(const int32_t* codebook, int S, int E, int cap, int M, int16
   // tree spreads over all SMs; large batches use 256-parent items
   long long big_items = 0;
   for (long long t = 0, q = 1; t < M; ++t, q *= R) big_items += (q + 255) / 256;
-  p.np_item = (big_items * S < 2ll * sm_count) ? 64 : cyr::kTreeThreads;
+  p.np_item = (big_items * S < 2ll * sm_count) ? 64 : kTreeThreads;
   long long parents = 1, nodes = 0;
   p.level_blocks[0] = 0;
   for (int t = 0; t < M; ++t) {
@@ -230,10 +369,44 @@ int cyr_launch_tree(const int32_t* codebook, int S, int E, int cap, int M, int16
   p.nodes_per_slot = nodes;
   p.blocks_per_slot = p.level_blocks[M];
   if ((long long)S * p.blocks_per_slot >= (1ll << 31)) return CYR_UNSUPPORTED;
-  switch (p.epad / 8) {
-    case 1: return cyr::launch_tree_r<1>(p, sm_count, stream);
-    case 2: return cyr::launch_tree_r<2>(p, sm_count, stream);
-    case 3: return cyr::launch_tree_r<3>(p, sm_count, stream);
-    default: return cyr::launch_tree_r<4>(p, sm_count, stream);
+  return CYR_OK;
+}
+
+}  // namespace cyr
+
+int cyr_launch_tree(const int32_t* codebook, int S, int E, int cap, int M, int16_t* out,
+                    int sm_count, cudaStream_t stream) {
+  if (S <= 0) return CYR_OK;
+  cyr::TreeParams p{};
+  const int rc = cyr::tree_params(p, codebook, S, E, cap, M, out, sm_count);
+  if (rc != CYR_OK) return rc;
+  return cyr::launch_tree_ch<false>(p, sm_count, stream);
+}
+
+int cyr_launch_tree_score(const int32_t* codebook, const int32_t* alloc, const double* margin,
+                          const double* prob, int S, int E, int cap, int M, int N, int16_t* out,
+                          uint32_t* leaf_ok, double* expect, int sm_count, cudaStream_t stream) {
+  if (S <= 0) return CYR_OK;
+  if (N <= 0 || N > 32767) return CYR_BAD_ARG;
+  cyr::TreeParams p{};
+  int rc = cyr::tree_params(p, codebook, S, E, cap, M, out, sm_count);
+  if (rc != CYR_OK) return rc;
+  p.alloc = alloc;
+  p.margin = margin;
+  p.prob = prob;
+  p.N = N;
+  p.leaf_ok = leaf_ok;
+  const int items = p.level_blocks[M] - p.level_blocks[M - 1];
+  double* partial = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&partial), (size_t)S * items * 2 * sizeof(double),
+                      stream) != cudaSuccess)
+    return CYR_CUDA_ERROR;
+  p.partial = partial;
+  rc = cyr::launch_tree_ch<true>(p, sm_count, stream);
+  if (rc == CYR_OK && expect != nullptr) {
+    cyr::tree_score_reduce_kernel<<<(S + 127) / 128, 128, 0, stream>>>(partial, items, S, N, expect);
+    if (cudaPeekAtLastError() != cudaSuccess) rc = CYR_CUDA_ERROR;
   }
+  cudaFreeAsync(partial, stream);
+  return rc;
 }

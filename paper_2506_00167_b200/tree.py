@@ -233,3 +233,67 @@ def gather_mode_t_tree(states, cap: int, minislots: int, level: int, group=None)
             full[:, off:off + n] = blocks[src][:, pos:pos + n]
             pos += width * r ** (tau - level)
     return full
+
+
+# ------------------------------------------------------------ leaf scoring
+# every leaf of the arrival tree is one full
+# admitted-count pattern of the slot; the reference's TTI step decodes each
+# user from its punctured total (threshold model, phy.py:73-80 via
+# decode_user, phy.py:196-198) and scores the TTI (core.py:132-153).  K1
+# evaluates that at every leaf while the leaf's state is in registers.
+
+# code rates of scheduler.DEFAULT_MCS_TABLE (scheduler.py:31-38)
+MCS_CODE_RATES = (1 / 3, 1 / 2, 1 / 2, 3 / 4, 2 / 3, 3 / 4)
+
+
+def threshold_margins(mcs, margin=None, code_rates=MCS_CODE_RATES) -> np.ndarray:
+    """Per-user puncture budget fraction of DecodabilityModel("threshold"):
+    ``margin`` when given, else 1 - code_rate of the user's MCS (phy.py:197)."""
+    mcs = np.asarray(mcs, dtype=np.int64)
+    if margin is not None:
+        if not 0.0 < float(margin) <= 1.0:
+            raise ValueError("margin must lie in (0, 1]")
+        return np.full(mcs.shape, float(margin))
+    return 1.0 - np.asarray(code_rates, dtype=np.float64)[mcs]
+
+
+def admitted_count_probs(cell, num_urllc: int = 12, per_ue_prob: float = 0.08) -> np.ndarray:
+    """[M][cap+1] probability of k admitted packets per mini-slot for the
+    reference's Bernoulli arrivals (traffic.py:46-52; TrafficConfig
+    defaults) capped at cap with an empty carry-in queue."""
+    from math import comb
+    cap, m = cell.num_branches, cell.minislots
+    pk = [comb(num_urllc, j) * per_ue_prob ** j * (1.0 - per_ue_prob) ** (num_urllc - j)
+          for j in range(num_urllc + 1)]
+    row = pk[:cap] + [sum(pk[cap:])] if num_urllc >= cap else pk + [0.0] * (cap - num_urllc)
+    return np.tile(np.asarray(row[:cap + 1], dtype=np.float64), (m, 1))
+
+
+def score_tree(codebooks, cell, allocs, margins, prob, out=None, leaf_ok: bool = True,
+               stream=None):
+    """K1 with the fused leaf epilogue.
+
+    codebooks: CUDA int32 (S, cap+1, E); allocs: CUDA int32 (S, E); margins:
+    CUDA float64 (S, E); prob: CUDA float64 (M, cap+1).  Returns (node
+    states (S, nodes, Epad) int16, leaf_ok (S, (cap+1)^M) int32 bitmask of
+    decoding users or None, expect (S, 3) float64 = E[reward], E[goodput],
+    E[lost SCs]).
+    """
+    import torch
+    check_tree_geometry(cell)
+    s, cols, e = codebooks.shape
+    cap, m = cols - 1, cell.minislots
+    dev = codebooks.device
+    if out is None:
+        out = torch.empty((s, num_nodes(cap, m), state_stride(e)), dtype=torch.int16, device=dev)
+    ok = torch.empty((s, (cap + 1) ** m), dtype=torch.int32, device=dev) if leaf_ok else None
+    expect = torch.empty((s, 3), dtype=torch.float64, device=dev)
+    prob = prob.contiguous()
+    if tuple(prob.shape) != (m, cap + 1):
+        raise ValueError("prob must be (M, cap+1)")
+    _native.check(_native.lib().cyr_tree_score_device(
+        codebooks.contiguous().data_ptr(), allocs.contiguous().data_ptr(),
+        margins.contiguous().data_ptr(), prob.data_ptr(), s, e, cap, m, cell.total_scs,
+        out.data_ptr(), None if ok is None else ok.data_ptr(), expect.data_ptr(),
+        _native.stream_handle(stream)), "score tree")
+    return out, ok, expect

@@ -476,3 +476,33 @@ def test_mode_t_subtree_shards_equal_whole_tree(golden, name, precision, level, 
             covered[off:off + n] = True
     assert covered.all()
     pol.close()
+
+
+# ------------------------------------------------------- leaf scoring (f2)
+@pytest.mark.parametrize("name,margin", [("cfg1", None), ("cfg1", 0.1), ("cfg2", None),
+                                         ("desk", None), ("paper", 0.05), ("cfg5", None)])
+def test_tree_leaf_scoring_matches_oracle(golden, name, margin):
+    """K1's fused leaf epilogue: node states unchanged, per-leaf decode
+    bitmask exact, expectations within 1e-12 relative (fp64 sums in another
+    order) of the oracle's (the oracle is pinned to the reference's
+    decode_user / compute_reward by tests/golden/leaf_golden.npz)."""
+    from oracle import leaf_score
+    cfg = golden.config(name)
+    slots = 4 if name != "cfg5" else 1
+    books = cfg["sto/codebook"][:slots]
+    m, n = cfg.meta["minislots"], cfg.meta["total_scs"]
+    margins = np.stack([tree.threshold_margins(cfg["mcs"][s], margin) for s in range(slots)])
+    prob = tree.admitted_count_probs(cfg.cell)
+    bd = torch.from_numpy(books).cuda()
+    states, ok, expect = tree.score_tree(bd, cfg.cell, torch.from_numpy(cfg["alloc"][:slots]).cuda(),
+                                         torch.from_numpy(margins).cuda(),
+                                         torch.from_numpy(prob).cuda())
+    plain = tree.expand_tree(bd, cfg.cell)
+    assert torch.equal(states, plain)
+    ok, expect = ok.cpu().numpy(), expect.cpu().numpy()
+    for s in range(slots):
+        bits, _, er, eg, el = leaf_score.score_leaves(books[s], cfg["alloc"][s], margins[s], prob,
+                                                      m, n)
+        assert np.array_equal(ok[s].astype(np.int64) & ((1 << cfg.meta["num_embb"]) - 1), bits)
+        for got, want in ((expect[s, 0], er), (expect[s, 1], eg), (expect[s, 2], el)):
+            assert abs(got - want) <= 1e-12 * max(1.0, abs(want)), (s, got, want)

@@ -174,3 +174,38 @@ def test_critic_oracle_matches_reference_golden():
         assert np.array_equal(y, case["y"]), case.name
         assert np.array_equal(details["grants"], case["grants"]), case.name
         assert np.array_equal(details["log_pi"], case["log_pi"]), case.name
+
+
+# ------------------------------------------------- leaf scoring (f2)
+def test_leaf_score_oracle_matches_reference_golden(golden):
+    """oracle.leaf_score restates the reference's threshold decode + reward
+    for every leaf (fixtures: tests/golden/make_leaf_golden.py)."""
+    import json
+    import os
+    from oracle import leaf_score
+    from paper_2506_00167_b200 import tree
+    path = os.path.join(os.path.dirname(__file__), "golden", "leaf_golden.npz")
+    z = np.load(path)
+    info = json.loads(str(z["meta_json"]))
+    for key, case in info.items():
+        cfg = golden.config(case["config"])
+        s = case["slot"]
+        book = cfg["sto/codebook"][s]
+        margin = tree.threshold_margins(cfg["mcs"][s], case["margin"])
+        prob = tree.admitted_count_probs(cfg.cell)
+        bits, reward, er, eg, el = leaf_score.score_leaves(book, cfg["alloc"][s], margin, prob,
+                                                           cfg.meta["minislots"],
+                                                           cfg.meta["total_scs"])
+        assert np.array_equal(bits, z[f"{key}/bits"]), key
+        assert np.array_equal(reward, z[f"{key}/reward"]), key
+        good = z[f"{key}/goodput"]
+        assert abs(eg - float(np.sum(_leaf_weights(prob) * good))) <= 1e-9 * max(1.0, abs(eg))
+        assert abs(prob.sum(axis=1) - 1.0).max() < 1e-12
+        assert er <= 0.0 and el >= 0.0
+
+
+def _leaf_weights(prob):
+    w = np.ones(1)
+    for row in prob:
+        w = (w[:, None] * row[None, :]).ravel()
+    return w
