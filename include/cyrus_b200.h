@@ -172,6 +172,18 @@ int cyr_mlp_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
 int cyr_mlp_forward_device(const cyr_policy* mlp, const double* x, int32_t cols, void* out,
                            void* stream);
 
+/* ---- batched PF scheduler (the producer of s(t)) -------- */
+/* scheduler.pf_schedule (scheduler.py:79-106) for C cells at once: every
+ * one of num_rbs RBs goes to argmax_e rate_e / max((1-beta)*avg_e +
+ * beta*granted_e, 1e-6) (first maximum on ties), then avg <- the same blend
+ * (the PfState EWMA commit).  avg_tput [C][E] float64 in/out (PfState
+ * .avg_tput), inst_rate [C][E] float64 (>= 0; status CYR_BAD_ARG
+ * otherwise), alloc [C][E] int32 out (SCs, multiples of rb_size).  Bit
+ * identical to the reference. */
+int cyr_pf_schedule_device(double* avg_tput, const double* inst_rate, int32_t C, int32_t E,
+                           double beta, int32_t num_rbs, int32_t rb_size, int32_t* alloc,
+                           int32_t* status, void* stream);
+
 /* ---- arrival tree, Mode R (K1) ------------------------------------------- */
 /* Node count excluding the root: sum_{t=1..M} (cap+1)^t. */
 int64_t cyr_tree_num_nodes(int32_t cap, int32_t M);

@@ -21,6 +21,8 @@ Modules:
   mlp          — actor forward + tanh-Gaussian head (neural.py:25-84, 144-183;
                  sac.py:334-355)
   slot         — one slot's codebook (engine.py:97-116), batched over slots
+  pf           — proportional-fair scheduler (scheduler.py:79-106; §8(f) f4)
+  leaf_score   — threshold decode + reward at every tree leaf (§8(f) f2)
   critic       — SAC critic targets (sac.py:167-214)
   arrival_tree — Mode-R arrival tree node states (no
                  reference counterpart: composition of engine.py:230 lookups)

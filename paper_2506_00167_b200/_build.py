@@ -22,7 +22,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build", "cyrus_b200")
 LIB = os.path.join(PKG, "libcyrus_b200.so")
-SOURCES = ("abi.cu", "actor.cu", "actor_tc.cu", "codebook.cu", "tree.cu")
+SOURCES = ("abi.cu", "actor.cu", "actor_tc.cu", "codebook.cu", "tree.cu", "scheduler.cu")
 HEADERS = ("cyrus_internal.cuh", "projection.cuh", "projection_lane.cuh")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

@@ -901,6 +901,19 @@ size_t cyr_tree_mode_t_workspace_bytes(const cyr_policy* p, int32_t S, int32_t c
   return raw + wide_act_bytes(p, (long long)S * widest * cap);
 }
 
+int cyr_pf_schedule_device(double* avg_tput, const double* inst_rate, int32_t C, int32_t E,
+                           double beta, int32_t num_rbs, int32_t rb_size, int32_t* alloc,
+                           int32_t* status, void* stream) {
+  if (C < 0 || E < 1 || num_rbs < 0 || rb_size < 1 || !(beta >= 0.0 && beta <= 1.0))
+    return CYR_BAD_ARG;
+  if (C > 0 && (!avg_tput || !inst_rate || !alloc || !status)) return CYR_BAD_ARG;
+  if ((long long)num_rbs * rb_size > (1ll << 30)) return CYR_BAD_ARG;
+  const int rc = cyr_launch_pf_schedule(avg_tput, inst_rate, C, E, beta, num_rbs, rb_size, alloc,
+                                        status, static_cast<cudaStream_t>(stream));
+  if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+  return rc;
+}
+
 int cyr_tree_score_device(const int32_t* codebook, const int32_t* alloc, const double* margin,
                           const double* prob, int32_t S, int32_t E, int32_t cap, int32_t M,
                           int32_t N, int16_t* node_state, uint32_t* leaf_ok, double* expect,

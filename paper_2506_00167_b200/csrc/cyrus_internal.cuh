@@ -200,6 +200,9 @@ int cyr_launch_tree(const int32_t* codebook, int S, int E, int cap, int M, int16
 int cyr_launch_tree_score(const int32_t* codebook, const int32_t* alloc, const double* margin,
                           const double* prob, int S, int E, int cap, int M, int N, int16_t* out,
                           uint32_t* leaf_ok, double* expect, int sm_count, cudaStream_t stream);
+int cyr_launch_pf_schedule(double* avg_tput, const double* rate, int C, int E, double beta,
+                           int num_rbs, int rb_size, int32_t* alloc, int32_t* status,
+                           cudaStream_t stream);
 unsigned long long* cyr_trace_buffer();  // device alias of the trace block or null
 int cyr_launch_latency_bench(int which, int iters, long long* cycles, double* sink);
 int cyr_launch_empty(int cluster, cudaStream_t stream);

@@ -209,3 +209,19 @@ def _leaf_weights(prob):
     for row in prob:
         w = (w[:, None] * row[None, :]).ravel()
     return w
+
+
+# ------------------------------------------------- PF scheduler (f4)
+def test_pf_oracle_matches_reference_golden():
+    """oracle.pf restates scheduler.pf_schedule bit for bit over consecutive
+    TTIs (fixtures: tests/golden/make_pf_golden.py)."""
+    import os
+    from oracle import pf
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "pf_golden.npz"))
+    for e in (4, 10, 16):
+        rates, beta, alloc, avg = (z[f"e{e}/{k}"] for k in ("rates", "beta", "alloc", "avg"))
+        for c in range(rates.shape[1]):
+            state = avg[0, c]
+            for t in range(rates.shape[0]):
+                a, state = pf.pf_schedule(state, rates[t, c], float(beta[c]), 65, 12)
+                assert np.array_equal(a, alloc[t, c]) and np.array_equal(state, avg[t + 1, c])
