@@ -452,10 +452,19 @@ int launch_actor_cluster(const ActorLaunch& p, int G, cudaStream_t stream,
 // consumer warps release a stage by arriving on its "empty" mbarrier, so no
 // CTA barrier sits inside the K loop.  Activations stay in shared memory;
 // biases are read into registers before each panel's K loop.
-constexpr int kTileThreads = 256;   // consumer threads
-constexpr int kTileProducer = 32;   // + one producer warp
+constexpr int kTileProducer = 32;   // one producer warp after the consumer warps
+
+// CYR_TILED16=0 disables the 12-warp in-place variant (A/B)
+inline bool cyr_tiled16_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CYR_TILED16");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
 constexpr int kTileStageBytes = 16 * 1024;
 constexpr int kTileStages = 4;
+constexpr int kTileStagesInplace = 6;  // the in-place variant has the shared memory for more
 
 __host__ __device__ inline int tile_rows(const LayerDesc& L, int elem) {
   const int r = kTileStageBytes / (L.pw * elem);
@@ -492,28 +501,37 @@ __device__ __forceinline__ void ld_vec(const T* src, T (&dst)[N]) {
   }
 }
 
-__device__ __forceinline__ void consumer_sync() {  // the 256 consumer threads only
-  asm volatile("bar.sync 1, 256;" ::: "memory");
+template <int NT>
+__device__ __forceinline__ void consumer_sync() {  // the NT consumer threads only
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
 }
 
-template <typename T, int TC>
-__global__ void __launch_bounds__(kTileThreads + kTileProducer, 1)
+// NW consumer warps (8: TC = 8 * CPT columns; 16: 4 warps per scheduler for
+// latency hiding, TC = 16 * CPT).  INPLACE (every layer one panel): ONE
+// activation buffer, each layer's epilogue overwriting its inputs after a
+// consumer barrier — half the activation shared memory, so a CTA holds
+// twice the columns (half the L2 weight traffic per column).
+template <typename T, int TC, int NW = 8, bool INPLACE = false>
+__global__ void __launch_bounds__(NW * 32 + kTileProducer, 1)
     actor_tiled_kernel(const ActorLaunch p) {
   extern __shared__ __align__(128) unsigned char smem[];
-  constexpr int CPT = TC / 8;
+  constexpr int kTileThreads = NW * 32;
+  constexpr int ST = INPLACE ? kTileStagesInplace : kTileStages;  // ring depth
+  constexpr int CPT = TC / NW;
+  static_assert(CPT * NW == TC && CPT >= 1, "");
   constexpr int TCP = TC + 16 / (int)sizeof(T);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + kTileStages;
+  uint64_t* empty = full + ST;
   unsigned char* ring = smem + 128;
-  T* act_a = reinterpret_cast<T*>(ring + (size_t)kTileStages * kTileStageBytes);
-  T* act_b = act_a + (size_t)p.desc.max_width * TCP;
+  T* act_a = reinterpret_cast<T*>(ring + (size_t)ST * kTileStageBytes);
+  T* act_b = INPLACE ? act_a : act_a + (size_t)p.desc.max_width * TCP;
   const int tid = threadIdx.x;
   const int c0 = blockIdx.x * TC;
   const T* blob = static_cast<const T*>(p.blob);
   const int nl = p.desc.n_layers;
 
   if (tid == 0) {
-    for (int st = 0; st < kTileStages; ++st) {
+    for (int st = 0; st < ST; ++st) {
       mbar_init(&full[st], 1);
       mbar_init(&empty[st], kTileThreads / 32);
     }
@@ -530,8 +548,8 @@ __global__ void __launch_bounds__(kTileThreads + kTileProducer, 1)
         const int npan = tile_panels(L);
         for (int panel = 0; panel < npan; ++panel)
           for (int i0 = 0; i0 < L.in; i0 += r, ++g) {
-            const int buf = g % kTileStages;
-            if (g >= kTileStages) mbar_wait(&empty[buf], (uint32_t)((g / kTileStages - 1) & 1));
+            const int buf = g % ST;
+            if (g >= ST) mbar_wait(&empty[buf], (uint32_t)((g / ST - 1) & 1));
             const uint32_t bytes = (uint32_t)min(r, L.in - i0) * L.pw * sizeof(T);
             mbar_expect_tx(&full[buf], bytes);
             bulk_g2s(ring + (size_t)buf * kTileStageBytes,
@@ -561,7 +579,7 @@ __global__ void __launch_bounds__(kTileThreads + kTileProducer, 1)
     }
     act_a[i * TCP + c] = (T)v;
   }
-  consumer_sync();
+  consumer_sync<kTileThreads>();
 
   T* cur = act_a;
   T* nxt = act_b;
@@ -596,8 +614,8 @@ __global__ void __launch_bounds__(kTileThreads + kTileProducer, 1)
         bias[a] = (active && o < L.out) ? blob[L.b_off + o] : T(0);
       }
       for (int i0 = 0; i0 < L.in; i0 += rows, ++g) {
-        const int buf = g % kTileStages;
-        mbar_wait(&full[buf], (uint32_t)((g / kTileStages) & 1));
+        const int buf = g % ST;
+        mbar_wait(&full[buf], (uint32_t)((g / ST) & 1));
         const T* W = reinterpret_cast<const T*>(ring + (size_t)buf * kTileStageBytes);
         const int nr = min(rows, L.in - i0);
         if (active && !narrow) {
@@ -635,6 +653,7 @@ __global__ void __launch_bounds__(kTileThreads + kTileProducer, 1)
         __syncwarp();
         if ((tid & 31) == 0) mbar_arrive(&empty[buf]);  // this warp is done with the stage
       }
+      if constexpr (INPLACE) consumer_sync<kTileThreads>();  // every warp has read cur
       if (active) {
         const int ncol = narrow ? kNc : CPT;
 #pragma unroll
@@ -655,20 +674,20 @@ __global__ void __launch_bounds__(kTileThreads + kTileProducer, 1)
         }
       }
     }
-    consumer_sync();
+    consumer_sync<kTileThreads>();
     T* t = cur;
     cur = nxt;
     nxt = t;
   }
 }
 
-template <typename T, int TC>
+template <typename T, int TC, int NW = 8, bool INPLACE = false>
 int launch_actor_tiled(const ActorLaunch& p, cudaStream_t stream) {
   constexpr int TCP = TC + 16 / (int)sizeof(T);
-  const size_t smem = 128 + (size_t)kTileStages * kTileStageBytes +
-                      2ull * p.desc.max_width * TCP * sizeof(T);
+  const size_t smem = 128 + (size_t)(INPLACE ? kTileStagesInplace : kTileStages) * kTileStageBytes +
+                      (INPLACE ? 1ull : 2ull) * p.desc.max_width * TCP * sizeof(T);
   if (smem > (size_t)kSmemLimit) return CYR_UNSUPPORTED;
-  auto kern = actor_tiled_kernel<T, TC>;
+  auto kern = actor_tiled_kernel<T, TC, NW, INPLACE>;
   static int configured = -1;
   if ((int)smem > configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
@@ -677,8 +696,15 @@ int launch_actor_tiled(const ActorLaunch& p, cudaStream_t stream) {
     configured = (int)smem;
   }
   const int blocks = (p.ncols + TC - 1) / TC;
-  kern<<<blocks, kTileThreads + kTileProducer, smem, stream>>>(p);
+  kern<<<blocks, NW * 32 + kTileProducer, smem, stream>>>(p);
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
+}
+
+// every layer a single panel (<= 256 outputs): the in-place variant applies
+inline bool single_panel(const ActorDesc& d) {
+  for (int l = 0; l < d.n_layers; ++l)
+    if (d.layer[l].out_pad > d.layer[l].pw) return false;
+  return true;
 }
 
 // largest tile that fits shared memory and still gives every SM a CTA
@@ -689,6 +715,14 @@ int launch_actor_tiled_auto(const ActorLaunch& p, int sm_count, cudaStream_t str
     return 128 + (size_t)kTileStages * kTileStageBytes +
                2ull * p.desc.max_width * tcp * sizeof(T) <= (size_t)kSmemLimit;
   };
+  // big fp32 batches of a single-panel actor (cfg2 Mode-T levels): 12
+  // consumer warps x 8 columns (3 per scheduler; 16 would cap registers at
+  // 96 and spill), one in-place activation buffer
+  if (sizeof(T) == 4 && single_panel(p.desc) && cyr_tiled16_enabled() &&
+      (long long)p.ncols >= 96ll * sm_count) {
+    const int rc = launch_actor_tiled<T, 96, 12, true>(p, stream);
+    if (rc != CYR_UNSUPPORTED) return rc;
+  }
   constexpr int kMax = sizeof(T) == 4 ? 64 : 32;
   int tc = 8;
   for (int cand = kMax; cand >= 8; cand >>= 1) {
