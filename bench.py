@@ -320,6 +320,12 @@ def run_ours(args, rank, world, local_rank):
         # ---- single-slot latency through the drop-in build_codebook
         lat = latency_run(agent, cell, allocs, args.latency_slots)
         mode_t = mode_t_all(cell) if (rank == 0 and not args.no_mode_t) else None
+        sharded = None
+        if not args.no_mode_t:
+            try:
+                sharded = mode_t_sharded(world, rank, dev)
+            except Exception as exc:  # reported, never fatal for the headline
+                sharded = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     mean_ms = float(np.mean(step_ms))
     mean_e2e = float(np.mean(e2e))
@@ -362,6 +368,7 @@ def run_ours(args, rank, world, local_rank):
                         "D2H of the codebooks (node states stay in HBM)"},
         "latency_us": lat,
         "mode_t": mode_t,
+        "mode_t_sharded": sharded,
         "roofline": roofline,
         "cpu_baseline": None if cores_rate is None else {
             "value": cores_rate, "unit": UNIT, "cores": cores, "kind": "port",
@@ -412,6 +419,60 @@ def mode_t_run(cell, hidden, slots, reps=3, fp32_reps=None):
                 "nodes_per_tree": int(same.shape[1]), "actor_columns_per_tree": cols,
                 "node_agreement_bf16_vs_fp32": float(same.mean())})
     return out
+
+
+def mode_t_sharded(world, rank, dev, reps=3):
+    """One BASELINE configs[4] Mode-T tree (cfg5: E=16, cap 6, 3x1024 actor,
+    bf16 tcgen05) split across the ranks by subtrees of level 3 (343
+    subtrees; levels <= 3 replicated) and assembled on every rank by ONE
+    all-gather over NCCL.  Times are CUDA events, max over
+    ranks.  At N > 1 rank 0 also builds the whole tree alone and checks the
+    assembled one against it."""
+    import torch
+    import torch.distributed as dist
+    from paper_2506_00167_b200 import CellConfig, DevicePolicy, substream, tree
+    cell = CellConfig(780, 16, 130)
+    cap, m = cell.num_branches, cell.minislots
+    actor = tree.make_mode_t_actor(cell, (1024, 1024, 1024), substream(0, "mode-t"))
+    allocs, eps = synthetic_inputs(cell, 1, seed=11)
+    mcs = np.random.default_rng(11).integers(0, 6, size=allocs.shape).astype(np.int32)
+    al, mc, ep = (torch.from_numpy(x).to(dev) for x in (allocs, mcs, eps))
+    level = 3 if world > 1 else 0
+    first, count = tree.shard_extent(cap, m, level, world, rank)
+    pol = DevicePolicy(actor, "bf16_tc")
+    out = tree.build_tree_mode_t(pol, cell, al, mc, ep, shard=(level, first, count))
+    full = tree.gather_mode_t_tree(out, cap, m, level) if world > 1 else out
+    torch.cuda.synchronize()
+    build, gather = [], []
+    stream = torch.cuda.current_stream()
+    for _ in range(reps):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e[0].record(stream)
+        tree.build_tree_mode_t(pol, cell, al, mc, ep, out=out, shard=(level, first, count))
+        e[1].record(stream)
+        if world > 1:
+            full = tree.gather_mode_t_tree(out, cap, m, level)
+        e[2].record(stream)
+        torch.cuda.synchronize()
+        build.append(e[0].elapsed_time(e[1]))
+        gather.append(e[1].elapsed_time(e[2]))
+    t = torch.tensor([np.mean(build), np.mean(gather), np.mean(build) + np.mean(gather)],
+                     dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    res = {"cell": {"N": 780, "E": 16, "L": 130, "cap": cap, "M": m}, "actor": "1024x1024x1024",
+           "precision": "bf16_tc", "shard_level": level, "subtrees": (cap + 1) ** level,
+           "ranks": world, "ms_build_max": float(t[0]), "ms_gather_max": float(t[1]),
+           "ms_per_tree": float(t[2]), "trees_per_s": 1e3 / float(t[2]),
+           "gathered_bytes": int(full.numel() * full.element_size())}
+    if world > 1 and rank == 0:
+        whole = tree.build_tree_mode_t(pol, cell, al, mc, ep)
+        res["matches_whole_tree"] = bool(torch.equal(whole, full))
+    pol.close()
+    return res
 
 
 def mode_t_all(cell):
