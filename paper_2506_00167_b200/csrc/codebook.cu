@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(256, 4) codebook_kernel(
 // Batch K3, one lane per row (projection_lane.cuh): each warp holds
 // 32 / cap whole slots; 4 warps per CTA, no CTA barrier.
 constexpr int kLaneWarps = 4;
+constexpr int kLaneMinBlocks = 6;  // <= 85 registers: 24 warps per SM (issue-latency bound)
 
 template <typename RawT>
 __global__ void __launch_bounds__(32 * kLaneWarps) codebook_lane_kernel(
@@ -103,7 +104,7 @@ struct TreeIO {
 // K3 of one Mode-T level, one lane per row: each warp holds 32 / cap
 // parents (one coupled call of cap rows each).
 template <typename RawT>
-__global__ void __launch_bounds__(32 * kLaneWarps) tree_level_kernel(const RawT* __restrict__ raw,
+__global__ void __launch_bounds__(32 * kLaneWarps, kLaneMinBlocks) tree_level_kernel(const RawT* __restrict__ raw,
                                                                   TreeIO io, long long groups,
                                                                   int L,
                                                                   int32_t* __restrict__ status) {

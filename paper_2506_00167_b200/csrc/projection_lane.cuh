@@ -12,9 +12,10 @@
 // trip.  Same float64 operations in the same order as projection.cuh (and
 // the reference: enforcer.py:49-165, neural.py:144-183), hence the same bits.
 //
-// Per-warp shared memory: b / m_hat as [E][32] doubles (column = lane, so
-// lanes access consecutive words) and the Huntington-Hill seat counts as
-// [E][32] ints.
+// Per-warp shared memory, every array [E][32] (column = lane, so lanes
+// access consecutive words): b / m_hat and the caps as doubles (the caps are
+// read in every fill evaluation: one conversion per row instead of a global
+// load + conversion per use) and the Huntington-Hill seat counts as ints.
 #pragma once
 
 #include "projection.cuh"
@@ -47,13 +48,13 @@ __device__ __forceinline__ double np_sum_lane(int n, F term) {
 // from the allocation row (int32, shared by the call's rows), demand d.
 struct LaneRow {
   double* bT;        // this lane's column of the warp's [E][32] array
-  const int32_t* n;  // allocation row (caps)
+  const double* cT;  // caps (allocation row as doubles), same layout
   int E;
   double d;
   bool bis, degen;
   double lo, hi;
   __device__ __forceinline__ double b(int e) const { return bT[e * 32]; }
-  __device__ __forceinline__ double c(int e) const { return (double)__ldg(n + e); }
+  __device__ __forceinline__ double c(int e) const { return cT[e * 32]; }
   __device__ __forceinline__ bool pos(int e) const { return b(e) > kMassFloor && c(e) > 0.0; }
 };
 
@@ -162,12 +163,12 @@ __device__ __forceinline__ double kl_finish_lane(LaneRow& r) {
   return 0.0;
 }
 
-// Huntington-Hill seats for m = mT[e * 32], caps c; seats into hT[e * 32]
+// Huntington-Hill seats for m = mT[e * 32], caps cT; seats into hT[e * 32]
 // (hh_row of projection.cuh, one lane).  Returns the near-tie margin.
-__device__ __forceinline__ double hh_lane(const double* mT, const int32_t* n, int E, long long want,
+__device__ __forceinline__ double hh_lane(const double* mT, const double* cT, int E, long long want,
                                           int* hT) {
   auto m = [&](int e) { return mT[e * 32]; };
-  auto cnt = [&](int e) { return (int)ceil((double)__ldg(n + e)); };
+  auto cnt = [&](int e) { return (int)ceil(cT[e * 32]); };
   auto posu = [&](int e) { return m(e) > 0.0 && cnt(e) >= 1; };
   double margin = CUDART_INF;
   for (int e = 0; e < E; ++e) hT[e * 32] = 0;
@@ -276,9 +277,10 @@ __device__ __forceinline__ double hh_lane(const double* mT, const int32_t* n, in
   return margin;
 }
 
-// Per-warp scratch for up to 32 rows of E users.
+// Per-warp scratch for up to 32 rows of E users: bT, cT (double) and hT
+// (int), each [E][32].
 __host__ __device__ constexpr size_t lane_scratch_bytes(int E) {
-  return (size_t)E * 32 * (sizeof(double) + sizeof(int));
+  return (size_t)E * 32 * (2 * sizeof(double) + sizeof(int));
 }
 
 // Rows row0 .. row0 + nrows of this warp (whole calls of `cap` rows, lane
@@ -288,15 +290,21 @@ template <typename RawT, typename IO>
 __device__ void codebook_rows_lane(const RawT* raw, long long row0, int nrows, int cap, int E, int L,
                                    const IO& io, int32_t* status, unsigned char* scratch) {
   const int lane = threadIdx.x & 31;
+  const size_t plane = (size_t)E * 32;  // elements of one [E][32] array
   double* bT = reinterpret_cast<double*>(scratch) + lane;
-  int* hT = reinterpret_cast<int*>(scratch + (size_t)E * 32 * sizeof(double)) + lane;
+  double* cT = bT + plane;
+  int* hT = reinterpret_cast<int*>(scratch + 2 * plane * sizeof(double)) + lane;
   const bool live = lane < nrows;
   const long long grow = row0 + (live ? lane : 0);
   const long long group = grow / cap;
   const int j = (int)(grow % cap) + 1;
   LaneRow r;
   r.bT = bT;
-  r.n = io.alloc_row(group);
+  r.cT = cT;
+  if (live) {
+    const int32_t* n = io.alloc_row(group);
+    for (int e = 0; e < E; ++e) cT[e * 32] = (double)__ldg(n + e);
+  }
   r.E = E;
   r.d = (double)((long long)j * L);
   r.bis = r.degen = false;
@@ -326,7 +334,7 @@ __device__ void codebook_rows_lane(const RawT* raw, long long row0, int nrows, i
   r.hi = hi[0];
   if (live) {
     const double nu = kl_finish_lane(r);
-    const double margin = hh_lane(bT, r.n, E, (long long)j * L, hT);
+    const double margin = hh_lane(bT, cT, E, (long long)j * L, hT);
     io.emit_lane(grow, group, j, hT, E, bT, nu, margin, iters);
   }
 }
