@@ -104,16 +104,17 @@ __device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 
 // K tile t of the layer-1 A operand for batch column `col`, written as row
 // `row` of the SW128 image `a` (zeros past in0).  Feature i of the actor
-// input, rounded to bf16 from the float64 value (double)x / (double)scale:
+// input, rounded to bf16 from the fp32 value x * (1 / scale) (this path is
+// bf16 end to end; fp32 feature math keeps the builders off the fp64
+// division sequences):
 //   Mode R: [n/N (E), j/cap]
 //   Mode T: [n/N (E), k/cap, cum/N (E), mcs/mcs_scale (E), arrivals/(M*cap),
 //            (tau-1)/M]
 // The column's indices are decoded once and the per-user loads are issued in
 // independent batches of four, so their latencies overlap.
-__device__ __forceinline__ void tc_put(unsigned char* a, int row, int t, int i, double x) {
+__device__ __forceinline__ void tc_put(unsigned char* a, int row, int t, int i, float x) {
   if (i >= t * 64 && i < t * 64 + 64)
-    *reinterpret_cast<__nv_bfloat16*>(a + sw128_offset(row, i - t * 64)) =
-        __float2bfloat16_rn((float)x);
+    *reinterpret_cast<__nv_bfloat16*>(a + sw128_offset(row, i - t * 64)) = __float2bfloat16_rn(x);
 }
 
 __device__ __forceinline__ void tc_feature_tile(const TcLaunch& p, int col, int t,
@@ -133,7 +134,7 @@ __device__ __forceinline__ void tc_feature_tile(const TcLaunch& p, int col, int 
       (p.mode_t && p.parent_off >= 0)
           ? p.node + ((long long)s * p.nodes_per_slot + p.parent_off + q) * p.epad
           : nullptr;
-  const double inv_n = (double)p.N;
+  const float inv_n = 1.0f / (float)p.N, inv_mcs = (float)(1.0 / p.mcs_scale);
   for (int e0 = 0; e0 < E; e0 += 4) {
     int av[4], mv[4], nv[4];
 #pragma unroll
@@ -147,23 +148,23 @@ __device__ __forceinline__ void tc_feature_tile(const TcLaunch& p, int col, int 
     for (int j = 0; j < 4; ++j) {
       const int e = e0 + j;
       if (e < E) {
-        tc_put(a, row, t, e, (double)av[j] / inv_n);
+        tc_put(a, row, t, e, (float)av[j] * inv_n);
         if (p.mode_t) {
-          tc_put(a, row, t, E + 1 + e, (double)nv[j] / inv_n);
-          tc_put(a, row, t, 2 * E + 1 + e, (double)mv[j] / p.mcs_scale);
+          tc_put(a, row, t, E + 1 + e, (float)nv[j] * inv_n);
+          tc_put(a, row, t, 2 * E + 1 + e, (float)mv[j] * inv_mcs);
         }
       }
     }
   }
-  tc_put(a, row, t, E, (double)k / (double)p.cap);
+  tc_put(a, row, t, E, (float)k / (float)p.cap);
   if (p.mode_t) {
     int arrivals = 0, x = p.parent_base + q;
     for (int d = 1; d < p.tau; ++d) {
       arrivals += x % (p.cap + 1);
       x /= (p.cap + 1);
     }
-    tc_put(a, row, t, 3 * E + 1, (double)arrivals / (double)(p.M * p.cap));
-    tc_put(a, row, t, 3 * E + 2, (double)(p.tau - 1) / (double)p.M);
+    tc_put(a, row, t, 3 * E + 1, (float)arrivals / (float)(p.M * p.cap));
+    tc_put(a, row, t, 3 * E + 2, (float)(p.tau - 1) / (float)p.M);
   }
 }
 
@@ -311,14 +312,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) actor_tc_kernel(const TcLaunch 
 // ------------------------------------------------------------- wide layers
 // Actors wider than one MMA tile (cfg5: 3 x 1024) run layer by layer, each
 // layer a persistent warp-specialised tcgen05 GEMM:
-//   warp 4  producer: TMA bulk copies of {A tile 16 KB, B tile <= 32 KB}
+//   warp 8  producer: TMA bulk copies of {A tile 16 KB, B tile <= 32 KB}
 //           K-tile stages into a ring (FIRST: streams only B);
-//   warps 6-9 (FIRST only) feature builders: thread = row of the block's
+//   warps 10-13 (FIRST only) feature builders: thread = row of the block's
 //           feature A tile, double-buffered across column blocks;
-//   warp 5  MMA issuer (one lane): D[128 x 256] per (column block, n tile)
+//   warp 9  MMA issuer (one lane): D[128 x 256] per (column block, n tile)
 //           into one of two TMEM accumulators (2 x 256 columns);
-//   warps 0-3 epilogue: tcgen05.ld, bias (+ReLU), bf16, into a 16 KB
-//           staging image, TMA bulk store (LAST: fp32 logits raw[col][2E]).
+//   warps 0-3 (FIRST: 0-7) epilogue, one (two) groups of 4 warps (warp w
+//           reads TMEM lane quarter w % 4), group g taking its share of the
+//           accumulator columns: tcgen05.ld, bias (+ReLU), bf16, into the
+//           group's two 16 KB staging images, TMA bulk store (LAST: fp32
+//           logits raw[col][2E]).  The K = 64 first layer gets two groups:
+//           it is epilogue-bound (4 MMAs per n tile against 4 images of
+//           stores); deeper layers keep the shared memory for the ring.
 // Each CTA walks column blocks with a grid stride and every n tile of a block
 // back to back, so the block's A tiles are L2-hot for tiles 2..4 and the
 // epilogue of one tile overlaps the MMAs of the next.  With fewer blocks
@@ -326,8 +332,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) actor_tc_kernel(const TcLaunch 
 // `split` CTAs instead, so a small level is not one SM streaming all weights.  Activations
 // live in HBM as the SW128 K-major images the MMA reads: [col block][k tile]
 // [128 x 64] bf16, written by the previous layer's epilogue.
-constexpr int kWideThreads = 192;       // + 128 feature builders for the first layer
-constexpr int kWideFirstThreads = 320;
+constexpr int kWideThreads = 320;       // + 128 feature builders for the first layer
+constexpr int kWideFirstThreads = 448;
 constexpr int kWideImage = kTcM * 128;  // one [128 x 64] bf16 image, 16 KB
 constexpr int kWideMaxSlots = 8;
 
@@ -345,8 +351,8 @@ struct TcWideLaunch {
   unsigned char* act_out;       // [ncb][ceil(out/64)][16 KB]
 };
 
-__device__ __forceinline__ void epi_sync() {  // the 128 epilogue threads only
-  asm volatile("bar.sync 1, 128;" ::: "memory");
+__device__ __forceinline__ void epi_sync(int grp) {  // the 128 threads of one epilogue group
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
 }
 
 template <bool FIRST, bool LAST>
@@ -356,8 +362,9 @@ __global__ void __launch_bounds__(kWideFirstThreads, 1) actor_tc_wide_kernel(con
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   unsigned char* ring = base;
   unsigned char* feat = ring + (size_t)q.nslots * q.slot_bytes;  // FIRST: 2 x 16 KB
-  unsigned char* stg = feat + (FIRST ? 2 * kWideImage : 0);      // !LAST: 2 x 16 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stg + (LAST ? 0 : 2 * kWideImage));
+  constexpr int EG = FIRST ? 2 : 1;  // epilogue groups of 4 warps
+  unsigned char* stg = feat + (FIRST ? 2 * kWideImage : 0);      // !LAST: EG x 2 x 16 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg + (LAST ? 0 : EG * 2 * kWideImage));
   uint64_t* full = bars;
   uint64_t* freeb = full + kWideMaxSlots;
   uint64_t* tfull = freeb + kWideMaxSlots;
@@ -382,7 +389,7 @@ __global__ void __launch_bounds__(kWideFirstThreads, 1) actor_tc_wide_kernel(con
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], 4 * EG);
       mbar_init(&ffull[i], 4);
       mbar_init(&ffree[i], 1);
     }
@@ -398,7 +405,7 @@ __global__ void __launch_bounds__(kWideFirstThreads, 1) actor_tc_wide_kernel(con
   const int cb0 = blockIdx.x / q.split, cbs = gridDim.x / q.split;
   const int nt0 = sp * q.nts / q.split, nt1 = (sp + 1) * q.nts / q.split;
 
-  if (warp == 4) {
+  if (warp == 8) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       long long st = 0;
@@ -421,10 +428,10 @@ __global__ void __launch_bounds__(kWideFirstThreads, 1) actor_tc_wide_kernel(con
       }
     }
     __syncwarp();
-  } else if (warp >= 6) {
+  } else if (warp >= 10) {
     // ---------------------------------------- feature builders (first layer)
     if (FIRST) {
-      const int row = tid - 192;
+      const int row = tid - 320;
       int i = 0;
       for (int cb = cb0; cb < q.ncb; cb += cbs, ++i) {
         const int fb = i & 1;
@@ -435,7 +442,7 @@ __global__ void __launch_bounds__(kWideFirstThreads, 1) actor_tc_wide_kernel(con
         if (lane == 0) mbar_arrive(&ffull[fb]);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     // ---------------------------------------------------------- MMA issuer
     if (lane == 0) {
       long long st = 0;
@@ -475,21 +482,24 @@ __global__ void __launch_bounds__(kWideFirstThreads, 1) actor_tc_wide_kernel(con
       }
     }
     __syncwarp();
-  } else if (warp < 4) {
+  } else if (warp < 4 * EG) {
     // ------------------------------------------------------------ epilogue
     const float* bias = p.bias + p.desc.layer[q.l].b_off;
     const int kt_next = (q.out + 63) / 64;
+    const int grp = warp >> 2, wq = warp & 3;  // group; TMEM lane quarter
+    const int row = tid & 127;                 // = TMEM lane = column within the block
+    const bool leader = row == 0;
     int a = 0, img = 0;
     for (int cb = cb0; cb < q.ncb; cb += cbs) {
-      const int col = cb * kTcM + tid;
+      const int col = cb * kTcM + row;
       for (int nt = nt0; nt < nt1; ++nt, ++a) {
         const int acc = a & 1, u = a >> 1;
         mbar_wait(&tfull[acc], (uint32_t)(u & 1));
         tc_fence_after();
         const int rows_n = nt == q.nts - 1 ? last_nt_rows : 256;
-        for (int n0 = 0; n0 < rows_n; n0 += 64) {
+        for (int n0 = grp * (256 / EG); n0 < min(rows_n, (grp + 1) * (256 / EG)); n0 += 64) {
           uint32_t r[64];
-          const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * 256 + n0);
+          const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(acc * 256 + n0);
           tc_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
           tc_ld32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
           const int o0 = nt * 256 + n0;
@@ -501,9 +511,9 @@ __global__ void __launch_bounds__(kWideFirstThreads, 1) actor_tc_wide_kernel(con
             }
           } else {
             const int sb = img & 1;
-            if (tid == 0) bulk_wait_read<1>();  // the store that last used stg[sb] has read it
-            epi_sync();
-            unsigned char* sp = stg + sb * kWideImage;
+            if (leader) bulk_wait_read<1>();  // the store that last used this image has read it
+            epi_sync(grp);
+            unsigned char* sp = stg + (grp * 2 + sb) * kWideImage;
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
               uint32_t w[4];
@@ -517,12 +527,12 @@ __global__ void __launch_bounds__(kWideFirstThreads, 1) actor_tc_wide_kernel(con
                 const __nv_bfloat162 pr = __floats2bfloat162_rn(v0, v1);
                 w[h] = *reinterpret_cast<const uint32_t*>(&pr);
               }
-              *reinterpret_cast<uint4*>(sp + sw128_offset(tid, c * 8)) =
+              *reinterpret_cast<uint4*>(sp + sw128_offset(row, c * 8)) =
                   make_uint4(w[0], w[1], w[2], w[3]);
             }
             fence_proxy_async_smem();
-            epi_sync();
-            if (tid == 0) {
+            epi_sync(grp);
+            if (leader) {
               bulk_s2g(q.act_out + ((long long)cb * kt_next + (o0 >> 6)) * kWideImage, sp,
                        kWideImage);
               bulk_commit();
@@ -535,7 +545,7 @@ __global__ void __launch_bounds__(kWideFirstThreads, 1) actor_tc_wide_kernel(con
         if (lane == 0) mbar_arrive(&tempty[acc]);
       }
     }
-    if (!LAST && tid == 0) bulk_wait_all();
+    if (!LAST && leader) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -653,7 +663,8 @@ int cyr_launch_actor_tc_layer(const cyr::ActorDesc& desc, const unsigned char* t
   const int b_rows = std::min(256, npad);
   q.slot_bytes = (uint32_t)((q.a_bytes + b_rows * 128 + 1023) / 1024 * 1024);
   const size_t fixed = 1024 + (first ? 2 * cyr::kWideImage : 0) +
-                       (last ? 0 : 2 * cyr::kWideImage) + (4 * cyr::kWideMaxSlots + 16) * 8 + 16;
+                       (last ? 0 : (first ? 4 : 2) * cyr::kWideImage) +
+                       (4 * cyr::kWideMaxSlots + 16) * 8 + 16;
   static int max_smem = 0, sms = 0;
   if (!max_smem) {
     int dev = 0;

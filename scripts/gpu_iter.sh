@@ -1,13 +1,10 @@
 # Quick GPU iteration: parity tests, Mode-T probes, launch lists.
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
-tail -5 gpurun_out/pytest_gpu.log
+tail -5 gpurun_out/pytest_gpu.log; cat gpurun_out/bf16_agreement.json
 P="python scripts/mode_t_probe.py --reps 3"
-timeout 300 $P --cfg cfg2 --slots 8 --precision fp32
+timeout 300 $P --cfg cfg2 --slots 8 --precision bf16_tc
 timeout 300 $P --cfg cfg5 --slots 1 --precision bf16_tc
-for c in "cfg2 8 fp32" "cfg5 1 bf16_tc"; do
-  set -- $c
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-    --log-file gpurun_out/launches_it_$1.csv python scripts/mode_t_probe.py --reps 1 --cfg $1 --slots $2 --precision $3 > /dev/null 2>&1
-  python scripts/launch_table.py gpurun_out/launches_it_$1.csv | grep -E "tree_level|total"
-done
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/launches_it_cfg5.csv python scripts/mode_t_probe.py --reps 1 --cfg cfg5 --slots 1 --precision bf16_tc > /dev/null 2>&1
+python scripts/launch_table.py gpurun_out/launches_it_cfg5.csv | tail -12
