@@ -311,6 +311,23 @@ int launch_actor_policy(const cyr_policy* p, const int32_t* alloc, int S, int N,
                                static_cast<const float*>(p->blob_d), alloc, S, p->E, N, cap,
                                static_cast<float*>(raw), 0, nullptr, nullptr, 0, 0, 0, 0, 0, 0,
                                1.0, st);
+  if (cyr_gemm_path_applies(simt_precision(p), p->desc, (long long)S * cap)) {
+    const size_t need = cyr_gemm_workspace_bytes(p->desc, (long long)S * cap);
+    if (need > p->wide_act_bytes) {  // grown outside any capture (it synchronises)
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(st, &cs);
+      if (cs == cudaStreamCaptureStatusNone) {
+        cudaFree(p->wide_act_d);
+        p->wide_act_d = nullptr;
+        p->wide_act_bytes = 0;
+        if (cudaMalloc(&p->wide_act_d, need) != cudaSuccess) return CYR_CUDA_ERROR;
+        p->wide_act_bytes = need;
+      }
+    }
+    if (need <= p->wide_act_bytes)
+      return cyr_launch_actor_rowcols(simt_precision(p), p->desc, p->blob_d, alloc, S, p->E, N,
+                                      cap, raw, p->wide_act_d, st);
+  }
   return cyr_launch_actor(simt_precision(p), p->desc, p->blob_d, alloc, S, p->E, N, cap, raw,
                           p->sm_count, st);
 }
@@ -898,7 +915,11 @@ size_t cyr_tree_mode_t_workspace_bytes(const cyr_policy* p, int32_t S, int32_t c
   long long widest = 1;
   for (int t = 1; t < M; ++t) widest *= (cap + 1);  // parents of the deepest level
   const size_t raw = ((size_t)S * widest * cap * 2 * p->E * p->elem + 255) / 256 * 256;
-  return raw + wide_act_bytes(p, (long long)S * widest * cap);
+  const long long cols = (long long)S * widest * cap;
+  size_t act = wide_act_bytes(p, cols);
+  if (!p->tc_wide && cyr_gemm_path_applies(simt_precision(p), p->desc, cols))
+    act = std::max(act, cyr_gemm_workspace_bytes(p->desc, cols));
+  return raw + act;
 }
 
 int cyr_pf_schedule_device(double* avg_tput, const double* inst_rate, int32_t C, int32_t E,
@@ -985,10 +1006,15 @@ int cyr_tree_mode_t_shard_device(const cyr_policy* p, const int32_t* alloc, cons
                                static_cast<const float*>(p->blob_d), alloc, S, p->E, N, cap,
                                static_cast<float*>(workspace), 1, mcs, node_state, M, tau,
                                (int)parents, nodes, par_off, epad, mcs_scale, st, (int)base);
-    else
+    else {
+      long long widest = 1;
+      for (int t = 1; t < M; ++t) widest *= R;
+      void* gemm_ws = static_cast<unsigned char*>(workspace) +
+                      ((size_t)S * widest * cap * 2 * p->E * p->elem + 255) / 256 * 256;
       rc = cyr_launch_actor_mode_t(simt_precision(p), p->desc, p->blob_d, alloc, mcs, node_state,
                                    S, p->E, N, cap, M, tau, (int)parents, nodes, par_off, epad,
-                                   mcs_scale, workspace, p->sm_count, st, (int)base);
+                                   mcs_scale, workspace, p->sm_count, st, (int)base, gemm_ws);
+    }
     if (rc != CYR_OK) break;
     // K3: one coupled enforcement per parent; writes the children's states
     const long long level_tau_off = prev_off < 0 ? 0 : prev_off + level_size;

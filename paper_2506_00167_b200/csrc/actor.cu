@@ -26,9 +26,11 @@
 // loads (lanes split the input dimension), reduces the partial dot products
 // with warp shuffles, and broadcasts the activations to every CTA of the
 // cluster through distributed shared memory; one cluster barrier per layer.
-#include "projection.cuh"
+#include "actor_common.cuh"
 
 #include <cooperative_groups.h>
+
+int cyr_launch_actor_gemm(const cyr::ActorLaunch& p, void* workspace, cudaStream_t stream);
 #include <cstdlib>
 
 namespace cyr {
@@ -37,65 +39,6 @@ constexpr int kActorThreads = 256;
 constexpr int kMaxStages = 4;
 constexpr int kStageBytes = 32 * 1024;
 constexpr int kSmemLimit = 227 * 1024;
-
-struct ActorLaunch {
-  ActorDesc desc;
-  const void* blob;
-  const int32_t* alloc;
-  void* raw;
-  int S, E, N, cap, ncols;
-  int stages;
-  // fused single-slot path (K2 -> K3 in one cluster launch)
-  const double* eps;
-  int L;
-  int32_t* cb;       // device codebook [S][cap+1][E]
-  int32_t* cb_host;  // optional mapped-host copy of the codebook
-  int32_t* status;
-  unsigned long long* trace;  // CYR_TRACE phase stamps (rank 0), or null
-  int inline_inputs;          // alloc / eps come from the SlotInline parameter
-  // Mode T (actor on arrival-tree node states), batch kernel only
-  int mode_t;
-  const int16_t* node;        // node states [S][nodes][epad]
-  const int32_t* mcs;         // [S][E]
-  long long nodes_per_slot;
-  long long parent_off;       // node offset of the first parent of this launch, -1 for the root
-  int parents, tau, M, epad;
-  int parent_base;            // level index of the first parent (subtree shards; digits -> arrivals)
-  double mcs_scale;
-  // column inputs (tiled kernel only): kcol -> column c is [alloc[c]/N, kcol[c]/cap]
-  // (sac.critic_targets, sac.py:190-192); x -> explicit float64 features [c][in]
-  const int32_t* kcol;
-  const double* x;
-};
-
-// Mode-T actor input for column (slot s, parent q, branch k) — feature i of
-// [n/N (E), k/cap, cum/N (E), mcs/mcs_scale (E), arrivals/(M*cap), (tau-1)/M].
-// With zero weights on the last 2E+2 inputs this is exactly the Mode-R
-// column [n/N, k/cap] (sac.py:344-346): the zero-pad bridge.
-__device__ __forceinline__ double mode_t_feature(const ActorLaunch& p, int col, int i) {
-  const int k = col % p.cap + 1;
-  const int g = col / p.cap;
-  const int s = g / p.parents;
-  const int q = g - s * p.parents;
-  const int E = p.E;
-  if (i < E) return (double)p.alloc[(long long)s * E + i] / (double)p.N;
-  if (i == E) return (double)k / (double)p.cap;
-  if (i <= 2 * E) {
-    if (p.parent_off < 0) return 0.0;
-    const long long rec = (long long)s * p.nodes_per_slot + p.parent_off + q;
-    return (double)p.node[rec * p.epad + (i - E - 1)] / (double)p.N;
-  }
-  if (i <= 3 * E) return (double)p.mcs[(long long)s * E + (i - 2 * E - 1)] / p.mcs_scale;
-  if (i == 3 * E + 1) {
-    int arrivals = 0, x = p.parent_base + q;
-    for (int d = 1; d < p.tau; ++d) {
-      arrivals += x % (p.cap + 1);
-      x /= (p.cap + 1);
-    }
-    return (double)arrivals / (double)(p.M * p.cap);
-  }
-  return (double)(p.tau - 1) / (double)p.M;
-}
 
 __host__ __device__ inline int rows_per_stage(const LayerDesc& L, int elem) {
   const int r = kStageBytes / (L.out_pad * elem);
@@ -564,20 +507,7 @@ __global__ void __launch_bounds__(NW * 32 + kTileProducer, 1)
   const int in0 = p.desc.layer[0].in;
   for (int idx = tid; idx < in0 * TC; idx += kTileThreads) {
     const int i = idx / TC, c = idx % TC, col = c0 + c;
-    double v = 0.0;
-    if (col < p.ncols) {
-      if (p.x) {
-        v = p.x[(long long)col * in0 + i];
-      } else if (p.mode_t) {
-        v = mode_t_feature(p, col, i);
-      } else {
-        const int s = p.kcol ? col : col / p.cap;
-        const int j = p.kcol ? p.kcol[col] : col % p.cap + 1;
-        v = (i < p.E) ? (double)p.alloc[(long long)s * p.E + i] / (double)p.N
-                      : (double)j / (double)p.cap;
-      }
-    }
-    act_a[i * TCP + c] = (T)v;
+    act_a[i * TCP + c] = (T)(col < p.ncols ? column_feature(p, col, i) : 0.0);
   }
   consumer_sync<kTileThreads>();
 
@@ -860,6 +790,24 @@ int cyr_launch_actor_columns(int precision, const cyr::ActorDesc& desc, const vo
   return cyr::launch_actor_tiled_auto<float>(p, sm_count, stream);
 }
 
+// Mode-R batch through the layer-GEMM path (wide fp32 actors, big batches)
+int cyr_launch_actor_rowcols(int precision, const cyr::ActorDesc& desc, const void* blob,
+                             const int32_t* alloc, int S, int E, int N, int cap, void* raw,
+                             void* gemm_workspace, cudaStream_t stream) {
+  cyr::ActorLaunch p{};
+  p.desc = desc;
+  p.blob = blob;
+  p.alloc = alloc;
+  p.raw = raw;
+  p.S = S;
+  p.E = E;
+  p.N = N;
+  p.cap = cap;
+  p.ncols = S * cap;
+  (void)precision;
+  return cyr_launch_actor_gemm(p, gemm_workspace, stream);
+}
+
 int cyr_cluster_size() {
   const char* env = getenv("CYR_ACTOR_CLUSTER");
   const int G = env ? atoi(env) : 8;
@@ -930,7 +878,7 @@ int cyr_launch_actor_mode_t(int precision, const cyr::ActorDesc& desc, const voi
                             int S, int E, int N, int cap, int M, int tau, int parents,
                             long long nodes_per_slot, long long parent_off, int epad,
                             double mcs_scale, void* raw, int sm_count, cudaStream_t stream,
-                            int parent_base) {
+                            int parent_base, void* gemm_workspace) {
   if (S <= 0) return CYR_OK;
   if (desc.max_width > cyr::kMaxWidth) return CYR_UNSUPPORTED;
   cyr::ActorLaunch p{};
@@ -956,6 +904,8 @@ int cyr_launch_actor_mode_t(int precision, const cyr::ActorDesc& desc, const voi
   p.M = M;
   p.epad = epad;
   p.mcs_scale = mcs_scale;
+  if (gemm_workspace && cyr_gemm_path_applies(precision, desc, ncols))
+    return cyr_launch_actor_gemm(p, gemm_workspace, stream);
   if (cyr_use_tiled()) {
     if (precision == CYR_FP64) return cyr::launch_actor_tiled_auto<double>(p, sm_count, stream);
     return cyr::launch_actor_tiled_auto<float>(p, sm_count, stream);

@@ -211,7 +211,13 @@ int cyr_launch_actor_mode_t(int precision, const cyr::ActorDesc& desc, const voi
                             int S, int E, int N, int cap, int M, int tau, int parents,
                             long long nodes_per_slot, long long parent_off, int epad,
                             double mcs_scale, void* raw, int sm_count, cudaStream_t stream,
-                            int parent_base = 0);
+                            int parent_base = 0, void* gemm_workspace = nullptr);
+// layer-GEMM path for wide fp32 actors (actor_gemm.cu)
+bool cyr_gemm_path_applies(int precision, const cyr::ActorDesc& desc, long long ncols);
+size_t cyr_gemm_workspace_bytes(const cyr::ActorDesc& desc, long long ncols);
+int cyr_launch_actor_rowcols(int precision, const cyr::ActorDesc& desc, const void* blob,
+                             const int32_t* alloc, int S, int E, int N, int cap, void* raw,
+                             void* gemm_workspace, cudaStream_t stream);
 int cyr_launch_tree_level(int precision, const void* raw, const int32_t* alloc, const double* eps,
                           int16_t* node, int S, int E, int L, int cap, int parents, int epad,
                           long long nodes_per_slot, long long parent_off, long long child_off,

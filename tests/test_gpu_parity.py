@@ -185,6 +185,34 @@ def test_actor_logits_within_tolerance(golden, name, precision):
     assert worst <= LOGIT_TOL[precision]
 
 
+def test_wide_fp32_gemm_path_bit_identical_to_fused_kernel(golden):
+    """A wide fp32 actor (cfg5, 3x1024) takes the layer-GEMM path from 2,048
+    columns on; below it the fused tiled kernel.  Both evaluate each output
+    as the same fp32 FMA chain, so the logits of shared columns are
+    bit-identical (and within the fp32 tolerance of the reference)."""
+    from paper_2506_00167_b200 import _native
+    cfg = golden.config("cfg5")
+    agent = cfg.agent()
+    pol = DevicePolicy(agent.actor, "fp32")
+    cap, e = cfg.meta["cap"], cfg.meta["num_embb"]
+    base = cfg["alloc"]
+    small, big = 2046 // cap, 4096 // cap + 1          # 341 slots (tiled), 683 (GEMM)
+    alloc = np.concatenate([base] * (big // len(base) + 1))[:big]
+    alloc_d = torch.from_numpy(np.ascontiguousarray(alloc)).cuda()
+    out = {}
+    for s in (small, big):
+        raw = torch.empty((s * cap, 2 * e), dtype=torch.float32, device="cuda")
+        _native.check(_native.lib().cyr_actor_forward_device(
+            pol.handle, alloc_d.data_ptr(), s, cfg.meta["total_scs"], cap, raw.data_ptr(),
+            _native.stream_handle()))
+        out[s] = raw.cpu().numpy()
+    assert np.array_equal(out[small], out[big][: small * cap])
+    got = out[big][: len(base) * cap].astype(np.float64).reshape(len(base), cap, 2 * e)
+    want = np.transpose(cfg["det/raw"], (0, 2, 1))
+    assert float((np.abs(got - want) / np.abs(want).max(axis=2, keepdims=True)).max()) <= 1e-5
+    pol.close()
+
+
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 @pytest.mark.parametrize("name", CONFIGS)
 @pytest.mark.parametrize("mode", ["det", "sto"])
@@ -421,15 +449,19 @@ def _taint(margins, cap, threshold):
     return np.concatenate(out)
 
 
-@pytest.mark.parametrize("name,minislots,precision", [("desk", 3, "fp64"), ("cfg1", 5, "fp64"),
-                                                      ("cfg1", 5, "fp32"), ("cfg2", 3, "fp32")])
-def test_mode_t_matches_oracle(golden, name, minislots, precision):
+@pytest.mark.parametrize("name,minislots,precision,hidden",
+                         [("desk", 3, "fp64", (64, 64)), ("cfg1", 5, "fp64", (64, 64)),
+                          ("cfg1", 5, "fp32", (64, 64)), ("cfg2", 3, "fp32", (64, 64)),
+                          # 3x1024 at M=4: the deepest level (2,058 columns) takes the
+                          # layer-GEMM path of wide fp32 actors (actor_gemm.cu)
+                          ("cfg5", 4, "fp32", (1024, 1024, 1024))])
+def test_mode_t_matches_oracle(golden, name, minislots, precision, hidden):
     from dataclasses import replace
     from oracle import mode_t
     from paper_2506_00167_b200 import substream
     cfg = golden.config(name)
     cell = replace(cfg.cell, minislots=minislots)
-    actor = tree.make_mode_t_actor(cell, (64, 64), substream(11, "mode-t"), final_scale=1.0)
+    actor = tree.make_mode_t_actor(cell, hidden, substream(11, "mode-t"), final_scale=1.0)
     pol = DevicePolicy(actor, precision)
     slots = 3
     alloc, mcs, eps = _mode_t_inputs(cfg, slots)
