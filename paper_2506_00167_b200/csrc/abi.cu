@@ -95,6 +95,7 @@ struct cyr_policy {
   // wider actors (cfg5): per-layer GEMM kernels over HBM activation images,
   // weight images [n tile of 256][k tile][256 x 128 B]
   bool tc_wide = false;
+  bool tc_layers = false;            // layer-by-layer kernels usable (wide, or narrow big levels)
   int tc_act_k = 0;                  // widest hidden width rounded to 64
   mutable unsigned char* wide_act_d = nullptr;  // Mode-R activation scratch (grown on demand)
   mutable size_t wide_act_bytes = 0;
@@ -176,8 +177,12 @@ void pack_tc(const cyr_policy& p, const double* src, std::vector<uint8_t>& dst) 
       for (int k = 0; k < L.in; ++k) {
         const int t = k / 64, kk = k % 64;
         const int chunk = (kk * 2) >> 4;
-        const int nt = p.tc_wide ? n / 256 : 0, r = p.tc_wide ? n % 256 : n;
-        const size_t tile = p.tc_wide ? ((size_t)nt * kt + t) * (256 * 128) : t * tile_bytes;
+        // layers of one n tile (npad <= 256): k tiles of npad rows back to back
+        // (the narrow kernel's layout, also read by the wide kernel);
+        // wider layers: [n tile of 256][k tile][256 rows]
+        const bool multi = p.tc_npad[l] > 256;
+        const int nt = multi ? n / 256 : 0, r = multi ? n % 256 : n;
+        const size_t tile = multi ? ((size_t)nt * kt + t) * (256 * 128) : t * tile_bytes;
         const size_t byte = (size_t)p.tc_off[l] + tile + (size_t)(r >> 3) * 1024 + (r & 7) * 128 +
                             ((chunk ^ (r & 7)) << 4) + ((kk * 2) & 15);
         const uint16_t v = f32_to_bf16_rne((float)src[off + (size_t)n * L.in + k]);
@@ -261,12 +266,15 @@ int ensure_host_path(cyr_policy* p, int S, int cap) {
 }
 
 constexpr long long kTcMinCols = 1024;  // below: the MLP is not a dense GEMM
+// narrow bf16 actors: from here on layer-by-layer GEMMs (overlapped
+// epilogues, HBM activations) beat the one-CTA-runs-all-layers kernel
+constexpr long long kTcLayerCols = 32768;
 
 int simt_precision(const cyr_policy* p) { return p->precision == CYR_FP64 ? CYR_FP64 : CYR_FP32; }
 
 // activation ping-pong bytes of the wide tensor-core actor for `cols` columns
 size_t wide_act_bytes(const cyr_policy* p, long long cols) {
-  if (!p->tc_wide) return 0;
+  if (!p->tc_layers) return 0;
   return 2 * (size_t)((cols + 127) / 128) * 128 * p->tc_act_k * 2;
 }
 
@@ -290,7 +298,9 @@ int launch_actor_wide(const cyr_policy* p, const int32_t* alloc, int S, int N, i
 // Mode-R actor for S slots with the policy's precision choice
 int launch_actor_policy(const cyr_policy* p, const int32_t* alloc, int S, int N, int cap, void* raw,
                         cudaStream_t st) {
-  if (p->tc_wide) {  // any width: the SIMT path streams MBs of weights per launch
+  if (p->tc_wide || (p->tc_layers && (long long)S * cap >= kTcLayerCols)) {
+    // wide: any batch (the SIMT path streams MBs of weights per launch);
+    // narrow: big batches
     const long long cols = (long long)S * cap;
     const size_t need = wide_act_bytes(p, cols);
     if (need > p->wide_act_bytes) {  // grown outside any capture (it synchronises)
@@ -451,10 +461,14 @@ int policy_create_impl(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
       for (int l = 0; l < n_sizes - 1; ++l) {
         const cyr::LayerDesc& L = p->desc.layer[l];
         p->tc_off[l] = (long long)tb;
-        tb += (size_t)((p->tc_npad[l] + 255) / 256) * ((L.in + 63) / 64) * 256 * 128;
-        if (l < n_sizes - 2) p->tc_act_k = std::max(p->tc_act_k, (L.out + 63) / 64 * 64);
+        const int rows = p->tc_npad[l] > 256 ? 256 : p->tc_npad[l];
+        tb += (size_t)((p->tc_npad[l] + 255) / 256) * ((L.in + 63) / 64) * rows * 128;
       }
     }
+    // the layer-by-layer kernels also serve narrow actors' big levels
+    p->tc_layers = p->tc_wide || (p->tc_ok && n_sizes >= 3 && p->desc.layer[0].in <= 64);
+    for (int l = 0; l < n_sizes - 2; ++l)
+      p->tc_act_k = std::max(p->tc_act_k, (p->desc.layer[l].out + 63) / 64 * 64);
     p->tc_bytes = tb;
     if (p->tc_ok || p->tc_wide) {
       cudaError_t e2 = cudaMalloc(&p->tc_blob_d, tb);
@@ -917,7 +931,7 @@ size_t cyr_tree_mode_t_workspace_bytes(const cyr_policy* p, int32_t S, int32_t c
   const size_t raw = ((size_t)S * widest * cap * 2 * p->E * p->elem + 255) / 256 * 256;
   const long long cols = (long long)S * widest * cap;
   size_t act = wide_act_bytes(p, cols);
-  if (!p->tc_wide && cyr_gemm_path_applies(simt_precision(p), p->desc, cols))
+  if (p->precision != CYR_BF16_TC && cyr_gemm_path_applies(simt_precision(p), p->desc, cols))
     act = std::max(act, cyr_gemm_workspace_bytes(p->desc, cols));
   return raw + act;
 }
@@ -993,7 +1007,7 @@ int cyr_tree_mode_t_shard_device(const cyr_policy* p, const int32_t* alloc, cons
     const long long par_off = prev_off < 0 ? -1 : prev_off + base;
     // K2: the actor on every (parent, branch) column of this level
     const long long cols = (long long)S * parents * cap;
-    if (p->tc_wide) {
+    if (p->tc_wide || (p->tc_layers && cols >= kTcLayerCols)) {
       long long widest = 1;
       for (int t = 1; t < M; ++t) widest *= R;
       unsigned char* act = static_cast<unsigned char*>(workspace) +

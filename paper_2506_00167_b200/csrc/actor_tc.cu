@@ -324,7 +324,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) actor_tc_kernel(const TcLaunch 
 //           group's two 16 KB staging images, TMA bulk store (LAST: fp32
 //           logits raw[col][2E]).  The K = 64 first layer gets two groups:
 //           it is epilogue-bound (4 MMAs per n tile against 4 images of
-//           stores); deeper layers keep the shared memory for the ring.
+//           stores), as does any layer with <= 4 K tiles (cfg2's 256 x 256);
+//           deeper K keeps the shared memory for the ring.
 // Each CTA walks column blocks with a grid stride and every n tile of a block
 // back to back, so the block's A tiles are L2-hot for tiles 2..4 and the
 // epilogue of one tile overlaps the MMAs of the next.  With fewer blocks
@@ -347,6 +348,7 @@ struct TcWideLaunch {
   int split;       // CTAs per column block (n tiles divided between them)
   uint32_t slot_bytes, a_bytes;  // per stage (a_bytes = 0 for the first layer)
   long long w_off;  // this layer's images: [n tile][k tile][256 x 128 B]
+  long long b_stride;  // bytes per k tile: 256 x 128, or npad x 128 for a single n tile
   const unsigned char* act_in;  // [ncb][kt][16 KB]
   unsigned char* act_out;       // [ncb][ceil(out/64)][16 KB]
 };
@@ -355,14 +357,15 @@ __device__ __forceinline__ void epi_sync(int grp) {  // the 128 threads of one e
   asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
 }
 
-template <bool FIRST, bool LAST>
+template <bool FIRST, bool LAST, int EG>
 __global__ void __launch_bounds__(kWideFirstThreads, 1) actor_tc_wide_kernel(const TcWideLaunch q) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   unsigned char* ring = base;
   unsigned char* feat = ring + (size_t)q.nslots * q.slot_bytes;  // FIRST: 2 x 16 KB
-  constexpr int EG = FIRST ? 2 : 1;  // epilogue groups of 4 warps
+  // EG epilogue groups of 4 warps: 2 where the layer is epilogue-bound
+  // (few K tiles per n tile), 1 where the MMAs dominate (ring depth first)
   unsigned char* stg = feat + (FIRST ? 2 * kWideImage : 0);      // !LAST: EG x 2 x 16 KB
   uint64_t* bars = reinterpret_cast<uint64_t*>(stg + (LAST ? 0 : EG * 2 * kWideImage));
   uint64_t* full = bars;
@@ -421,7 +424,7 @@ __global__ void __launch_bounds__(kWideFirstThreads, 1) actor_tc_wide_kernel(con
               bulk_g2s(dst, q.act_in + ((long long)cb * q.kt + t) * kWideImage, kWideImage,
                        &full[slot]);
             bulk_g2s(dst + q.a_bytes,
-                     p.tc_blob + q.w_off + ((long long)nt * q.kt + t) * (256 * 128), b_bytes,
+                     p.tc_blob + q.w_off + ((long long)nt * q.kt + t) * q.b_stride, b_bytes,
                      &full[slot]);
           }
         }
@@ -657,13 +660,15 @@ int cyr_launch_actor_tc_layer(const cyr::ActorDesc& desc, const unsigned char* t
   q.nts = (npad + 255) / 256;
   q.ncb = (int)((ncols + cyr::kTcM - 1) / cyr::kTcM);
   q.w_off = w_off;
+  q.b_stride = (q.nts > 1 ? 256 : npad) * 128ll;
   q.act_in = act_in;
   q.act_out = act_out;
   q.a_bytes = first ? 0u : (uint32_t)cyr::kWideImage;
   const int b_rows = std::min(256, npad);
   q.slot_bytes = (uint32_t)((q.a_bytes + b_rows * 128 + 1023) / 1024 * 1024);
+  const int eg = (first || q.kt <= 4) ? 2 : 1;  // epilogue groups (see the kernel)
   const size_t fixed = 1024 + (first ? 2 * cyr::kWideImage : 0) +
-                       (last ? 0 : (first ? 4 : 2) * cyr::kWideImage) +
+                       (last ? 0 : eg * 2 * cyr::kWideImage) +
                        (4 * cyr::kWideMaxSlots + 16) * 8 + 16;
   static int max_smem = 0, sms = 0;
   if (!max_smem) {
@@ -677,18 +682,19 @@ int cyr_launch_actor_tc_layer(const cyr::ActorDesc& desc, const unsigned char* t
   const size_t smem = fixed + (size_t)q.nslots * q.slot_bytes;
   q.split = std::max(1, std::min(q.nts, sms / std::max(q.ncb, 1)));
   const dim3 grid((unsigned)(std::min(q.ncb, sms / q.split) * q.split));
-#define CYR_WIDE(F, LST)                                                                       \
+#define CYR_WIDE(F, LST, G)                                                                    \
   do {                                                                                         \
-    if (cudaFuncSetAttribute(cyr::actor_tc_wide_kernel<F, LST>,                                \
+    if (cudaFuncSetAttribute(cyr::actor_tc_wide_kernel<F, LST, G>,                             \
                              cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem) !=         \
         cudaSuccess)                                                                           \
       return CYR_CUDA_ERROR;                                                                   \
-    cyr::actor_tc_wide_kernel<F, LST>                                                          \
+    cyr::actor_tc_wide_kernel<F, LST, G>                                                       \
         <<<grid, F ? cyr::kWideFirstThreads : cyr::kWideThreads, smem, stream>>>(q);           \
   } while (0)
-  if (first) CYR_WIDE(true, false);
-  else if (last) CYR_WIDE(false, true);
-  else CYR_WIDE(false, false);
+  if (first) CYR_WIDE(true, false, 2);
+  else if (last) CYR_WIDE(false, true, 1);
+  else if (eg == 2) CYR_WIDE(false, false, 2);
+  else CYR_WIDE(false, false, 1);
 #undef CYR_WIDE
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
 }
