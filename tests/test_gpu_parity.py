@@ -538,3 +538,57 @@ def test_tree_leaf_scoring_matches_oracle(golden, name, margin):
         assert np.array_equal(ok[s].astype(np.int64) & ((1 << cfg.meta["num_embb"]) - 1), bits)
         for got, want in ((expect[s, 0], er), (expect[s, 1], eg), (expect[s, 2], el)):
             assert abs(got - want) <= 1e-12 * max(1.0, abs(want)), (s, got, want)
+
+
+# ------------------------------------------------ envelope: E = 32 users
+def _e32_inputs(slots, seed):
+    from paper_2506_00167_b200 import CellConfig, draw_branch_noise, make_streams, substream
+    cell = CellConfig(780, 32, 195)
+    rng = substream(seed, "scenario")
+    allocs = np.stack([np.bincount(rng.integers(0, 32, size=65), minlength=32) * 12
+                       for _ in range(slots)]).astype(np.int32)
+    eps = draw_branch_noise(make_streams(seed, cell.num_branches), cell.num_branches, 32, slots)
+    return cell, allocs, eps
+
+
+@pytest.mark.parametrize("slots", [48, 1300])  # warp-per-row K3 / lane-per-row K3
+def test_codebooks_e32_match_oracle(slots):
+    """The widest supported cell (E = 32: every lane of the warp mapping, a
+    32-user serial loop in the lane mapping) against the oracle."""
+    from oracle import slot
+    from paper_2506_00167_b200 import AgentHyper, make_agent, substream
+    cell, allocs, eps = _e32_inputs(slots, 5)
+    agent = make_agent(cell, AgentHyper(actor_hidden=(64, 64), actor_final_scale=1.0),
+                       substream(5, "agent-init"))
+    pol = DevicePolicy(agent.actor, "fp64")
+    eng = CodebookEngine(pol, cell, max_slots=slots)
+    got = eng.run(torch.from_numpy(allocs).cuda(), torch.from_numpy(eps).cuda()).cpu().numpy()
+    eng.check()
+    want, infos = slot.batch_codebooks(agent.actor.weights, agent.actor.biases, allocs,
+                                       cell.total_scs, cell.urllc_sc_len, eps, details=True)
+    bad = [(s, j) for s in range(slots) for j in range(1, cell.num_branches + 1)
+           if not np.array_equal(got[s, j], want[s, j]) and infos[s]["margin"][j - 1] >= 1e-9]
+    assert not bad, bad[:5]
+    pol.close()
+
+
+def test_mode_t_e32_matches_oracle():
+    from dataclasses import replace
+    from oracle import mode_t
+    from paper_2506_00167_b200 import substream
+    cell, allocs, eps = _e32_inputs(2, 6)
+    cell = replace(cell, minislots=3)
+    actor = tree.make_mode_t_actor(cell, (64, 64), substream(6, "mode-t"), final_scale=1.0)
+    pol = DevicePolicy(actor, "fp64")
+    mcs = np.random.default_rng(6).integers(0, 6, size=allocs.shape).astype(np.int32)
+    got = tree.build_tree_mode_t(pol, cell, torch.from_numpy(allocs).cuda(),
+                                 torch.from_numpy(mcs).cuda(),
+                                 torch.from_numpy(eps).cuda()).cpu().numpy()
+    for s in range(2):
+        want, margins = mode_t.mode_t_tree(actor.weights, actor.biases, allocs[s], mcs[s],
+                                           cell.total_scs, cell.urllc_sc_len, 3, eps[s],
+                                           details=True)
+        taint = _taint(margins, cell.num_branches, 1e-9)
+        diff = (got[s, :, :32] != want).any(axis=1)
+        assert not (diff & ~taint).any()
+    pol.close()
