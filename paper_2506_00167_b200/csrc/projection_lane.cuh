@@ -51,7 +51,7 @@ struct LaneRow {
   const double* cT;  // caps (allocation row as doubles), same layout
   int E;
   double d;
-  bool bis, degen;
+  bool bis, degen, full;
   double lo, hi;
   __device__ __forceinline__ double b(int e) const { return bT[e * 32]; }
   __device__ __forceinline__ double c(int e) const { return cT[e * 32]; }
@@ -68,6 +68,7 @@ __device__ __forceinline__ void kl_setup_lane(LaneRow& r) {
   const bool active = r.d > 0.0;
   r.degen = active && (pos_cap < __dsub_rn(r.d, 1e-12));
   r.bis = active && !r.degen;
+  r.full = r.bis && pos_cap <= r.d;
   r.lo = 0.0;
   r.hi = 0.0;
   if (r.bis) {
@@ -83,6 +84,7 @@ __device__ __forceinline__ void kl_setup_lane(LaneRow& r) {
 // Water-level estimate (any summation order: only a starting point for the
 // exact threshold search) — water_level of projection.cuh.
 __device__ __forceinline__ double water_level_lane(const LaneRow& r) {
+  if (r.full) return r.lo;  // all users capped (water_level of projection.cuh)
   double nu = r.hi;
   unsigned prev = 0xffffffffu;
   for (int it = 0; it <= r.E; ++it) {
@@ -307,7 +309,7 @@ __device__ void codebook_rows_lane(const RawT* raw, long long row0, int nrows, i
   }
   r.E = E;
   r.d = (double)((long long)j * L);
-  r.bis = r.degen = false;
+  r.bis = r.degen = r.full = false;
   r.lo = r.hi = 0.0;
   long long thr = 0;
   if (live) {
