@@ -10,6 +10,7 @@ from .device import DevicePolicy, policy_for, publish, set_default_precision, se
 from .engine import (
     Codebook,
     CodebookEngine,
+    CodebookStream,
     Streams,
     build_codebook,
     build_codebooks_host,
@@ -21,7 +22,7 @@ from .policy import AgentHyper, MlpParams, SacAgent, init_mlp, load_mlp, make_ag
 from .seeding import substream
 
 __all__ = [
-    "AgentHyper", "CellConfig", "Codebook", "CodebookEngine", "DevicePolicy",
+    "AgentHyper", "CellConfig", "Codebook", "CodebookEngine", "CodebookStream", "DevicePolicy",
     "InfeasibleDemandError", "MlpParams", "NativeLibraryError", "PuncturingVector",
     "SacAgent", "ScheduleVector", "Streams", "build_codebook", "build_codebooks_host",
     "draw_branch_noise", "init_mlp", "load_mlp", "make_agent", "make_streams", "policy_for",

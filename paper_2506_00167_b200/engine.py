@@ -249,3 +249,91 @@ class CodebookEngine:
         out_pinned.copy_(self.codebooks[:s], non_blocking=True)
         self.check()
         return out_pinned
+
+
+class CodebookStream:
+    """Slot-after-slot O-DU serving loop on one GPU (the batch API a
+    scheduler calls every slot).
+
+    ``submit(alloc_pinned, eps_pinned, out_pinned)`` enqueues one batch:
+    H2D of its schedules and branch noise from pinned host memory, K2 -> K3
+    (codebooks), the D2H of the codebooks into ``out_pinned``, and K1 (the
+    arrival tree, left in HBM) when ``with_tree``.  Two batches are in
+    flight: batch i+1's upload and actor/enforcement are issued while batch
+    i's tree expansion and download run, on separate CUDA streams, with the
+    device buffers double-buffered.  ``wait(handle)`` returns ``out_pinned``
+    once that batch's codebooks are on the host, raising the reference's
+    exception for a failing slot.  Nothing is skipped: every batch does all
+    of its H2D, kernels and D2H.
+    """
+
+    def __init__(self, policy: DevicePolicy, cell, max_slots: int, with_tree: bool = True,
+                 device=None):
+        import torch
+        self.torch = torch
+        self.engines = [CodebookEngine(policy, cell, max_slots, with_tree=False, device=device)
+                        for _ in range(2)]
+        eng = self.engines[0]
+        self.cell, self.cap, self.users, self.device = cell, eng.cap, eng.users, eng.device
+        self.with_tree = with_tree
+        self.node_state = None
+        if with_tree:
+            from . import tree as _tree
+            _tree.check_tree_geometry(cell)
+            self.node_state = torch.empty(
+                (int(max_slots), _tree.num_nodes(self.cap, cell.minislots),
+                 _tree.state_stride(self.users)), dtype=torch.int16, device=eng.device)
+        self.s_main = torch.cuda.Stream(device=eng.device)  # uploads, K2, K3, downloads
+        self.s_tree = torch.cuda.Stream(device=eng.device)  # K1
+        self.free = [torch.cuda.Event() for _ in range(2)]  # buffer set reusable
+        self.count = 0
+        self.waited = 0
+
+    def submit(self, alloc_pinned, eps_pinned=None, out_pinned=None):
+        torch = self.torch
+        if self.count - self.waited >= 2:
+            raise RuntimeError("at most two batches in flight: wait() for the oldest first")
+        b = self.count % 2
+        self.count += 1
+        eng = self.engines[b]
+        s = int(alloc_pinned.shape[0])
+        if out_pinned is None:
+            out_pinned = torch.empty((s, self.cap + 1, self.users), dtype=torch.int32,
+                                     pin_memory=True)
+        main = self.s_main
+        main.wait_event(self.free[b])  # the tree of the batch that last used set b read it
+        with torch.cuda.stream(main):
+            alloc_d = alloc_pinned.to(eng.device, non_blocking=True)
+            eps_d = None if eps_pinned is None else eps_pinned.to(eng.device, non_blocking=True)
+            eng.run(alloc_d, eps_d, slots=s, stream=main)
+            books = torch.cuda.Event()
+            books.record(main)
+            out_pinned.copy_(eng.codebooks[:s], non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(main)
+        if self.with_tree:
+            tree_stream = self.s_tree
+            tree_stream.wait_event(books)
+            _native.check(_native.lib().cyr_tree_expand_device(
+                eng.codebooks.data_ptr(), s, self.users, self.cap, self.cell.minislots,
+                self.node_state.data_ptr(), tree_stream.cuda_stream), "tree")
+            self.free[b].record(tree_stream)
+        else:
+            self.free[b].record(main)
+        # keep the device inputs alive until their stream has consumed them
+        return (ready, eng, out_pinned, alloc_d, eps_d)
+
+    def wait(self, handle):
+        ready, eng, out_pinned, _, _ = handle
+        ready.synchronize()
+        self.waited += 1
+        code = int(eng.status[0].item())
+        if code:
+            eng.status.zero_()
+            _native.check(code, "codebook stream")
+        return out_pinned
+
+    def drain(self):
+        """Block until every submitted batch (trees included) has finished."""
+        self.s_main.synchronize()
+        self.s_tree.synchronize()

@@ -592,3 +592,37 @@ def test_mode_t_e32_matches_oracle():
         diff = (got[s, :, :32] != want).any(axis=1)
         assert not (diff & ~taint).any()
     pol.close()
+
+
+def test_codebook_stream_matches_engine(golden):
+    """CodebookStream (two batches in flight, double-buffered, separate
+    streams for K1) returns every batch's codebooks exactly as the one-shot
+    engine does, and the tree of the last batch equals expand_tree's."""
+    from paper_2506_00167_b200 import CodebookStream
+    cfg = golden.config("cfg2")
+    agent = cfg.agent()
+    pol = DevicePolicy(agent.actor, "fp32")
+    allocs, eps = cfg["alloc"], cfg["eps"]
+    batches = [(allocs[i:i + 16], eps[i:i + 16]) for i in range(0, 64, 16)]
+    ref = CodebookEngine(pol, cfg.cell, max_slots=16)
+    want = [ref.run(torch.from_numpy(a).cuda(), torch.from_numpy(e).cuda()).cpu().numpy()
+            for a, e in batches]
+    st = CodebookStream(pol, cfg.cell, max_slots=16, with_tree=True)
+    outs, pending = [], None
+    for a, e in batches:
+        h = st.submit(torch.from_numpy(a).pin_memory(), torch.from_numpy(e).pin_memory())
+        if pending is not None:
+            outs.append(st.wait(pending).numpy().copy())
+        pending = h
+    outs.append(st.wait(pending).numpy().copy())
+    st.drain()
+    for got, w in zip(outs, want):
+        assert np.array_equal(got, w)
+    last = tree.expand_tree(torch.from_numpy(want[-1]).cuda(), cfg.cell)
+    assert torch.equal(st.node_state[:16], last)
+    with pytest.raises(RuntimeError):
+        a, e = batches[0]
+        st.submit(torch.from_numpy(a).pin_memory(), torch.from_numpy(e).pin_memory())
+        st.submit(torch.from_numpy(a).pin_memory(), torch.from_numpy(e).pin_memory())
+        st.submit(torch.from_numpy(a).pin_memory(), torch.from_numpy(e).pin_memory())
+    st.drain()
