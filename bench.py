@@ -178,6 +178,14 @@ def measured_peak_hbm():
         return HBM_FALLBACK_GBS, "B200_PROFILING.md fallback (of fallback)"
 
 
+def measured_peak_bf16():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["bf16_tflops_sustained"])
+    except (OSError, KeyError, ValueError):
+        return 2250.0  # nominal dense bf16 (B200_PROFILING.md)
+
+
 def committed_traffic():
     """dram read+write bytes per K1 launch from the committed ncu --set full
     capture (profiles/), or None."""
@@ -254,12 +262,14 @@ def run_ours(args, rank, world, local_rank):
 
     def step(events=None):
         """K2 -> K3 (-> K1) for all slots (+ all-gather); events = (start,
-        tree_start, tree_end, end) recorded on the launching stream."""
+        tree_start, tree_end, end, actor_end) recorded on the launching stream."""
         if events:
             events[0].record(stream)
         _native.check(lib.cyr_actor_forward_device(pol.handle, alloc_d.data_ptr(), SLOTS,
                                                    cell.total_scs, cell.num_branches,
                                                    eng.raw.data_ptr(), st))
+        if events:
+            events[4].record(stream)
         _native.check(lib.cyr_codebook_from_raw_device(
             pol.handle, eng.raw.data_ptr(), alloc_d.data_ptr(), eps_d.data_ptr(), SLOTS,
             cell.total_scs, cell.urllc_sc_len, eng.codebooks.data_ptr(), None, None, None, None,
@@ -282,7 +292,7 @@ def run_ours(args, rank, world, local_rank):
         step()
     eng.check()
 
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
     with ClockSampler(local_rank) as clocks:
         if world > 1:
             dist.barrier()
@@ -296,6 +306,8 @@ def run_ours(args, rank, world, local_rank):
         eng.check()
         step_ms = [e[0].elapsed_time(e[3]) for e in evs]
         tree_ms = [e[1].elapsed_time(e[2]) for e in evs]
+        actor_ms = float(np.mean([e[0].elapsed_time(e[4]) for e in evs]))
+        k3_ms = float(np.mean([e[4].elapsed_time(e[1]) for e in evs]))
 
         # ---- e2e through the public serving API (CodebookStream) with host
         # buffers: every step uploads its schedules + noise from pinned host
@@ -368,6 +380,30 @@ def run_ours(args, rank, world, local_rank):
                     "traffic": None if traffic is None else traffic.get("bytes_per_launch"),
                     "traffic_source": None if traffic is None else traffic.get("source")}
 
+    # every kernel of the step against its bound (live CUDA-event times)
+    sizes = [cell.num_embb + 1, *HIDDEN, 2 * cell.num_embb]
+    k2_flops = 2.0 * SLOTS * cell.num_branches * sum(i * o for i, o in zip(sizes[:-1], sizes[1:]))
+    fma_peak = 148 * 128 * 2 * 1965e6 / 1e12
+    k3_bytes = SLOTS * (cell.num_branches * 2 * cell.num_embb * 4 + cell.num_embb * 4
+                        + cell.num_branches * cell.num_embb * 8
+                        + (cell.num_branches + 1) * cell.num_embb * 4)
+    kernels = [
+        {"kernel": "K2 actor_tiled_kernel (fp32 SIMT, 4096 branch columns)", "bound": "fma",
+         "ms": actor_ms, "achieved": k2_flops / (actor_ms * 1e-3) / 1e12, "peak": fma_peak,
+         "unit": "TFLOP/s", "frac": k2_flops / (actor_ms * 1e-3) / 1e12 / fma_peak,
+         "peak_source": "spec: 148 SMs x 128 FP32 lanes x 2 x 1965 MHz",
+         "work": f"{k2_flops / 1e6:.0f} MFLOP (2 * sum in*out per column)"},
+        {"kernel": "K3 codebook_kernel (fp64 head + exact projection + Huntington-Hill)",
+         "bound": "latency", "ms": k3_ms,
+         "achieved": k3_bytes / (k3_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+         "frac": k3_bytes / (k3_ms * 1e-3) / 1e9 / peak,
+         "work": f"{k3_bytes / 1e6:.2f} MB in/out; one warp per row, ~46 dependent fp64 "
+                 "sqrt steps per coupled call: latency-bound, not bandwidth-bound"},
+    ]
+    if roofline:
+        kernels.append({k: roofline[k] for k in ("kernel", "bound", "achieved", "peak", "unit",
+                                                 "frac")} | {"ms": roofline["kernel_ms"]})
+
     cores_rate, cores, cpu_wall = cpu_baseline(agent, cell, allocs, eps) if world == 1 else \
         (None, None, None)
     core1 = single_core_latency_us(agent, cell, allocs, eps) if world == 1 else None
@@ -388,6 +424,7 @@ def run_ours(args, rank, world, local_rank):
         "mode_t": mode_t,
         "mode_t_sharded": sharded,
         "roofline": roofline,
+        "kernels": kernels,
         "cpu_baseline": None if cores_rate is None else {
             "value": cores_rate, "unit": UNIT, "cores": cores, "kind": "port",
             "sample": f"{SLOTS} slots (one step's workload) over {cores} processes, "
@@ -427,8 +464,14 @@ def mode_t_run(cell, hidden, slots, reps=3, fp32_reps=None):
         torch.cuda.synchronize()
         ms = a.elapsed_time(b) / n
         states[prec] = st.cpu().numpy()[:, :, :cell.num_embb]
+        eff = flops / (ms * 1e-3) / 1e12
+        peak = 148 * 128 * 2 * 1965e6 / 1e12 if prec == "fp32" else measured_peak_bf16()
         out[prec] = {"ms_per_tree_batch": ms, "trees_per_s": slots / (ms * 1e-3),
-                     "actor_tflops_effective": flops / (ms * 1e-3) / 1e12}
+                     "actor_tflops_effective": eff,
+                     "effective_frac_of_peak": eff / peak,
+                     "peak": peak, "peak_source": "spec fp32 FMA (148x128x2x1965 MHz)"
+                     if prec == "fp32" else "MEASURED_PEAKS.json bf16 sustained",
+                     "note": "whole tree time (actor + K3 + features) over actor FLOPs"}
         pol.close()
     same = (states["fp32"] == states["bf16_tc"]).all(axis=2)
     out.update({"actor": "x".join(str(h) for h in hidden), "slots": slots,
