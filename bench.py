@@ -536,12 +536,43 @@ def mode_t_sharded(world, rank, dev, reps=3):
     return res
 
 
+def mode_t_cpu(cell, hidden, sample_levels, seed=11):
+    """The Mode-T oracle (float64 numpy: the reference's actor, head and
+    enforcer per node) timed on a sampled subtree — levels 1..sample_levels
+    of one slot — and scaled by parents (one coupled enforcement and cap
+    actor columns each) to the full tree.  Mode T has no reference
+    implementation; this is the port's cost."""
+    from dataclasses import replace
+    from oracle import mode_t
+    from paper_2506_00167_b200 import substream, tree
+    actor = tree.make_mode_t_actor(cell, hidden, substream(0, "mode-t"))
+    allocs, eps = synthetic_inputs(cell, 1, seed=seed)
+    mcs = np.random.default_rng(seed).integers(0, 6, size=allocs.shape).astype(np.int32)
+    r = cell.num_branches + 1
+    sample_parents = sum(r ** t for t in range(sample_levels))
+    full_parents = sum(r ** t for t in range(cell.minislots))
+    t0 = time.perf_counter()
+    mode_t.mode_t_tree(actor.weights, actor.biases, allocs[0], mcs[0], cell.total_scs,
+                       cell.urllc_sc_len, sample_levels, eps[0])
+    wall = time.perf_counter() - t0
+    per_parent = wall / sample_parents
+    return {"sample": f"levels 1..{sample_levels} of one slot ({sample_parents} parents, "
+                      f"{sample_parents * cell.num_branches} actor columns), one process",
+            "sample_s": wall, "per_parent_ms": per_parent * 1e3,
+            "est_s_per_tree_one_core": per_parent * full_parents,
+            "est_trees_per_s_all_cores": (os.cpu_count() or 1) / (per_parent * full_parents),
+            "cores": os.cpu_count() or 1, "kind": "port (estimate: per-parent cost x parents)"}
+
+
 def mode_t_all(cell):
     """cfg2 geometry (8 slots) and the cfg5 large tree (configs[4])."""
     from paper_2506_00167_b200 import CellConfig
-    return {"cfg2": mode_t_run(cell, HIDDEN, 8),
-            "cfg5": mode_t_run(CellConfig(780, 16, 130), (1024, 1024, 1024), 1, reps=3,
-                               fp32_reps=1)}
+    cfg5 = CellConfig(780, 16, 130)
+    out = {"cfg2": mode_t_run(cell, HIDDEN, 8),
+           "cfg5": mode_t_run(cfg5, (1024, 1024, 1024), 1, reps=3, fp32_reps=1)}
+    out["cfg2"]["cpu"] = mode_t_cpu(cell, HIDDEN, 4)
+    out["cfg5"]["cpu"] = mode_t_cpu(cfg5, (1024, 1024, 1024), 3)
+    return out
 
 
 def latency_run(agent, cell, allocs, n):
