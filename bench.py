@@ -347,6 +347,7 @@ def run_ours(args, rank, world, local_rank):
 
         # ---- single-slot latency through the drop-in build_codebook
         lat = latency_run(agent, cell, allocs, args.latency_slots)
+        strong = cfg4_strong(pol, cell, world, rank, dev)
         mode_t = mode_t_all(cell) if (rank == 0 and not args.no_mode_t) else None
         sharded = None
         if not args.no_mode_t:
@@ -423,6 +424,7 @@ def run_ours(args, rank, world, local_rank):
         "latency_us": lat,
         "mode_t": mode_t,
         "mode_t_sharded": sharded,
+        "cfg4_strong": strong,
         "roofline": roofline,
         "kernels": kernels,
         "cpu_baseline": None if cores_rate is None else {
@@ -605,7 +607,76 @@ def latency_run(agent, cell, allocs, n):
                         "device_p99": float(np.percentile(device, 99)),
                         "slots": n}
     set_weight_sync("check")
+    # BASELINE configs[0]: the reference's CPU-runnable cell (E=4, cap 2)
+    from paper_2506_00167_b200 import AgentHyper, CellConfig, make_agent, substream
+    cell1 = CellConfig(780, 4, 300)
+    agent1 = make_agent(cell1, AgentHyper(actor_hidden=HIDDEN), substream(0, "agent-init"))
+    allocs1, _ = synthetic_inputs(cell1, 64)
+    streams = make_streams(7, cell1.num_branches)
+    for s in range(20):
+        build_codebook(agent1, ScheduleVector(allocs1[s], [0] * 4), streams)
+    host, device = [], []
+    for s in range(n):
+        cb = build_codebook(agent1, ScheduleVector(allocs1[s % 64], [0] * 4), streams)
+        host.append(cb.gen_ns / 1e3)
+        device.append(cb.device_ns / 1e3)
+    out["cfg1_stochastic"] = {"host_p50": float(np.percentile(host, 50)),
+                              "host_p99": float(np.percentile(host, 99)),
+                              "host_max": float(np.max(host)),
+                              "device_p50": float(np.percentile(device, 50)),
+                              "device_p99": float(np.percentile(device, 99)), "slots": n,
+                              "cell": "N=780, E=4, L=300 (cap 2), actor 2x256"}
+    out["cell"] = "stochastic/deterministic: cfg2 (N=780, E=10, L=195, cap 4), actor 2x256"
     return out
+
+
+def cfg4_strong(pol, cell, world, rank, dev, steps=20):
+    """BASELINE configs[3] literally: ONE 256-cell O-DU batch split across the
+    ranks (strong scaling: 256 / N cells per GPU) with the NCCL all-gather of
+    the codebooks; K2 -> K3 -> K1 per rank, CUDA events, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2506_00167_b200 import CodebookEngine, sharding
+    cells = 256
+    allocs, eps = synthetic_inputs(cell, cells, seed=4)
+    lo, hi = sharding.shard_bounds(cells, world, rank)
+    eng = CodebookEngine(pol, cell, max_slots=max(1, hi - lo), with_tree=True, device=dev)
+    al = torch.from_numpy(allocs[lo:hi]).to(dev)
+    ep = torch.from_numpy(eps[lo:hi]).to(dev)
+    width = sharding.max_shard(cells, world)
+    padded = torch.zeros((width, cell.num_branches + 1, cell.num_embb), dtype=torch.int32,
+                         device=dev)
+    gathered = torch.empty((world * width,) + tuple(padded.shape[1:]), dtype=torch.int32,
+                           device=dev)
+
+    def step():
+        if hi > lo:
+            eng.run(al, ep)
+            padded[: hi - lo].copy_(eng.codebooks[: hi - lo])
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, padded)
+
+    for _ in range(3):
+        step()
+    eng.check()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        step()
+    b.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b) / steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    return {"workload": "cfg4: one 256-cell batch (cfg2 geometry) split across ranks, codebooks "
+                        "+ Mode-R trees, NCCL all-gather of the codebooks",
+            "cells": cells, "cells_per_rank": hi - lo, "ranks": world, "ms_per_batch": ms,
+            "codebooks_per_s": cells / (ms * 1e-3), "scaling": "strong",
+            "timing": "CUDA events around back-to-back batches (no L2 flush), max over ranks"}
 
 
 def main():
@@ -616,7 +687,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--precision", choices=("fp32", "fp64"), default="fp32")
     ap.add_argument("--no-tree", action="store_true")
-    ap.add_argument("--latency-slots", type=int, default=2000)
+    ap.add_argument("--latency-slots", type=int, default=10000)
     ap.add_argument("--no-mode-t", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
