@@ -567,10 +567,10 @@ def mode_t_cpu(cell, hidden, sample_levels, seed=11):
 
 
 def mode_t_all(cell):
-    """cfg2 geometry (8 slots) and the cfg5 large tree (configs[4])."""
+    """cfg2 geometry (32 slots per tree batch) and the cfg5 large tree (configs[4])."""
     from paper_2506_00167_b200 import CellConfig
     cfg5 = CellConfig(780, 16, 130)
-    out = {"cfg2": mode_t_run(cell, HIDDEN, 8),
+    out = {"cfg2": mode_t_run(cell, HIDDEN, 32),
            "cfg5": mode_t_run(cfg5, (1024, 1024, 1024), 1, reps=3, fp32_reps=1)}
     out["cfg2"]["cpu"] = mode_t_cpu(cell, HIDDEN, 4)
     out["cfg5"]["cpu"] = mode_t_cpu(cfg5, (1024, 1024, 1024), 3)

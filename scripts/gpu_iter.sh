@@ -1,8 +1,11 @@
-# Quick GPU iteration: parity tests, latency trace, K3-heavy Mode-T probe.
+# Quick GPU iteration: parity tests, Mode-T probes with launch lists (K3 focus).
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
 tail -3 gpurun_out/pytest_gpu.log
-CYR_TRACE=1 timeout 300 python scripts/latency_probe.py --calls 300 | head -30
-timeout 300 python scripts/latency_probe.py --calls 2000 | head -3
-timeout 600 python scripts/mode_t_probe.py --reps 3 --cfg cfg2 --slots 8 --precision bf16_tc
-timeout 600 python scripts/mode_t_probe.py --reps 3 --cfg cfg5 --slots 1 --precision bf16_tc
+for c in "cfg2 8 fp32" "cfg5 1 bf16_tc"; do
+  set -- $c
+  timeout 600 python scripts/mode_t_probe.py --reps 3 --cfg $1 --slots $2 --precision $3
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/launches_k3_$1.csv python scripts/mode_t_probe.py --reps 1 --cfg $1 --slots $2 --precision $3 > /dev/null 2>&1
+  python scripts/launch_table.py gpurun_out/launches_k3_$1.csv | grep -E "tree_level_kernel|total"
+done
