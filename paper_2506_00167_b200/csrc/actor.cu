@@ -655,11 +655,20 @@ int launch_actor_tiled_auto(const ActorLaunch& p, int sm_count, cudaStream_t str
   }
   constexpr int kMax = sizeof(T) == 4 ? 64 : 32;
   int tc = 8;
+  // largest tile that still gives ~every SM a CTA: at 8/16 columns the
+  // tile is shared-memory-bound (weights re-read per 2 columns), so 80 %
+  // of the SMs with 32-column tiles beat all of them with 16 (bench K2 at
+  // 4096 columns: 48 -> 33 us)
   for (int cand = kMax; cand >= 8; cand >>= 1) {
     if (!fits(cand)) continue;
     tc = cand;
-    if ((p.ncols + cand - 1) / cand >= sm_count) break;
+    if ((p.ncols + cand - 1) / cand * 5 >= 4ll * sm_count) break;
   }
+  static const int forced = [] {  // CYR_TILED_TC: force the column tile (A/B)
+    const char* e = getenv("CYR_TILED_TC");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 8 || forced == 16 || forced == 32 || (forced == 64 && sizeof(T) == 4)) tc = forced;
   if (!fits(tc)) return CYR_UNSUPPORTED;
   switch (tc) {
     case 64: if constexpr (sizeof(T) == 4) return launch_actor_tiled<T, 64>(p, stream);
