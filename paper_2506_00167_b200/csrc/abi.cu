@@ -60,6 +60,20 @@ static inline void host_stamp(int k) {
   }
 }
 
+// CYR_TRACE=1: device-memory counters of the lane-mapped K3 phase profile
+// (device atomics; cyr_debug_trace reports them in slots 36..44)
+static unsigned long long* g_prof_dev = nullptr;
+unsigned long long* cyr_prof_buffer() {
+  if (cyr_trace_buffer() == nullptr) return nullptr;
+  if (g_prof_dev == nullptr) {
+    if (cudaMalloc(reinterpret_cast<void**>(&g_prof_dev), 16 * sizeof(unsigned long long)) !=
+        cudaSuccess)
+      return nullptr;
+    cudaMemset(g_prof_dev, 0, 16 * sizeof(unsigned long long));
+  }
+  return g_prof_dev;
+}
+
 unsigned long long* cyr_trace_buffer() {
   static const bool on = [] {
     const char* e = getenv("CYR_TRACE");
@@ -877,6 +891,11 @@ int cyr_debug_trace(int64_t* out, int32_t n) {
   if (!out || n < 0) return CYR_BAD_ARG;
   for (int i = 0; i < n && i < 64; ++i)
     out[i] = g_trace_host ? (int64_t)g_trace_host[i] : 0;
+  if (g_prof_dev != nullptr) {
+    unsigned long long h[9] = {};
+    cudaMemcpy(h, g_prof_dev, sizeof(h), cudaMemcpyDeviceToHost);
+    for (int i = 0; i < 9 && 36 + i < n; ++i) out[36 + i] = (int64_t)h[i];
+  }
   return CYR_OK;
 }
 

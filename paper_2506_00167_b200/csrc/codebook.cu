@@ -58,6 +58,7 @@ struct TreeIO {
   int16_t* node;
   int E, cap, epad, parents;
   long long nodes_per_slot, parent_off, child_off;
+  unsigned long long* prof;  // CYR_TRACE=1: lane-mapping phase profile, or null
   __device__ const int32_t* alloc_row(long long group) const {
     return alloc + (group / parents) * E;
   }
@@ -116,7 +117,8 @@ __global__ void __launch_bounds__(32 * kLaneWarps, kLaneMinBlocks) tree_level_ke
   const int n = (int)min((long long)gpw, groups - g0);
   const long long row0 = g0 * io.cap;
   codebook_rows_lane<RawT, TreeIO>(raw + row0 * 2 * io.E, row0, n * io.cap, io.cap, io.E, L, io,
-                                   status, lane_smem + (size_t)w * lane_scratch_bytes(io.E));
+                                   status, lane_smem + (size_t)w * lane_scratch_bytes(io.E),
+                                   io.prof);
 }
 
 // K3 of a SMALL Mode-T level (few rows: the lane mapping would leave the
@@ -585,7 +587,8 @@ int cyr_launch_tree_level(int precision, const void* raw, const int32_t* alloc, 
                           int32_t* status, cudaStream_t stream) {
   if (S <= 0) return CYR_OK;
   if (E < 1 || E > cyr::kMaxUsers || cap < 1 || cap > 16) return CYR_UNSUPPORTED;
-  cyr::TreeIO io{alloc, eps, node, E, cap, epad, parents, nodes_per_slot, parent_off, child_off};
+  cyr::TreeIO io{alloc, eps, node, E, cap, epad, parents, nodes_per_slot, parent_off, child_off,
+                 cyr_prof_buffer()};
   const long long groups = (long long)S * parents;
   if (groups * cap <= warp_level_rows()) {  // small level: warp per row (latency)
     const int gpc = 32 / cap;

@@ -203,7 +203,8 @@ int cyr_launch_tree_score(const int32_t* codebook, const int32_t* alloc, const d
 int cyr_launch_pf_schedule(double* avg_tput, const double* rate, int C, int E, double beta,
                            int num_rbs, int rb_size, int32_t* alloc, int32_t* status,
                            cudaStream_t stream);
-unsigned long long* cyr_trace_buffer();  // device alias of the trace block or null
+unsigned long long* cyr_trace_buffer();
+unsigned long long* cyr_prof_buffer();  // CYR_TRACE=1: K3 lane phase counters (device)  // device alias of the trace block or null
 int cyr_launch_latency_bench(int which, int iters, long long* cycles, double* sink);
 int cyr_launch_empty(int cluster, cudaStream_t stream);
 int cyr_launch_actor_mode_t(int precision, const cyr::ActorDesc& desc, const void* blob,

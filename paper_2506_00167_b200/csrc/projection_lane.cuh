@@ -288,10 +288,24 @@ __host__ __device__ constexpr size_t lane_scratch_bytes(int E) {
 // Rows row0 .. row0 + nrows of this warp (whole calls of `cap` rows, lane
 // r = local row r).  IO: alloc_row(group), eps_row(grow, group, j) and
 // emit_lane(grow, group, j, hT, E, mT, nu, margin, iters) (one lane).
+// CYR_TRACE=1 phase profile of the lane mapping (prof != null): per warp,
+// clock64 cycles of each phase summed into prof[0..7] (head, setup, water
+// level, threshold, coupled loop, finish, Huntington-Hill, emit), warps in
+// prof[8].  Diagnostics only (system-scope atomics on mapped memory).
 template <typename RawT, typename IO>
 __device__ void codebook_rows_lane(const RawT* raw, long long row0, int nrows, int cap, int E, int L,
-                                   const IO& io, int32_t* status, unsigned char* scratch) {
+                                   const IO& io, int32_t* status, unsigned char* scratch,
+                                   unsigned long long* prof = nullptr) {
   const int lane = threadIdx.x & 31;
+  long long tp = prof ? clock64() : 0;
+  auto mark = [&](int k) {
+    if (prof) {
+      __syncwarp();
+      const long long now = clock64();
+      if (lane == 0) atomicAdd(prof + k, (unsigned long long)(now - tp));
+      tp = now;
+    }
+  };
   const size_t plane = (size_t)E * 32;  // elements of one [E][32] array
   double* bT = reinterpret_cast<double*>(scratch) + lane;
   double* cT = bT + plane;
@@ -322,11 +336,19 @@ __device__ void codebook_rows_lane(const RawT* raw, long long row0, int nrows, i
       const double a = eps ? tanh(__dadd_rn(mu, __dmul_rn(exp(ls), eps[e]))) : tanh(mu);
       bT[e * 32] = __dmul_rn(__dmul_rn(__dadd_rn(a, 1.0), 0.5), r.c(e));
     }
+  }
+  mark(0);
+  double x0 = 0.0;
+  if (live) {
     const double capsum = np_sum_lane(E, [&](int e) { return r.c(e); });  // enforcer.py:64
     if (r.d > capsum) set_status(status, CYR_INFEASIBLE);
     kl_setup_lane(r);
-    if (r.bis) thr = fill_threshold_lane(r, water_level_lane(r));
   }
+  mark(1);
+  if (live && r.bis) x0 = water_level_lane(r);
+  mark(2);
+  if (live && r.bis) thr = fill_threshold_lane(r, x0);
+  mark(3);
   // the coupled loop of every call of the warp at once (lanes = rows)
   double lo[1] = {r.lo}, hi[1] = {r.hi};
   const long long tt[1] = {thr};
@@ -334,11 +356,15 @@ __device__ void codebook_rows_lane(const RawT* raw, long long row0, int nrows, i
   const int iters = coupled_bisection<1>(lo, hi, tt, bis, cap);
   r.lo = lo[0];
   r.hi = hi[0];
-  if (live) {
-    const double nu = kl_finish_lane(r);
-    const double margin = hh_lane(bT, cT, E, (long long)j * L, hT);
-    io.emit_lane(grow, group, j, hT, E, bT, nu, margin, iters);
-  }
+  mark(4);
+  double nu = 0.0, margin = 0.0;
+  if (live) nu = kl_finish_lane(r);
+  mark(5);
+  if (live) margin = hh_lane(bT, cT, E, (long long)j * L, hT);
+  mark(6);
+  if (live) io.emit_lane(grow, group, j, hT, E, bT, nu, margin, iters);
+  mark(7);
+  if (prof && lane == 0) atomicAdd(prof + 8, 1ull);
 }
 
 }  // namespace cyr
