@@ -347,7 +347,10 @@ def run_ours(args, rank, world, local_rank):
 
         # ---- single-slot latency through the drop-in build_codebook
         lat = latency_run(agent, cell, allocs, args.latency_slots)
-        strong = cfg4_strong(pol, cell, world, rank, dev)
+        try:
+            strong = cfg4_strong(pol, cell, world, rank, dev)
+        except Exception as exc:  # reported, never fatal for the headline
+            strong = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         mode_t = mode_t_all(cell) if (rank == 0 and not args.no_mode_t) else None
         sharded = None
         if not args.no_mode_t:
