@@ -41,6 +41,7 @@ HIDDEN = (256, 256)
 SLOTS = 1024
 BUDGET_US = 125.0
 HBM_FALLBACK_GBS = 6650.0
+WRITE_PEAK_GBS = 6990.0  # measured pure-write ceiling (profiles/r01_write_patterns.txt)
 L2_FLUSH_BYTES = 256 << 20
 
 
@@ -382,7 +383,12 @@ def run_ours(args, rank, world, local_rank):
                     "peak_source": peak_src, "algorithmic_bytes_per_launch": tree_bytes,
                     "kernel_ms": tree_ms, "share_of_step": tree_ms / mean_ms,
                     "traffic": None if traffic is None else traffic.get("bytes_per_launch"),
-                    "traffic_source": None if traffic is None else traffic.get("source")}
+                    "traffic_source": None if traffic is None else traffic.get("source"),
+                    # K1 only writes: the pure-write ceiling measured on this pool
+                    # (scripts/micro/write_patterns.cu, incompressible 3.2 GB, best
+                    # store pattern; profiles/r01_write_patterns.txt)
+                    "write_peak": WRITE_PEAK_GBS,
+                    "frac_of_write_peak": achieved / WRITE_PEAK_GBS}
 
     # every kernel of the step against its bound (live CUDA-event times)
     sizes = [cell.num_embb + 1, *HIDDEN, 2 * cell.num_embb]

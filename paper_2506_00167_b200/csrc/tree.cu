@@ -13,7 +13,8 @@
 // Epad = roundup(E, 8) lanes (16/32/48/64 bytes): 128-bit vector granules.
 //
 // B200 design (HBM-write-bound): a persistent grid walks work items =
-// (slot, level, block of NP parents).  Codebook column 0 is the all-zero
+// (slot, level, block of NP parents; NP = 128 for large batches, five CTAs
+// per SM).  Codebook column 0 is the all-zero
 // vector (engine.py:112), so leading zero digits add nothing and a parent's
 // state is T3[p mod R^3] + T3[p div R^3] (+ T3[...] for deeper trees) where
 // T3 holds the sums of every 3-digit suffix — two shared-memory lookups
@@ -28,6 +29,7 @@
 #include "cyrus_b200.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace cyr {
 
@@ -300,7 +302,12 @@ int launch_tree_t(const TreeParams& p, int sm_count, cudaStream_t stream) {
       cudaSuccess)
     return CYR_CUDA_ERROR;
   const long long items = (long long)p.S * p.blocks_per_slot;
-  const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (227 * 1024) / (smem + 1024)));
+  int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (227 * 1024) / (smem + 1024)));
+  static const int per_sm_env = [] {  // CYR_TREE_PER_SM: cap on resident CTAs per SM (A/B)
+    const char* e = getenv("CYR_TREE_PER_SM");
+    return e ? atoi(e) : 0;
+  }();
+  if (per_sm_env > 0) per_sm = std::min(per_sm, per_sm_env);
   const long long grid = std::min<long long>(items, (long long)sm_count * per_sm);
   kern<<<(unsigned)grid, p.np_item, smem, stream>>>(p);
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
@@ -355,7 +362,16 @@ int tree_params(TreeParams& p, const int32_t* codebook, int S, int E, int cap, i
   // tree spreads over all SMs; large batches use 256-parent items
   long long big_items = 0;
   for (long long t = 0, q = 1; t < M; ++t, q *= R) big_items += (q + 255) / 256;
-  p.np_item = (big_items * S < 2ll * sm_count) ? 64 : kTreeThreads;
+  // large batches: 128-parent items (20 KB child runs), so five CTAs fit an
+  // SM and keep ~10 bulk stores in flight per SM (sweep, bench workload:
+  // 256-parent items with 2 CTAs/SM 538 us = 5.95 TB/s; 128-parent items
+  // with 5 CTAs/SM 470 us = 6.8 TB/s)
+  p.np_item = (big_items * S < 2ll * sm_count) ? 64 : 128;
+  static const int np_env = [] {  // CYR_TREE_NP: parents per work item, 64/128/256 (A/B)
+    const char* e = getenv("CYR_TREE_NP");
+    return e ? atoi(e) : 0;
+  }();
+  if (np_env == 64 || np_env == 128 || np_env == 256) p.np_item = np_env;
   long long parents = 1, nodes = 0;
   p.level_blocks[0] = 0;
   for (int t = 0; t < M; ++t) {
