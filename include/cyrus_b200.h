@@ -172,6 +172,23 @@ int cyr_mlp_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
 int cyr_mlp_forward_device(const cyr_policy* mlp, const double* x, int32_t cols, void* out,
                            void* stream);
 
+/* ---- erasure LDPC peeling (decodability model "erasure_ldpc", §8(f) f2) --- */
+/* phy.peel_decode (phy.py:125-143) for B erasure patterns on one code graph
+ * (phy.LdpcCode, phy.py:83-120): edge_var / edge_check [n_edges] int32 (the
+ * graph's sockets), erased [B][n] uint8 (punctured + channel-erased
+ * symbols), ok [B] uint8 = 1 iff peeling recovers every erasure.  Device
+ * pointers; n_checks * 4 + n <= 200 KiB. */
+int cyr_ldpc_peel_device(const int32_t* edge_var, const int32_t* edge_check, int32_t n,
+                         int32_t n_checks, int32_t n_edges, const uint8_t* erased, int32_t B,
+                         uint8_t* ok, void* stream);
+/* The same with the erasures given as per-mini-slot puncture counts
+ * counts [B][M] of one user with n_sym = M * n_e symbols: symbol v < n_sym
+ * is erased iff v / M < counts[v % M] (decode_user's layout, phy.py:204-208,
+ * clean channel); padding symbols n_sym..n-1 are known. */
+int cyr_ldpc_peel_counts_device(const int32_t* edge_var, const int32_t* edge_check, int32_t n,
+                                int32_t n_checks, int32_t n_edges, const int32_t* counts,
+                                int32_t M, int32_t n_sym, int32_t B, uint8_t* ok, void* stream);
+
 /* ---- batched PF scheduler (the producer of s(t)) -------- */
 /* scheduler.pf_schedule (scheduler.py:79-106) for C cells at once: every
  * one of num_rbs RBs goes to argmax_e rate_e / max((1-beta)*avg_e +

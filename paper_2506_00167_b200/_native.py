@@ -61,6 +61,9 @@ SIGNATURES = {
                                        _vp, _vp, _vp, _vp]),
     "cyr_pf_schedule_device": (_c_int, [_vp, _vp, _c_i32, _c_i32, ctypes.c_double, _c_i32, _c_i32,
                                         _vp, _vp, _vp]),
+    "cyr_ldpc_peel_device": (_c_int, [_vp, _vp, _c_i32, _c_i32, _c_i32, _vp, _c_i32, _vp, _vp]),
+    "cyr_ldpc_peel_counts_device": (_c_int, [_vp, _vp, _c_i32, _c_i32, _c_i32, _vp, _c_i32, _c_i32,
+                                             _c_i32, _vp, _vp]),
     "cyr_debug_trace": (_c_int, [_pi64, _c_i32]),
     "cyr_selftest_latency": (_c_int, [_c_i32, _c_i32, _pi64]),
     "cyr_selftest_launch": (_c_int, [_c_i32, _c_i32, _pi64]),

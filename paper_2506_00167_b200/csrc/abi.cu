@@ -955,6 +955,29 @@ size_t cyr_tree_mode_t_workspace_bytes(const cyr_policy* p, int32_t S, int32_t c
   return raw + act;
 }
 
+int cyr_ldpc_peel_device(const int32_t* edge_var, const int32_t* edge_check, int32_t n,
+                         int32_t n_checks, int32_t n_edges, const uint8_t* erased, int32_t B,
+                         uint8_t* ok, void* stream) {
+  if (n < 1 || n_checks < 1 || n_edges < 1 || B < 0) return CYR_BAD_ARG;
+  if (B > 0 && (!edge_var || !edge_check || !erased || !ok)) return CYR_BAD_ARG;
+  const int rc = cyr_launch_ldpc_peel(edge_var, edge_check, n, n_checks, n_edges, erased, nullptr,
+                                      1, 0, B, ok, static_cast<cudaStream_t>(stream));
+  if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+  return rc;
+}
+
+int cyr_ldpc_peel_counts_device(const int32_t* edge_var, const int32_t* edge_check, int32_t n,
+                                int32_t n_checks, int32_t n_edges, const int32_t* counts,
+                                int32_t M, int32_t n_sym, int32_t B, uint8_t* ok, void* stream) {
+  if (n < 1 || n_checks < 1 || n_edges < 1 || B < 0 || M < 1 || n_sym < 0 || n_sym > n)
+    return CYR_BAD_ARG;
+  if (B > 0 && (!edge_var || !edge_check || !counts || !ok)) return CYR_BAD_ARG;
+  const int rc = cyr_launch_ldpc_peel(edge_var, edge_check, n, n_checks, n_edges, nullptr, counts,
+                                      M, n_sym, B, ok, static_cast<cudaStream_t>(stream));
+  if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+  return rc;
+}
+
 int cyr_pf_schedule_device(double* avg_tput, const double* inst_rate, int32_t C, int32_t E,
                            double beta, int32_t num_rbs, int32_t rb_size, int32_t* alloc,
                            int32_t* status, void* stream) {

@@ -203,6 +203,9 @@ int cyr_launch_tree_score(const int32_t* codebook, const int32_t* alloc, const d
 int cyr_launch_pf_schedule(double* avg_tput, const double* rate, int C, int E, double beta,
                            int num_rbs, int rb_size, int32_t* alloc, int32_t* status,
                            cudaStream_t stream);
+int cyr_launch_ldpc_peel(const int32_t* edge_var, const int32_t* edge_check, int n, int n_checks,
+                         int n_edges, const uint8_t* erased, const int32_t* counts, int M,
+                         int n_sym, int B, uint8_t* ok, cudaStream_t stream);
 unsigned long long* cyr_trace_buffer();
 unsigned long long* cyr_prof_buffer();  // CYR_TRACE=1: K3 lane phase counters (device)  // device alias of the trace block or null
 int cyr_launch_latency_bench(int which, int iters, long long* cycles, double* sink);

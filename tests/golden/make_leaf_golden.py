@@ -31,9 +31,10 @@ from punctsim.scheduler import DEFAULT_MCS_TABLE  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 OUT = os.path.join(HERE, "leaf_golden.npz")
-# (config, slot, margin)
+# (config, slot, margin); margin "ldpc": DecodabilityModel("erasure_ldpc",
+# code_seed=3) with a clean channel (sc_erasure_prob 0)
 CASES = [("cfg1", 0, None), ("cfg1", 5, 0.1), ("paper", 3, None), ("desk", 2, None),
-         ("cfg1", 9, None)]
+         ("cfg1", 9, None), ("cfg1", 2, "ldpc")]
 
 
 def main():
@@ -46,7 +47,8 @@ def main():
         alloc = [int(v) for v in z[f"{name}/alloc"][slot]]
         mcs = [int(v) for v in z[f"{name}/mcs"][slot]]
         sched = core.ScheduleVector(alloc, mcs)
-        model = phy.DecodabilityModel("threshold", margin=margin)
+        model = (phy.DecodabilityModel("erasure_ldpc", code_seed=3) if margin == "ldpc"
+                 else phy.DecodabilityModel("threshold", margin=margin))
         q = phy.LinkQuality(snr_db=20.0, sc_erasure_prob=0.0)
         rng = np.random.default_rng(0)
         mm, r = m["minislots"], book.shape[0]

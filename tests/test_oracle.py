@@ -188,6 +188,8 @@ def test_leaf_score_oracle_matches_reference_golden(golden):
     z = np.load(path)
     info = json.loads(str(z["meta_json"]))
     for key, case in info.items():
+        if case["margin"] == "ldpc":
+            continue  # erasure_ldpc: test_ldpc_leaf_oracle_matches_reference_golden
         cfg = golden.config(case["config"])
         s = case["slot"]
         book = cfg["sto/codebook"][s]
@@ -225,3 +227,68 @@ def test_pf_oracle_matches_reference_golden():
             for t in range(rates.shape[0]):
                 a, state = pf.pf_schedule(state, rates[t, c], float(beta[c]), 65, 12)
                 assert np.array_equal(a, alloc[t, c]) and np.array_equal(state, avg[t + 1, c])
+
+
+# ------------------------------------------------- erasure LDPC (f2)
+def _ldpc_cases():
+    import json
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "ldpc_golden.npz"))
+    meta = json.loads(str(z["meta_json"]))
+    return z, meta
+
+
+def test_ldpc_graphs_and_oracle_match_reference_golden():
+    """paper_2506_00167_b200.phy builds the reference's graphs bit for bit
+    (same seeded construction), and oracle.ldpc.peel_decode reproduces
+    phy.peel_decode on every frozen pattern."""
+    import hashlib
+    from oracle import ldpc
+    from paper_2506_00167_b200 import phy
+    z, meta = _ldpc_cases()
+    model = phy.DecodabilityModel(code_seed=3)
+    for key, m in meta.items():
+        code = model.code_for(m["n_symbols"], m["code_rate"])
+        h = hashlib.sha256()
+        h.update(code.edge_var.astype("<i8").tobytes())
+        h.update(code.edge_check.astype("<i8").tobytes())
+        assert (code.n, code.dv, code.dc) == (m["n"], m["dv"], m["dc"])
+        assert h.hexdigest() == m["graph_sha256"], key
+        erased = np.unpackbits(z[key + "/erased"], axis=1)[:, :code.n].astype(bool)
+        got = [ldpc.peel_decode(code.edge_var, code.edge_check, code.n_checks, e) for e in erased]
+        assert got == list(z[key + "/ok"]), key
+
+
+def test_ldpc_leaf_oracle_matches_reference_golden(golden):
+    """Every leaf of a cfg1 slot under the erasure_ldpc model (clean
+    channel): the oracle peel on our graphs reproduces decode_user."""
+    import json
+    import os
+    from oracle import leaf_score, ldpc
+    from paper_2506_00167_b200 import phy, tree
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "leaf_golden.npz"))
+    info = json.loads(str(z["meta_json"]))
+    key = [k for k, c in info.items() if c["margin"] == "ldpc"][0]
+    case = info[key]
+    cfg = golden.config(case["config"])
+    s = case["slot"]
+    book, alloc, mcs = cfg["sto/codebook"][s], cfg["alloc"][s], cfg["mcs"][s]
+    m = cfg.meta["minislots"]
+    model = phy.DecodabilityModel(code_seed=3)
+    rates = np.asarray(tree.MCS_CODE_RATES)[mcs]
+    cum = leaf_score.leaf_states(book, m)
+    r = book.shape[0]
+    digits = np.stack(np.unravel_index(np.arange(r ** m), (r,) * m), axis=1)
+    bits = np.zeros(r ** m, dtype=np.int64)
+    for e in range(alloc.size):
+        n_e = int(alloc[e])
+        if n_e <= 0:
+            bits |= 1 << e
+            continue
+        code = model.code_for(m * n_e, float(rates[e]))
+        pats, inv = np.unique(book[digits, e], axis=0, return_inverse=True)
+        ok = np.array([ldpc.peel_decode(code.edge_var, code.edge_check, code.n_checks,
+                                        phy.puncture_mask(code, p, m)) for p in pats])
+        bits |= ok[inv.ravel()].astype(np.int64) << e
+    assert np.array_equal(bits, z[key + "/bits"])
+    assert cum.shape[0] == r ** m
