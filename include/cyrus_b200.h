@@ -204,7 +204,8 @@ int cyr_pf_schedule_device(double* avg_tput, const double* inst_rate, int32_t C,
 /* ---- arrival tree, Mode R (K1) ------------------------------------------- */
 /* Node count excluding the root: sum_{t=1..M} (cap+1)^t. */
 int64_t cyr_tree_num_nodes(int32_t cap, int32_t M);
-/* int16 lanes per node record (E rounded up to a multiple of 8). */
+/* int16 lanes per node record: E rounded up to a multiple of 2 (packed
+ * 4-byte words; 20 B at E = 10). */
 int32_t cyr_tree_state_stride(int32_t E);
 /* node_state[s][off(t) + q][:E] = sum of codebook[s][digit_i(q)] over the
  * t digits of q in base cap+1 (engine.py:230 lookups, engine.py:240-241

@@ -876,7 +876,7 @@ int64_t cyr_tree_num_nodes(int32_t cap, int32_t M) {
   return total;
 }
 
-int32_t cyr_tree_state_stride(int32_t E) { return E < 1 ? 0 : (E + 7) / 8 * 8; }
+int32_t cyr_tree_state_stride(int32_t E) { return E < 1 ? 0 : (E + 1) / 2 * 2; }
 
 int cyr_tree_expand_device(const int32_t* codebook, int32_t S, int32_t E, int32_t cap, int32_t M,
                            int16_t* node_state, void* stream) {

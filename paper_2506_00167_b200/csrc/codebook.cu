@@ -77,27 +77,25 @@ struct TreeIO {
       if (j == 1) node[first + lane] = (int16_t)(lane < E ? cum : 0);
     }
   }
-  // one lane = one row: child j's record (and child 0's for j == 1), 16 B at a time
+  // one lane = one row: child j's record (and child 0's for j == 1), one
+  // 4-byte word (two users) at a time; records are epad = roundup(E, 2) lanes
   __device__ void emit_lane(long long, long long group, int j, const int* hT, int, const double*,
                             double, double, int) const {
     const long long s = group / parents, q = group % parents;
     const long long base = s * nodes_per_slot;
-    const int16_t* par = parent_off >= 0 ? node + (base + parent_off + q) * epad : nullptr;
-    int16_t* first = node + (base + child_off + q * (cap + 1)) * epad;
-    for (int e0 = 0; e0 < epad; e0 += 8) {
-      uint4 pv = make_uint4(0, 0, 0, 0);
-      if (par) pv = *reinterpret_cast<const uint4*>(par + e0);
-      const int16_t* pc = reinterpret_cast<const int16_t*>(&pv);
-      alignas(16) int16_t v[8], v0[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int e = e0 + k;
-        const int cum = e < E ? pc[k] : 0;
-        v[k] = (int16_t)(e < E ? cum + hT[e * 32] : 0);
-        v0[k] = (int16_t)cum;
-      }
-      *reinterpret_cast<uint4*>(first + (long long)j * epad + e0) = *reinterpret_cast<const uint4*>(v);
-      if (j == 1) *reinterpret_cast<uint4*>(first + e0) = *reinterpret_cast<const uint4*>(v0);
+    const uint32_t* par =
+        parent_off >= 0 ? reinterpret_cast<const uint32_t*>(node + (base + parent_off + q) * epad)
+                        : nullptr;
+    uint32_t* first = reinterpret_cast<uint32_t*>(node + (base + child_off + q * (cap + 1)) * epad);
+    const int W = epad / 2;
+    for (int w = 0; w < W; ++w) {
+      const uint32_t pv = par ? par[w] : 0u;
+      const int e = 2 * w;
+      const int lo = (int16_t)(pv & 0xffffu), hi = (int16_t)(pv >> 16);
+      const int v0 = lo + hT[e * 32];
+      const int v1 = e + 1 < E ? hi + hT[(e + 1) * 32] : 0;
+      first[(long long)j * W + w] = (uint32_t)(uint16_t)v0 | ((uint32_t)(uint16_t)v1 << 16);
+      if (j == 1) first[w] = pv;
     }
   }
 };

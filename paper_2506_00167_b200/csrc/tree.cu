@@ -9,22 +9,28 @@
 // Layout: per slot, levels t = 1..M in BFS order; level t holds (cap+1)^t
 // nodes; the children of node p of level t-1 are p*(cap+1) + k, k = 0..cap,
 // so the children of a contiguous parent range are one contiguous run.
-// A node record is the per-user cumulative puncture count as int16, padded to
-// Epad = roundup(E, 8) lanes (16/32/48/64 bytes): 128-bit vector granules.
+// A node record is the per-user cumulative puncture count as int16, packed:
+// Ep = roundup(E, 2) lanes = W 4-byte words (20 B at E = 10, 8 B at E = 4,
+// 32 B at E = 16).  Only the algorithmic bytes reach HBM (the earlier
+// 16-byte-granule padding wrote 32 B records at E = 10: 60 % more).
 //
-// B200 design (HBM-write-bound): a persistent grid walks work items =
-// (slot, level, block of NP parents; NP = 128 for large batches, five CTAs
-// per SM).  Codebook column 0 is the all-zero
-// vector (engine.py:112), so leading zero digits add nothing and a parent's
-// state is T3[p mod R^3] + T3[p div R^3] (+ T3[...] for deeper trees) where
-// T3 holds the sums of every 3-digit suffix — two shared-memory lookups
-// instead of a per-digit divide-and-add loop.  The cap+1 codebook columns
-// live in registers; each child is one packed 16-bit vector add per
-// 16-byte granule into a shared-memory staging buffer, and one thread then
-// writes the whole contiguous child run with a single TMA bulk store
-// (cp.async.bulk.global.shared::cta, SASS UBLKCP).  Two staging buffers let
-// the next item's compute overlap the previous item's store.  A codebook
-// whose column 0 is not zero falls back to the per-digit sum.
+// B200 design (HBM-write-bound): a persistent grid; each CTA owns a
+// contiguous range of work items = (slot, level, block of NP parents), so
+// the per-slot setup — the codebook columns in registers and the 3-digit
+// suffix table T3 in shared memory — is built once per slot a CTA touches,
+// not once per item.  Codebook column 0 is the all-zero vector
+// (engine.py:112), so leading zero digits add nothing and a parent's state
+// is T3[p mod R^3] + T3[p div R^3] (+ T3[...] for deeper trees): two
+// shared-memory lookups instead of a per-digit divide-and-add loop.  Each
+// child is one packed 16-bit vector add (__vadd2) per word into a
+// shared-memory staging buffer laid out exactly like the child run in HBM
+// (shifted so smem and global addresses agree mod 16).  One thread writes
+// the run's 16-byte-aligned body with a single TMA bulk store
+// (cp.async.bulk.global.shared::cta, SASS UBLKCP); the at most 3 + 3 words
+// of unaligned head and tail go out as plain stores.  A ring of kStages
+// staging buffers with ONE CTA barrier per item lets the next items'
+// compute overlap the previous stores.  A codebook whose column 0 is not
+// zero falls back to the per-digit sum.
 #include "cyrus_internal.cuh"
 #include "cyrus_b200.h"
 
@@ -33,14 +39,16 @@
 
 namespace cyr {
 
-constexpr int kTreeThreads = 256;  // max parents per work item (= threads per CTA)
+constexpr int kTreeThreads = 128;  // parents per full work item (= threads per CTA)
+constexpr int kStages = 3;         // staging buffers per CTA
 constexpr int kMaxLevels = 16;
 
 struct TreeParams {
   const int32_t* codebook;
   int16_t* out;
-  int S, E, cap, M, epad;
-  int np_item;                       // parents per work item (= blockDim.x)
+  int S, E, cap, M;
+  int words;                         // 4-byte words per record (Ep / 2)
+  int np_item;                       // parents per work item (<= kTreeThreads)
   int r3;                            // (cap+1)^3
   unsigned r3_magic;                 // floor(q / r3) == __umulhi(q, r3_magic) in range
   long long nodes_per_slot;
@@ -56,6 +64,10 @@ struct TreeParams {
   uint32_t* leaf_ok;                 // [S][R^M] decoding-user bitmask, or null
   double* partial;                   // [S][leaf items][2]: sum w*lost, sum w*goodput
 };
+
+__host__ __device__ __forceinline__ size_t tree_stage_bytes(int np, int R, int words) {
+  return ((size_t)np * R * words * 4 + 15) / 16 * 16 + 16;  // + 16: the mod-16 shift
+}
 
 __device__ __forceinline__ uint4 vadd16(uint4 a, uint4 b) {
   return make_uint4(__vadd2(a.x, b.x), __vadd2(a.y, b.y), __vadd2(a.z, b.z), __vadd2(a.w, b.w));
@@ -74,14 +86,15 @@ __device__ __forceinline__ unsigned lane_bits(unsigned m) {  // 0xffff lanes -> 
   return (m & 1u) | ((m >> 15) & 2u);
 }
 
-template <int CH, int R, bool SCORE>  // CH: 16-byte granules per record; R = cap + 1
-__global__ void __launch_bounds__(kTreeThreads, 2) tree_kernel(const TreeParams p) {
+template <int CH, int R, bool SCORE>  // CH: 16-byte register granules per record; R = cap + 1
+__global__ void __launch_bounds__(kTreeThreads) tree_kernel(const TreeParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int NP = p.np_item;
-  const size_t stage_bytes = (size_t)NP * R * CH * 16;
+  const int W = p.words;
+  const size_t stage_bytes = tree_stage_bytes(NP, R, W);
   const int r3 = p.r3;
-  uint4* t3 = reinterpret_cast<uint4*>(smem + 2 * stage_bytes);  // [r3][CH], per item
-  int16_t* bookw = reinterpret_cast<int16_t*>(t3 + (size_t)r3 * CH);  // [R][CH*8]
+  uint4* t3 = reinterpret_cast<uint4*>(smem + kStages * stage_bytes);  // [r3][CH], per slot
+  int16_t* bookw = reinterpret_cast<int16_t*>(t3 + (size_t)r3 * CH);   // [R][CH*8]
   // SCORE: per-user int16 bounds and allocations as packed granules, leaf-digit
   // probabilities, and the CTA reduction scratch
   int16_t* boundw = bookw + R * CH * 8;                 // [CH*8]
@@ -90,29 +103,33 @@ __global__ void __launch_bounds__(kTreeThreads, 2) tree_kernel(const TreeParams 
   double* red = probs + kMaxLevels * R;                 // [kTreeThreads / 32][2]
   const int tid = threadIdx.x;
   const int items = p.S * p.blocks_per_slot;  // host-checked to fit in int
+  // this CTA's contiguous item range
+  const int chunk = (items + gridDim.x - 1) / gridDim.x;
+  const int w_begin = blockIdx.x * chunk;
+  const int w_end = min(items, w_begin + chunk);
+  int cur_s = -1;
+  uint4 col[R][CH];
+  bool zero0 = true;
   int it = 0;
-  for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
-    const int buf = it & 1;
-    uint4* stage = reinterpret_cast<uint4*>(smem + buf * stage_bytes);
+  for (int w = w_begin; w < w_end; ++w, ++it) {
     const int s = w / p.blocks_per_slot;
     const int bw = w - s * p.blocks_per_slot;
     int t = 0;
     while (bw >= p.level_blocks[t + 1]) ++t;
     const int p0 = (bw - p.level_blocks[t]) * NP;
     const int np = (int)min((long long)NP, p.level_parents[t] - p0);
-    double acc_lost = 0.0, acc_good = 0.0;  // SCORE: this thread's weighted leaf sums
 
-    if (tid == 0) bulk_wait_read<1>();  // the store issued two items ago released this stage
-    // this slot's codebook as packed int16 granules: cooperative load to
-    // shared memory, then every thread keeps the cap+1 columns in registers
-    const int32_t* cb = p.codebook + (long long)s * R * p.E;
-    for (int idx = tid; idx < R * CH * 8; idx += NP) {
-      const int k = idx / (CH * 8), e = idx % (CH * 8);
-      bookw[idx] = (int16_t)((e < p.E) ? cb[k * p.E + e] : 0);
-    }
-    if constexpr (SCORE) {
-      if (t == p.M - 1) {
-        for (int e = tid; e < CH * 8; e += NP) {
+    if (s != cur_s) {  // per-slot setup (uniform branch)
+      __syncthreads();  // every thread is done with the previous slot's tables
+      // the slot's codebook as packed int16 granules, then every thread keeps
+      // the cap+1 columns in registers
+      const int32_t* cb = p.codebook + (long long)s * R * p.E;
+      for (int idx = tid; idx < R * CH * 8; idx += kTreeThreads) {
+        const int k = idx / (CH * 8), e = idx % (CH * 8);
+        bookw[idx] = (int16_t)((e < p.E) ? cb[k * p.E + e] : 0);
+      }
+      if constexpr (SCORE) {
+        for (int e = tid; e < CH * 8; e += kTreeThreads) {
           int bound = 32767, n = 0;  // padding lanes: always "ok", no SCs
           if (e < p.E) {
             n = p.alloc[(long long)s * p.E + e];
@@ -124,38 +141,44 @@ __global__ void __launch_bounds__(kTreeThreads, 2) tree_kernel(const TreeParams 
           boundw[e] = (int16_t)bound;
           allocw[e] = (int16_t)(n > 0 ? n : 0);
         }
-        for (int idx = tid; idx < p.M * R; idx += NP) probs[idx] = p.prob[idx];
+        for (int idx = tid; idx < p.M * R; idx += kTreeThreads) probs[idx] = p.prob[idx];
       }
-    }
-    __syncthreads();
-    uint4 col[R][CH];
+      __syncthreads();
 #pragma unroll
-    for (int k = 0; k < R; ++k)
+      for (int k = 0; k < R; ++k)
 #pragma unroll
-      for (int c = 0; c < CH; ++c) col[k][c] = reinterpret_cast<const uint4*>(bookw)[k * CH + c];
-    const uint4 c0 = col[0][0];
-    bool zero0 = (c0.x | c0.y | c0.z | c0.w) == 0u;
+        for (int c = 0; c < CH; ++c) col[k][c] = reinterpret_cast<const uint4*>(bookw)[k * CH + c];
+      zero0 = true;
 #pragma unroll
-    for (int c = 1; c < CH; ++c)
-      zero0 = zero0 && (col[0][c].x | col[0][c].y | col[0][c].z | col[0][c].w) == 0u;
-
-    // suffix table (also reused across items: rebuilt per item, it is small)
-    for (int x = tid; x < r3; x += NP) {
-      const int d0 = x % R, d1 = (x / R) % R, d2 = x / (R * R);
+      for (int c = 0; c < CH; ++c)
+        zero0 = zero0 && (col[0][c].x | col[0][c].y | col[0][c].z | col[0][c].w) == 0u;
+      // suffix table of every 3-digit suffix
+      for (int x = tid; x < r3; x += kTreeThreads) {
+        const int d0 = x % R, d1 = (x / R) % R, d2 = x / (R * R);
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        uint4 v = make_uint4(0, 0, 0, 0);
+        for (int c = 0; c < CH; ++c) {
+          uint4 v = make_uint4(0, 0, 0, 0);
 #pragma unroll
-        for (int k = 0; k < R; ++k) {
-          const uint4 ck = col[k][c];
-          if (d0 == k) v = vadd16(v, ck);
-          if (d1 == k) v = vadd16(v, ck);
-          if (d2 == k) v = vadd16(v, ck);
+          for (int k = 0; k < R; ++k) {
+            const uint4 ck = col[k][c];
+            if (d0 == k) v = vadd16(v, ck);
+            if (d1 == k) v = vadd16(v, ck);
+            if (d2 == k) v = vadd16(v, ck);
+          }
+          t3[x * CH + c] = v;
         }
-        t3[x * CH + c] = v;
       }
+      __syncthreads();
+      cur_s = s;
     }
-    __syncthreads();
+
+    // this item's child run in HBM: bytes [gbeg, gend) from p.out
+    const long long first = (long long)s * p.nodes_per_slot + p.child_off[t] + (long long)p0 * R;
+    const long long gbeg = first * W * 4;
+    const int shift = (int)(gbeg & 15);  // smem copy sits at the same address mod 16
+    uint32_t* stw =
+        reinterpret_cast<uint32_t*>(smem + (size_t)(it % kStages) * stage_bytes + shift);
+    double acc_lost = 0.0, acc_good = 0.0;  // SCORE: this thread's weighted leaf sums
 
     if (tid < np) {
       uint4 cum[CH];
@@ -188,11 +211,26 @@ __global__ void __launch_bounds__(kTreeThreads, 2) tree_kernel(const TreeParams 
               for (int c = 0; c < CH; ++c) cum[c] = vadd16(cum[c], col[kk][c]);
         }
       }
-      uint4* dst = stage + (size_t)tid * R * CH;
+      uint32_t* dst = stw + (size_t)tid * R * W;
+      if (W == CH * 4) {  // E a multiple of 8: whole granules (shift is 0, 16-B aligned)
 #pragma unroll
-      for (int k = 0; k < R; ++k)
+        for (int k = 0; k < R; ++k)
 #pragma unroll
-        for (int c = 0; c < CH; ++c) dst[k * CH + c] = vadd16(cum[c], col[k][c]);
+          for (int c = 0; c < CH; ++c)
+            reinterpret_cast<uint4*>(dst)[k * CH + c] = vadd16(cum[c], col[k][c]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+#pragma unroll
+          for (int c = 0; c < CH; ++c) {
+            const uint4 v = vadd16(cum[c], col[k][c]);
+            uint32_t* d = dst + k * W + 4 * c;
+            if (4 * c + 0 < W) d[0] = v.x;
+            if (4 * c + 1 < W) d[1] = v.y;
+            if (4 * c + 2 < W) d[2] = v.z;
+            if (4 * c + 3 < W) d[3] = v.w;
+          }
+      }
       if constexpr (SCORE) {
         if (t == p.M - 1) {  // children are leaves
           double wq = 1.0;   // parent weight: its M-1 digits, first mini-slot first
@@ -220,7 +258,7 @@ __global__ void __launch_bounds__(kTreeThreads, 2) tree_kernel(const TreeParams 
             unsigned okbits = 0, lost2 = 0;
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
-              const uint4 v = dst[k * CH + c], b = bw4[c], a = aw4[c];
+              const uint4 v = vadd16(cum[c], col[k][c]), b = bw4[c], a = aw4[c];
               const unsigned m0 = __vcmples2(v.x, b.x), m1 = __vcmples2(v.y, b.y);
               const unsigned m2 = __vcmples2(v.z, b.z), m3 = __vcmples2(v.w, b.w);
               okbits |= (lane_bits(m0) | lane_bits(m1) << 2 | lane_bits(m2) << 4 |
@@ -229,10 +267,11 @@ __global__ void __launch_bounds__(kTreeThreads, 2) tree_kernel(const TreeParams 
                                              __vadd2(~m2 & a.z, ~m3 & a.w)));
             }
             const unsigned lost = (lost2 & 0xffffu) + (lost2 >> 16);
-            const double w = __dmul_rn(wq, probs[(p.M - 1) * R + k]);
-            acc_lost = __fma_rn(w, (double)lost, acc_lost);
-            acc_good = __fma_rn(w, (double)(tot - lost), acc_good);
-            if (p.leaf_ok) p.leaf_ok[leaf0 + k] = okbits & (p.E >= 32 ? 0xffffffffu : ((1u << p.E) - 1u));
+            const double wgt = __dmul_rn(wq, probs[(p.M - 1) * R + k]);
+            acc_lost = __fma_rn(wgt, (double)lost, acc_lost);
+            acc_good = __fma_rn(wgt, (double)(tot - lost), acc_good);
+            if (p.leaf_ok)
+              p.leaf_ok[leaf0 + k] = okbits & (p.E >= 32 ? 0xffffffffu : ((1u << p.E) - 1u));
           }
         }
       }
@@ -252,7 +291,7 @@ __global__ void __launch_bounds__(kTreeThreads, 2) tree_kernel(const TreeParams 
         __syncthreads();
         if (tid == 0) {
           double l = 0.0, g = 0.0;
-          for (int wi = 0; wi < NP / 32; ++wi) {
+          for (int wi = 0; wi < kTreeThreads / 32; ++wi) {
             l += red[wi * 2];
             g += red[wi * 2 + 1];
           }
@@ -261,14 +300,34 @@ __global__ void __launch_bounds__(kTreeThreads, 2) tree_kernel(const TreeParams 
           p.partial[item * 2] = l;
           p.partial[item * 2 + 1] = g;
         }
-        acc_lost = acc_good = 0.0;
       }
     }
+    // Before the barrier, the store issued kStages-1 items ago must have read
+    // its stage: that is the buffer the NEXT item writes after the barrier.
+    if (tid == 0) bulk_wait_read<kStages - 2>();
     __syncthreads();
-    if (tid == 0) {
-      const long long first = (long long)s * p.nodes_per_slot + p.child_off[t] + (long long)p0 * R;
-      bulk_s2g(p.out + first * p.epad, stage, (uint32_t)((size_t)np * R * CH * 16));
-      bulk_commit();
+    {
+      // body [a16, b16): one bulk store; head [gbeg, a16) and tail [b16, gend):
+      // at most 3 words each, plain stores (neighbouring items own the other
+      // bytes of those granules)
+      const long long gend = gbeg + (long long)np * R * W * 4;
+      long long a16 = (gbeg + 15) & ~15ll, b16 = gend & ~15ll;
+      if (b16 < a16) a16 = b16 = gend;  // shorter than one granule: all plain
+      unsigned char* ob = reinterpret_cast<unsigned char*>(p.out);
+      const unsigned char* sb = reinterpret_cast<const unsigned char*>(stw);
+      if (tid == 0) {
+        if (b16 > a16) bulk_s2g(ob + a16, sb + (a16 - gbeg), (uint32_t)(b16 - a16));
+        bulk_commit();  // one group per item (possibly empty): the ring parity stays exact
+      }
+      if (tid >= 32 && tid < 35) {  // head words
+        const long long g = gbeg + 4 * (tid - 32);
+        if (g < a16)
+          *reinterpret_cast<uint32_t*>(ob + g) = *reinterpret_cast<const uint32_t*>(sb + (g - gbeg));
+      } else if (tid >= 64 && tid < 67) {  // tail words
+        const long long g = b16 + 4 * (tid - 64);
+        if (g >= a16 && g < gend)
+          *reinterpret_cast<uint32_t*>(ob + g) = *reinterpret_cast<const uint32_t*>(sb + (g - gbeg));
+      }
     }
   }
   if (tid == 0) bulk_wait_all();
@@ -291,8 +350,8 @@ __global__ void tree_score_reduce_kernel(const double* __restrict__ partial, int
 
 template <int CH, int R, bool SCORE>
 int launch_tree_t(const TreeParams& p, int sm_count, cudaStream_t stream) {
-  const size_t smem = 2 * (size_t)p.np_item * R * CH * 16 + (size_t)p.r3 * CH * 16 +
-                      (size_t)R * CH * 16 +
+  const size_t smem = kStages * tree_stage_bytes(p.np_item, R, p.words) +
+                      (size_t)p.r3 * CH * 16 + (size_t)R * CH * 16 +
                       (SCORE ? 2 * (size_t)CH * 16 + (size_t)kMaxLevels * R * 8 +
                                    (kTreeThreads / 32) * 16
                              : 0);
@@ -302,14 +361,18 @@ int launch_tree_t(const TreeParams& p, int sm_count, cudaStream_t stream) {
       cudaSuccess)
     return CYR_CUDA_ERROR;
   const long long items = (long long)p.S * p.blocks_per_slot;
-  int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (227 * 1024) / (smem + 1024)));
-  static const int per_sm_env = [] {  // CYR_TREE_PER_SM: cap on resident CTAs per SM (A/B)
+  const int fit = (int)std::max<size_t>(1, (227 * 1024) / (smem + 1024));
+  // 4 resident CTAs per SM (sweep, bench workload, 128-parent items: 3 / 4 / 5
+  // per SM = 368 / 301 / 353 us; more concurrent write streams lose HBM
+  // efficiency, as in the pure-write microbenchmark, profiles/r01_write_patterns.txt)
+  int per_sm = std::min(fit, 4);
+  static const int per_sm_env = [] {  // CYR_TREE_PER_SM: resident CTAs per SM (A/B)
     const char* e = getenv("CYR_TREE_PER_SM");
     return e ? atoi(e) : 0;
   }();
-  if (per_sm_env > 0) per_sm = std::min(per_sm, per_sm_env);
+  if (per_sm_env > 0) per_sm = std::min(per_sm_env, fit);
   const long long grid = std::min<long long>(items, (long long)sm_count * per_sm);
-  kern<<<(unsigned)grid, p.np_item, smem, stream>>>(p);
+  kern<<<(unsigned)grid, kTreeThreads, smem, stream>>>(p);
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
 }
 
@@ -330,7 +393,7 @@ int launch_tree_r(const TreeParams& p, int sm_count, cudaStream_t stream) {
 
 template <bool SCORE>
 int launch_tree_ch(const TreeParams& p, int sm_count, cudaStream_t stream) {
-  switch (p.epad / 8) {
+  switch ((p.words * 2 + 7) / 8) {
     case 1: return launch_tree_r<1, SCORE>(p, sm_count, stream);
     case 2: return launch_tree_r<2, SCORE>(p, sm_count, stream);
     case 3: return launch_tree_r<3, SCORE>(p, sm_count, stream);
@@ -343,13 +406,14 @@ int tree_params(TreeParams& p, const int32_t* codebook, int S, int E, int cap, i
                 int16_t* out, int sm_count) {
   if (E < 1 || E > kMaxUsers || cap < 1 || M < 1 || M > 10) return CYR_BAD_ARG;
   if (cap + 1 > 9) return CYR_UNSUPPORTED;
+  if ((reinterpret_cast<uintptr_t>(out) & 15) != 0) return CYR_BAD_ARG;
   p.codebook = codebook;
   p.out = out;
   p.S = S;
   p.E = E;
   p.cap = cap;
   p.M = M;
-  p.epad = (E + 7) / 8 * 8;
+  p.words = (E + 1) / 2;
   const long long R = cap + 1;
   p.r3 = (int)(R * R * R);
   // ceil(2^32 / r3): floor(q * magic / 2^32) == floor(q / r3) while
@@ -358,20 +422,16 @@ int tree_params(TreeParams& p, const int32_t* codebook, int S, int E, int cap, i
   long long top = 1;
   for (int t = 0; t < M - 1; ++t) top *= R;
   if (top * p.r3 >= (1ll << 32)) return CYR_UNSUPPORTED;
-  // small batches (the single-slot latency path) use 64-parent items so the
-  // tree spreads over all SMs; large batches use 256-parent items
+  // small batches (the single-slot latency path) use 32-parent items so the
+  // tree spreads over all SMs; large batches use kTreeThreads-parent items
   long long big_items = 0;
-  for (long long t = 0, q = 1; t < M; ++t, q *= R) big_items += (q + 255) / 256;
-  // large batches: 128-parent items (20 KB child runs), so five CTAs fit an
-  // SM and keep ~10 bulk stores in flight per SM (sweep, bench workload:
-  // 256-parent items with 2 CTAs/SM 538 us = 5.95 TB/s; 128-parent items
-  // with 5 CTAs/SM 470 us = 6.8 TB/s)
-  p.np_item = (big_items * S < 2ll * sm_count) ? 64 : 128;
-  static const int np_env = [] {  // CYR_TREE_NP: parents per work item, 64/128/256 (A/B)
+  for (long long t = 0, q = 1; t < M; ++t, q *= R) big_items += (q + kTreeThreads - 1) / kTreeThreads;
+  p.np_item = (big_items * S < 2ll * sm_count) ? 32 : kTreeThreads;
+  static const int np_env = [] {  // CYR_TREE_NP: parents per work item, 32/64/128 (A/B)
     const char* e = getenv("CYR_TREE_NP");
     return e ? atoi(e) : 0;
   }();
-  if (np_env == 64 || np_env == 128 || np_env == 256) p.np_item = np_env;
+  if (np_env == 32 || np_env == 64 || np_env == 128) p.np_item = np_env;
   long long parents = 1, nodes = 0;
   p.level_blocks[0] = 0;
   for (int t = 0; t < M; ++t) {

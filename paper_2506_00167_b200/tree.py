@@ -12,7 +12,7 @@ with arrivals-so-far = sum of the path digits (derivable from the index).
 
 Layout (shared with K1 and the oracle): per slot, BFS over levels 1..M;
 level t has (cap+1)^t nodes; node q of level t has parent q // (cap+1) and
-last digit q % (cap+1); records are int16 x Epad (Epad = roundup(E, 8)).
+last digit q % (cap+1); records are int16 x Epad (Epad = roundup(E, 2), packed: only the algorithmic bytes).
 """
 
 from __future__ import annotations

@@ -41,7 +41,7 @@ def test_host_only_helpers():
     assert lib.cyr_tree_num_nodes(4, 7) == 97_655
     assert lib.cyr_tree_num_nodes(2, 7) == 3_279
     assert lib.cyr_tree_num_nodes(6, 7) == 960_799
-    assert [lib.cyr_tree_state_stride(e) for e in (4, 10, 16, 17)] == [8, 16, 16, 24]
+    assert [lib.cyr_tree_state_stride(e) for e in (3, 4, 10, 16, 17)] == [4, 4, 10, 16, 18]
     assert lib.cyr_status_string(1) == b"demand exceeds total capacity"
 
 
