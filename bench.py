@@ -11,7 +11,7 @@ rank with one NCCL all-gather of the codebooks per step):
   * synthetic schedules (engine._synthetic_schedule's generator: uniform
     random RB owners, 65 RBs of 12 SCs) and per-branch noise;
   * one step = K2 actor + K3 codebook for 1024 slots + K1 Mode-R arrival
-    tree (97,655 node states per slot, 3.2 GB written).
+    tree (97,655 packed 20-byte node records per slot, 2.0 GB written).
 value = codebooks/s over all ranks (each codebook carries its full arrival
 tree).  The single-slot latency against the 125 us numerology-3 budget (the
 first half of BASELINE's metric) is measured in the same run through the
@@ -429,7 +429,9 @@ def run_ours(args, rank, world, local_rank):
                 "note": "CodebookStream (public serving API), host wall clock over all "
                         "steps: per step pinned H2D of schedules+noise, K2/K3/K1, D2H of "
                         "the codebooks (node states stay in HBM); two steps in flight; each "
-                        "step writes 3.2 GB (25x L2), no separate flush"},
+                        + (f"step writes {SLOTS * eng.nodes * eng.stride * 2 / 1e9:.1f} GB "
+                           "(16x L2), no separate flush" if not args.no_tree else
+                           "step has no tree (--no-tree)")},
         "latency_us": lat,
         "mode_t": mode_t,
         "mode_t_sharded": sharded,
