@@ -80,6 +80,13 @@ int cyr_policy_update(cyr_policy* policy, const double* weights_blob);
 /* Load a PSIMMLP1 checkpoint file (neural.py:211-225) straight to device. */
 int cyr_policy_load(cyr_policy** out, const char* path, int32_t precision);
 int cyr_policy_destroy(cyr_policy* policy);
+/* The single-slot path (cyr_codebook_host with S*cap <= 8) is served by a
+ * resident 8-CTA cluster kernel that polls a mapped mailbox: no launch per
+ * call.  It leaves by itself after 20 ms without a request
+ * (CYR_SLOT_SERVER_IDLE_MS) and is relaunched on demand; this stops it now
+ * (e.g. before timing other work on the device).  CYR_SLOT_SERVER=0 selects
+ * the per-call graph launch instead. */
+int cyr_policy_quiesce(cyr_policy* policy);
 int cyr_policy_info(const cyr_policy* policy, int32_t* num_users, int32_t* n_sizes,
                     int32_t* precision);
 

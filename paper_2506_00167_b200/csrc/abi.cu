@@ -10,6 +10,8 @@
 #include "cyrus_b200.h"
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
@@ -138,7 +140,21 @@ struct cyr_policy {
     cudaKernelNodeParams kp{};
   };
   std::map<std::tuple<int, int, int, int>, FusedGraph> fused;
+  // persistent slot server of the fused path (actor.cu, slot_server_kernel)
+  struct SlotServer {
+    cyr::SlotMailbox* mb = nullptr;      // mapped pinned host block
+    cyr::SlotMailbox* mb_dev = nullptr;  // its device alias
+    cudaStream_t stream = nullptr;
+    cudaEvent_t exited = nullptr;        // recorded after each server launch
+    bool running = false;
+    std::tuple<int, int, int, int> key{};
+    uint32_t seq = 0;                    // last request issued (== served, between calls)
+  } srv;
 };
+
+extern "C" {
+static void slot_server_stop(cyr_policy* p);
+}
 
 namespace {
 
@@ -565,6 +581,7 @@ int cyr_policy_actions_device(const cyr_policy* p, const int32_t* alloc, const i
 
 int cyr_policy_update(cyr_policy* p, const double* weights_blob) {
   if (!p || !weights_blob) return CYR_BAD_ARG;
+  slot_server_stop(p);
   CYR_CUDA(cudaDeviceSynchronize());  // no launch may still read the old weights
   return upload(p, weights_blob);
 }
@@ -610,8 +627,18 @@ int cyr_policy_load(cyr_policy** out, const char* path, int32_t precision) {
   return cyr_policy_create(out, sizes.data(), (int32_t)n_sizes, blob.data(), precision);
 }
 
+int cyr_policy_quiesce(cyr_policy* p) {
+  if (!p) return CYR_BAD_ARG;
+  slot_server_stop(p);
+  return CYR_OK;
+}
+
 int cyr_policy_destroy(cyr_policy* p) {
   if (!p) return CYR_OK;
+  slot_server_stop(p);
+  if (p->srv.stream) cudaStreamDestroy(p->srv.stream);
+  if (p->srv.exited) cudaEventDestroy(p->srv.exited);
+  if (p->srv.mb) cudaFreeHost(p->srv.mb);
   cudaDeviceSynchronize();
   release_host_path(p);
   if (p->stream) cudaStreamDestroy(p->stream);
@@ -679,6 +706,112 @@ int cyr_codebook_device(const cyr_policy* p, const int32_t* alloc, const double*
                                       nullptr, nullptr, nullptr, status, stream);
 }
 
+// ---- persistent slot server (the fused path without per-call launches) ----
+// CYR_SLOT_SERVER=0 falls back to the per-call graph launch (A/B);
+// CYR_SLOT_SERVER_IDLE_MS: how long an idle server keeps polling (default 20).
+static bool slot_server_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CYR_SLOT_SERVER");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
+static unsigned long long slot_server_idle_ns() {
+  static const unsigned long long ns = [] {
+    const char* e = getenv("CYR_SLOT_SERVER_IDLE_MS");
+    const double ms = e ? atof(e) : 20.0;
+    return (unsigned long long)((ms > 0.0 ? ms : 20.0) * 1e6);
+  }();
+  return ns;
+}
+
+// stop a running server and wait for it to leave (before anything that
+// synchronises the whole device, and before the policy changes)
+static void slot_server_stop(cyr_policy* p) {
+  auto& sv = p->srv;
+  if (!sv.running) return;
+  sv.mb->quit = 1u;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  cudaEventSynchronize(sv.exited);
+  sv.mb->quit = 0u;
+  sv.running = false;
+}
+
+static int slot_server_launch(cyr_policy* p, bool det, int S, int N, int L, int cap) {
+  auto& sv = p->srv;
+  const int rc = cyr_launch_slot_server(p->precision, p->desc, p->blob_d, det, S, p->E, N, L, cap,
+                                        p->cb_d, sv.mb_dev, sv.seq, slot_server_idle_ns(),
+                                        sv.stream);
+  if (rc != CYR_OK) {
+    if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+    return rc;
+  }
+  CYR_CUDA(cudaEventRecord(sv.exited, sv.stream));
+  sv.running = true;
+  return CYR_OK;
+}
+
+// One request through the server: inputs into the mailbox, bump req_seq,
+// spin on done_seq.  A server that idled out just before the request is
+// relaunched (it picks the pending request up: it starts from the last
+// request served).  CYR_UNSUPPORTED: geometry outside the server's range.
+static int slot_server_call(cyr_policy* p, const std::tuple<int, int, int, int>& key,
+                            const int32_t* alloc, const double* eps, int S, int N, int L, int cap,
+                            int32_t* codebook, int64_t* device_ns) {
+  auto& sv = p->srv;
+  const int E = p->E;
+  if (S * (cap + 1) * E > 512 || S * E > 256 || S * cap * E > 256) return CYR_UNSUPPORTED;
+  if (sv.mb == nullptr) {
+    CYR_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&sv.mb), sizeof(cyr::SlotMailbox),
+                           cudaHostAllocMapped | cudaHostAllocPortable));
+    std::memset(static_cast<void*>(sv.mb), 0, sizeof(cyr::SlotMailbox));
+    CYR_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&sv.mb_dev), sv.mb, 0));
+    CYR_CUDA(cudaStreamCreateWithFlags(&sv.stream, cudaStreamNonBlocking));
+    CYR_CUDA(cudaEventCreateWithFlags(&sv.exited, cudaEventDisableTiming));
+  }
+  const bool det = (eps == nullptr);
+  if (sv.running && sv.key != key) slot_server_stop(p);
+  if (sv.running && cudaEventQuery(sv.exited) == cudaSuccess) sv.running = false;  // idled out
+  std::memcpy(sv.mb->alloc, alloc, (size_t)S * E * 4);
+  if (!det) std::memcpy(sv.mb->eps, eps, (size_t)S * cap * E * 8);
+  sv.mb->status = CYR_OK;
+  if (!sv.running) {
+    const int rc = slot_server_launch(p, det, S, N, L, cap);
+    if (rc != CYR_OK) return rc;
+    sv.key = key;
+  }
+  uint32_t next = sv.seq + 1u;
+  if (next == 0u) next = 1u;  // 0 means "leave" to the server
+  std::atomic_thread_fence(std::memory_order_release);
+  sv.mb->req_seq = next;
+  host_stamp(1);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (unsigned spin = 1;; ++spin) {
+    if (sv.mb->done_seq == next) break;
+    if ((spin & 4095u) == 0u) {
+      if (cudaEventQuery(sv.exited) == cudaSuccess && sv.mb->done_seq != next) {
+        // the server left (idle timeout) without seeing this request: relaunch
+        const int rc = slot_server_launch(p, det, S, N, L, cap);
+        if (rc != CYR_OK) return rc;
+      }
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(10)) {
+        slot_server_stop(p);
+        g_last_error = "slot server did not answer within 10 s";
+        return CYR_CUDA_ERROR;
+      }
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  sv.seq = next;
+  host_stamp(4);
+  const int32_t code = sv.mb->status;
+  if (code != CYR_OK) return code;
+  std::memcpy(codebook, sv.mb->cb, (size_t)S * (cap + 1) * E * 4);
+  if (device_ns) *device_ns = (int64_t)(sv.mb->t_end - sv.mb->t_start);
+  return CYR_OK;
+}
+
 int cyr_codebook_host(cyr_policy* p, const int32_t* alloc, const double* eps, int32_t S,
                       int32_t N, int32_t L, int32_t* codebook, int64_t* device_ns) {
   if (!p || p->mode_t || !alloc || !codebook) return CYR_BAD_ARG;
@@ -710,6 +843,13 @@ int cyr_codebook_host(cyr_policy* p, const int32_t* alloc, const double* eps, in
            (reinterpret_cast<const unsigned char*>(host_ptr) - p->pin);
   };
   *p->pin_status = CYR_OK;
+  if (fused && slot_server_enabled()) {
+    // latency path: the resident slot server (no launch per call)
+    host_stamp(0);
+    const int src = slot_server_call(p, key, alloc, eps, S, N, L, cap, codebook, device_ns);
+    if (src != CYR_UNSUPPORTED) return src;
+  }
+  if (p->srv.running) slot_server_stop(p);  // the batch paths below synchronise streams
   if (fused) {
     // latency path: ONE cluster launch (K2 + K3), inputs by value in the
     // launch parameters, codebook + status written straight to mapped pages

@@ -226,9 +226,11 @@ struct Vec16<double> {
   }
 };
 
+// One slot (or a few) through the cluster: K2 layers split over the CTAs,
+// K3 fused on rank 0 (FUSE).  Ranks other than 0 return after the last layer.
 template <typename T, int C, bool FUSE>
-__global__ void __launch_bounds__(kLatThreads, 1)
-    actor_cluster_kernel(const ActorLaunch p, const __grid_constant__ SlotInline inl) {
+__device__ __forceinline__ void cluster_slot(const ActorLaunch& p, const int32_t* alloc,
+                                             const double* eps) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   const int G = (int)cluster.num_blocks();
@@ -241,8 +243,6 @@ __global__ void __launch_bounds__(kLatThreads, 1)
   T* raw_s = act1 + (size_t)rows * C;  // FUSE: rank 0 collects the logits [col][2E]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const T* blob = static_cast<const T*>(p.blob);
-  const int32_t* alloc = p.inline_inputs ? inl.alloc : p.alloc;
-  const double* eps = p.inline_inputs ? (p.eps ? inl.eps : nullptr) : p.eps;
 
   unsigned long long* tr = (FUSE && g == 0) ? p.trace : nullptr;
   trace_stamp(tr, 0);
@@ -348,6 +348,131 @@ __global__ void __launch_bounds__(kLatThreads, 1)
     }
     trace_stamp(tr, 15);
   }
+}
+
+template <typename T, int C, bool FUSE>
+__global__ void __launch_bounds__(kLatThreads, 1)
+    actor_cluster_kernel(const ActorLaunch p, const __grid_constant__ SlotInline inl) {
+  const int32_t* alloc = p.inline_inputs ? inl.alloc : p.alloc;
+  const double* eps = p.inline_inputs ? (p.eps ? inl.eps : nullptr) : p.eps;
+  cluster_slot<T, C, FUSE>(p, alloc, eps);
+}
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Persistent slot server: the fused cluster path in a loop.  Rank 0's thread
+// 0 polls the mapped mailbox (one PCIe read per probe) for a new request
+// number, hands it to every CTA through DSMEM, and all CTAs copy the inputs
+// (the slot's allocations and branch noise) from the mailbox into shared
+// memory; the slot then runs exactly as in actor_cluster_kernel, and rank 0
+// stores the codebook and status into the mailbox, a system-scope fence,
+// the finish time and finally the request number (release).  No kernel
+// launch, graph launch or event sits on the per-call path.  The server
+// leaves on `quit` or after idle_ns without a request; the host relaunches
+// it on demand (abi.cu, slot_server_call).
+template <typename T, int C>
+__global__ void __launch_bounds__(kLatThreads, 1)
+    slot_server_kernel(const ActorLaunch p, SlotMailbox* mb, uint32_t last,
+                       unsigned long long idle_ns) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int G = (int)cluster.num_blocks();
+  const int g = (int)cluster.block_rank();
+  __shared__ int32_t s_alloc[256];
+  __shared__ double s_eps[256];
+  __shared__ uint32_t s_cmd;
+  const int tid = threadIdx.x;
+  const int n_alloc = p.S * p.E, n_eps = p.eps != nullptr ? p.S * p.cap * p.E : 0;
+  for (;;) {
+    if (g == 0) {
+      if (tid == 0) {
+        uint32_t cmd = 0;  // 0: leave
+        const unsigned long long t0 = globaltimer_ns();
+        for (;;) {
+          uint32_t r;
+          asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(r) : "l"(&mb->req_seq) : "memory");
+          if (r != last) {
+            cmd = r;
+            break;
+          }
+          if (mb->quit != 0u) break;
+          if (globaltimer_ns() - t0 > idle_ns) break;
+        }
+        if (cmd != 0u) mb->t_start = globaltimer_ns();
+        s_cmd = cmd;
+      }
+      __syncthreads();
+      // rank 0 alone reads the inputs over PCIe (one round trip), then
+      // hands them and the request to the other CTAs through DSMEM
+      if (s_cmd != 0u) {
+        const volatile int32_t* va = mb->alloc;
+        const volatile double* ve = mb->eps;
+        for (int i = tid; i < n_alloc; i += blockDim.x) s_alloc[i] = va[i];
+        for (int i = tid; i < n_eps; i += blockDim.x) s_eps[i] = ve[i];
+      }
+      __syncthreads();
+      const uint32_t cmd = s_cmd;
+      for (int r = 1; r < G; ++r) {
+        int32_t* ra = cluster.map_shared_rank(s_alloc, r);
+        double* re = cluster.map_shared_rank(s_eps, r);
+        if (cmd != 0u) {
+          for (int i = tid; i < n_alloc; i += blockDim.x) ra[i] = s_alloc[i];
+          for (int i = tid; i < n_eps; i += blockDim.x) re[i] = s_eps[i];
+        }
+        if (tid == 0) *cluster.map_shared_rank(&s_cmd, r) = cmd;
+      }
+    }
+    cluster.sync();
+    const uint32_t cmd = s_cmd;
+    if (cmd == 0u) break;  // cluster-uniform
+    last = cmd;
+    cluster_slot<T, C, true>(p, s_alloc, p.eps != nullptr ? s_eps : nullptr);
+    if (g == 0) {
+      __syncthreads();  // the codebook copy into the mailbox is complete
+      if (tid == 0) {
+        __threadfence_system();
+        mb->t_end = globaltimer_ns();
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(&mb->done_seq), "r"(cmd)
+                     : "memory");
+      }
+    }
+  }
+}
+
+template <typename T, int C>
+int launch_slot_server(const ActorLaunch& p, int G, SlotMailbox* mb, uint32_t last,
+                       unsigned long long idle_ns, cudaStream_t stream) {
+  const size_t smem = (2ull * p.desc.max_rows * C + (size_t)C * 2 * p.E) * sizeof(T);
+  if (smem + 4096 > (size_t)kSmemLimit) return CYR_UNSUPPORTED;
+  auto kern = slot_server_kernel<T, C>;
+  static int configured_smem = -1;
+  if ((int)smem > configured_smem) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return CYR_CUDA_ERROR;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+        cudaSuccess)
+      return CYR_CUDA_ERROR;
+    configured_smem = (int)smem;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(kLatThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, p, mb, last, idle_ns) == cudaSuccess ? CYR_OK
+                                                                             : CYR_CUDA_ERROR;
 }
 
 template <typename T, int C, bool FUSE>
@@ -637,6 +762,213 @@ inline bool single_panel(const ActorDesc& d) {
   return true;
 }
 
+// ------------------------------------------- tiled batch K2, output split
+// Same GEMM chain as actor_tiled_kernel, for actors whose every layer is one
+// panel (<= 256 outputs: cfg1/cfg2's 2x256), with the thread mapping turned
+// so that shared memory stops being the bound.  In actor_tiled_kernel a warp
+// is a column group and its 32 lanes own 256 distinct outputs: every input
+// row costs each warp 1 KB of distinct weight reads (8 shared-memory
+// wavefronts) against 32 FMAs per lane (8 FMA-pipe cycles) — ncu: FMA pipe
+// 41 %, smem-bound.  Here warp w owns outputs [32w, 32w+32) and its lanes
+// are 4 output groups x 8 column groups: a lane's 8 consecutive weights
+// (two LDS.128) are shared by the 8 lanes of its output group and its CPT
+// activations by the 4 lanes of its column group, so one input row costs a
+// warp 2-3 wavefronts for 8*CPT FMAs per lane.  Weights stream straight from
+// the natural Wt [in][out_pad] image (one panel = whole rows).  Every output
+// is still one fp32 FMA chain over k in order, plus the bias, so the logits
+// are bit-identical to actor_tiled_kernel's and the fused kernel's.
+template <typename T, int CPT>
+__global__ void __launch_bounds__(8 * 32 + kTileProducer, 1)
+    actor_osplit_kernel(const ActorLaunch p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int NW = 8;
+  constexpr int kThreads = NW * 32;
+  constexpr int ST = kTileStages;
+  constexpr int TC = 8 * CPT;
+  constexpr int TCP = TC + 16 / (int)sizeof(T);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + ST;
+  unsigned char* ring = smem + 128;
+  T* act_a = reinterpret_cast<T*>(ring + (size_t)ST * kTileStageBytes);
+  T* act_b = act_a + (size_t)p.desc.max_width * TCP;
+  const int tid = threadIdx.x;
+  const int c0 = blockIdx.x * TC;
+  const T* blob = static_cast<const T*>(p.blob);
+  const int nl = p.desc.n_layers;
+
+  if (tid == 0) {
+    for (int st = 0; st < ST; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], NW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (tid >= kThreads) {  // producer warp: whole Wt rows, layer by layer
+    if (tid == kThreads) {
+      int g = 0;
+      for (int l = 0; l < nl; ++l) {
+        const LayerDesc& L = p.desc.layer[l];
+        const int r = max(1, kTileStageBytes / (L.out_pad * (int)sizeof(T)));
+        for (int i0 = 0; i0 < L.in; i0 += r, ++g) {
+          const int buf = g % ST;
+          if (g >= ST) mbar_wait(&empty[buf], (uint32_t)((g / ST - 1) & 1));
+          const uint32_t bytes = (uint32_t)min(r, L.in - i0) * L.out_pad * sizeof(T);
+          mbar_expect_tx(&full[buf], bytes);
+          bulk_g2s(ring + (size_t)buf * kTileStageBytes, blob + L.w_off + (long long)i0 * L.out_pad,
+                   bytes, &full[buf]);
+        }
+      }
+    }
+    return;
+  }
+
+  const int wo = tid >> 5, lane = tid & 31;
+  const int og = lane >> 3, cg = lane & 7;
+  const int in0 = p.desc.layer[0].in;
+  for (int idx = tid; idx < in0 * TC; idx += kThreads) {
+    const int i = idx / TC, c = idx % TC, col = c0 + c;
+    act_a[i * TCP + c] = (T)(col < p.ncols ? column_feature(p, col, i) : 0.0);
+  }
+  consumer_sync<kThreads>();
+
+  T* cur = act_a;
+  T* nxt = act_b;
+  int g = 0;
+  for (int l = 0; l < nl; ++l) {
+    const LayerDesc L = p.desc.layer[l];
+    const int op = L.out_pad;
+    const int rows = max(1, kTileStageBytes / (op * (int)sizeof(T)));
+    const bool last = (l == nl - 1);
+    // narrow layers (the 2E-output head): 8 outputs x 2 columns per thread
+    // over all warps, as in actor_tiled_kernel
+    const bool narrow = op <= 64;
+    const int ogn = (op + 7) / 8;
+    constexpr int kNc = CPT > 1 ? 2 : 1;
+    const int my_og = narrow ? tid % ogn : 0;
+    const int my_c = narrow ? (tid / ogn) * kNc : cg * CPT;
+    const bool active = narrow ? my_c < TC : wo * 32 < L.out;  // warp-uniform when wide
+    auto out_of = [&](int a) { return narrow ? my_og * 8 + a : wo * 32 + og * 8 + a; };
+    T acc[8][CPT];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < CPT; ++b) acc[a][b] = T(0);
+    T bias[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const int o = out_of(a);
+      bias[a] = (active && o < L.out) ? blob[L.b_off + o] : T(0);
+    }
+    for (int i0 = 0; i0 < L.in; i0 += rows, ++g) {
+      const int buf = g % ST;
+      mbar_wait(&full[buf], (uint32_t)((g / ST) & 1));
+      const T* W = reinterpret_cast<const T*>(ring + (size_t)buf * kTileStageBytes);
+      const int nr = min(rows, L.in - i0);
+      if (active && !narrow) {
+        const T* wrow = W + wo * 32 + og * 8;
+        const T* xrow = cur + (size_t)i0 * TCP + cg * CPT;
+#pragma unroll 4
+        for (int r = 0; r < nr; ++r) {
+          T w[8], x[CPT];
+          ld_vec<T, 8>(wrow + (size_t)r * op, w);
+          ld_vec<T, CPT>(xrow + (size_t)r * TCP, x);
+#pragma unroll
+          for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int b = 0; b < CPT; ++b) acc[a][b] = fma(w[a], x[b], acc[a][b]);
+        }
+      } else if (active) {
+#pragma unroll 4
+        for (int r = 0; r < nr; ++r) {
+          T w[8];
+          ld_vec<T, 8>(W + r * op + my_og * 8, w);
+          const T* xr = cur + (size_t)(i0 + r) * TCP + my_c;
+          const T x0 = xr[0], x1 = xr[kNc - 1];
+#pragma unroll
+          for (int a = 0; a < 8; ++a) {
+            acc[a][0] = fma(w[a], x0, acc[a][0]);
+            if constexpr (CPT > 1) acc[a][1] = fma(w[a], x1, acc[a][1]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[buf]);  // this warp is done with the stage
+    }
+    if (active) {
+      const int ncol = narrow ? kNc : CPT;
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        const int o = out_of(a);
+        if (o >= L.out) continue;
+        if constexpr (CPT % 4 == 0 && sizeof(T) == 4) {
+          if (!last && !narrow) {
+#pragma unroll
+          for (int b = 0; b < CPT; b += 4) {
+            float4 v;
+            v.x = (float)(acc[a][b] + bias[a]);
+            v.y = (float)(acc[a][b + 1] + bias[a]);
+            v.z = (float)(acc[a][b + 2] + bias[a]);
+            v.w = (float)(acc[a][b + 3] + bias[a]);
+            v.x = v.x > 0.f ? v.x : 0.f;
+            v.y = v.y > 0.f ? v.y : 0.f;
+            v.z = v.z > 0.f ? v.z : 0.f;
+            v.w = v.w > 0.f ? v.w : 0.f;
+            *reinterpret_cast<float4*>(nxt + (size_t)o * TCP + my_c + b) = v;
+          }
+          continue;
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < CPT; ++b) {
+          if (b >= ncol) break;
+          const T z = acc[a][b] + bias[a];
+          if (!last) {
+            nxt[(size_t)o * TCP + my_c + b] = z > T(0) ? z : T(0);
+          } else {
+            const int col = c0 + my_c + b;
+            if (col < p.ncols) static_cast<T*>(p.raw)[(long long)col * L.out + o] = z;
+          }
+        }
+      }
+    }
+    consumer_sync<kThreads>();
+    T* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+}
+
+template <typename T, int CPT>
+int launch_actor_osplit(const ActorLaunch& p, cudaStream_t stream) {
+  constexpr int TC = 8 * CPT;
+  constexpr int TCP = TC + 16 / (int)sizeof(T);
+  const size_t smem = 128 + (size_t)kTileStages * kTileStageBytes +
+                      2ull * p.desc.max_width * TCP * sizeof(T);
+  if (smem > (size_t)kSmemLimit) return CYR_UNSUPPORTED;
+  auto kern = actor_osplit_kernel<T, CPT>;
+  static int configured = -1;
+  if ((int)smem > configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return CYR_CUDA_ERROR;
+    configured = (int)smem;
+  }
+  const int blocks = (p.ncols + TC - 1) / TC;
+  kern<<<blocks, 8 * 32 + kTileProducer, smem, stream>>>(p);
+  return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
+}
+
+// CYR_TILED_OSPLIT=0 disables the output-split variant (A/B)
+inline bool cyr_osplit_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CYR_TILED_OSPLIT");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
 // largest tile that fits shared memory and still gives every SM a CTA
 template <typename T>
 int launch_actor_tiled_auto(const ActorLaunch& p, int sm_count, cudaStream_t stream) {
@@ -651,6 +983,29 @@ int launch_actor_tiled_auto(const ActorLaunch& p, int sm_count, cudaStream_t str
   if (sizeof(T) == 4 && single_panel(p.desc) && cyr_tiled16_enabled() &&
       (long long)p.ncols >= 96ll * sm_count) {
     const int rc = launch_actor_tiled<T, 96, 12, true>(p, stream);
+    if (rc != CYR_UNSUPPORTED) return rc;
+  }
+  // single-panel actors below the in-place regime (the bench's 1024-slot
+  // Mode-R batch: 4096 columns): the output-split mapping; column tile = the
+  // largest that still gives ~every SM a CTA
+  static const int forced_os = [] {  // CYR_OSPLIT_TC: force its column tile (A/B)
+    const char* e = getenv("CYR_OSPLIT_TC");
+    return e ? atoi(e) : 0;
+  }();
+  if constexpr (sizeof(T) == 4) if (single_panel(p.desc) && cyr_osplit_enabled()) {
+    int tc = 8;
+    for (int cand = 32; cand >= 8; cand >>= 1) {
+      tc = cand;
+      if ((p.ncols + cand - 1) / cand * 5 >= 4ll * sm_count) break;
+    }
+    if (forced_os == 8 || forced_os == 16 || forced_os == 32 || forced_os == 64) tc = forced_os;
+    int rc = CYR_UNSUPPORTED;
+    switch (tc) {
+      case 64: rc = launch_actor_osplit<T, 8>(p, stream); break;
+      case 32: rc = launch_actor_osplit<T, 4>(p, stream); break;
+      case 16: rc = launch_actor_osplit<T, 2>(p, stream); break;
+      default: rc = launch_actor_osplit<T, 1>(p, stream); break;
+    }
     if (rc != CYR_UNSUPPORTED) return rc;
   }
   constexpr int kMax = sizeof(T) == 4 ? 64 : 32;
@@ -855,6 +1210,36 @@ int cyr_launch_slot_fused(int precision, const cyr::ActorDesc& desc, const void*
                 : cyr::launch_actor_cluster<float, 4, true>(p, G, stream, inl);
   return fp64 ? cyr::launch_actor_cluster<double, 8, true>(p, G, stream, inl)
               : cyr::launch_actor_cluster<float, 8, true>(p, G, stream, inl);
+}
+
+int cyr_launch_slot_server(int precision, const cyr::ActorDesc& desc, const void* blob, bool det,
+                           int S, int E, int N, int L, int cap, int32_t* cb,
+                           cyr::SlotMailbox* mb, uint32_t last, unsigned long long idle_ns,
+                           cudaStream_t stream) {
+  if (S <= 0 || S * cap > 8 || S * E > 256 || S * cap * E > 256 || S * (cap + 1) * E > 512 ||
+      E > cyr::kMaxUsers || desc.max_width > cyr::kMaxWidth)
+    return CYR_UNSUPPORTED;
+  cyr::ActorLaunch p{};
+  p.desc = desc;
+  p.blob = blob;
+  p.S = S;
+  p.E = E;
+  p.N = N;
+  p.cap = cap;
+  p.ncols = S * cap;
+  p.eps = det ? nullptr : mb->eps;  // non-null marks the stochastic head (inputs come via smem)
+  p.L = L;
+  p.cb = cb;
+  p.cb_host = mb->cb;
+  p.status = const_cast<int32_t*>(&mb->status);
+  p.trace = cyr_trace_buffer();
+  const int G = cyr_cluster_size();
+  const bool fp64 = precision == CYR_FP64;
+  if (p.ncols <= 4)
+    return fp64 ? cyr::launch_slot_server<double, 4>(p, G, mb, last, idle_ns, stream)
+                : cyr::launch_slot_server<float, 4>(p, G, mb, last, idle_ns, stream);
+  return fp64 ? cyr::launch_slot_server<double, 8>(p, G, mb, last, idle_ns, stream)
+              : cyr::launch_slot_server<float, 8>(p, G, mb, last, idle_ns, stream);
 }
 
 namespace cyr {

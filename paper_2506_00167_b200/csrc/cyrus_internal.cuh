@@ -165,6 +165,23 @@ struct SlotInline {
   double eps[256];
 };
 
+// Persistent single-slot server (the drop-in build_codebook's latency path):
+// one resident 8-CTA cluster polls this mapped host block for requests, so a
+// call costs no kernel launch.  Host-written and device-written fields sit on
+// separate 128-byte lines.
+struct SlotMailbox {
+  volatile uint32_t req_seq;  // host: request number, stored after the inputs
+  volatile uint32_t quit;     // host: leave the polling loop
+  uint32_t pad0[30];
+  volatile uint32_t done_seq;  // device: last request served, stored after cb/status
+  volatile int32_t status;     // device: cyr_status of the last request (host resets it)
+  volatile unsigned long long t_start, t_end;  // device %globaltimer of the last request
+  uint32_t pad1[26];
+  int32_t alloc[256];  // inputs [S][E]
+  double eps[256];     // [S][cap][E]
+  int32_t cb[512];     // output [S][cap+1][E]
+};
+
 struct ActorDesc {
   int n_layers;
   int max_width;          // max over layers of max(in, out_pad)
@@ -184,6 +201,13 @@ int cyr_launch_slot_fused(int precision, const cyr::ActorDesc& desc, const void*
                           const int32_t* alloc, const double* eps, int S, int E, int N, int L,
                           int cap, int32_t* cb, int32_t* cb_host, int32_t* status,
                           cudaStream_t stream, const cyr::SlotInline* inl = nullptr);
+// the persistent server kernel of the fused slot path (mb: device alias of
+// the mapped mailbox; last: the last request already served; it exits on quit
+// or after idle_ns without a request)
+int cyr_launch_slot_server(int precision, const cyr::ActorDesc& desc, const void* blob, bool det,
+                           int S, int E, int N, int L, int cap, int32_t* cb,
+                           cyr::SlotMailbox* mb, uint32_t last, unsigned long long idle_ns,
+                           cudaStream_t stream);
 int cyr_launch_codebook(int precision, const void* raw, const int32_t* alloc, const double* eps,
                         int S, int E, int N, int L, int cap, int32_t* codebook, double* m_hat,
                         double* nu, double* margin, int32_t* iters, int32_t* status,

@@ -102,6 +102,11 @@ class DevicePolicy:
             raise ValueError("actor shape differs from the published policy")
         _native.check(_native.lib().cyr_policy_update(self.handle, blob.ctypes.data), "update")
 
+    def quiesce(self) -> None:
+        """Stop the resident single-slot server kernel now (it also leaves by
+        itself after 20 ms idle); the next drop-in call relaunches it."""
+        _native.check(_native.lib().cyr_policy_quiesce(self.handle), "quiesce")
+
     def close(self) -> None:
         if getattr(self, "_h", None) is not None:
             try:

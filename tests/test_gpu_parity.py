@@ -213,6 +213,36 @@ def test_wide_fp32_gemm_path_bit_identical_to_fused_kernel(golden):
     pol.close()
 
 
+def test_single_panel_fp32_paths_bit_identical(golden):
+    """A single-panel fp32 actor (cfg2, 2x256) takes, by batch size, the
+    output-split tiled kernel (8- and 32-column tiles), the 12-warp in-place
+    tiled kernel (>= 96 columns per SM) and the layer-GEMM path (>= 65,536
+    columns).  Every output is the same fp32 FMA chain over k plus the bias,
+    so the logits of shared columns are bit-identical across all of them."""
+    from paper_2506_00167_b200 import _native
+    cfg = golden.config("cfg2")
+    agent = cfg.agent()
+    pol = DevicePolicy(agent.actor, "fp32")
+    cap, e = cfg.meta["cap"], cfg.meta["num_embb"]
+    base = cfg["alloc"]
+    sizes = (256, 1024, 4000, 17500)  # 1,024 / 4,096 / 16,000 / 70,000 columns
+    alloc = np.concatenate([base] * (sizes[-1] // len(base) + 1))[:sizes[-1]]
+    alloc_d = torch.from_numpy(np.ascontiguousarray(alloc)).cuda()
+    out = {}
+    for s in sizes:
+        raw = torch.empty((s * cap, 2 * e), dtype=torch.float32, device="cuda")
+        _native.check(_native.lib().cyr_actor_forward_device(
+            pol.handle, alloc_d.data_ptr(), s, cfg.meta["total_scs"], cap, raw.data_ptr(),
+            _native.stream_handle()))
+        out[s] = raw.cpu().numpy()
+    for s in sizes[1:]:
+        assert np.array_equal(out[sizes[0]], out[s][: sizes[0] * cap]), s
+    got = out[sizes[1]][: len(base) * cap].astype(np.float64).reshape(len(base), cap, 2 * e)
+    want = np.transpose(cfg["det/raw"], (0, 2, 1))
+    assert float((np.abs(got - want) / np.abs(want).max(axis=2, keepdims=True)).max()) <= 1e-5
+    pol.close()
+
+
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 @pytest.mark.parametrize("name", CONFIGS)
 @pytest.mark.parametrize("mode", ["det", "sto"])
@@ -284,6 +314,38 @@ def test_single_slot_fused_path(golden, name, precision):
                       None if mode == "det" else torch.from_numpy(cfg["eps"][:per_call]).cuda())
         eng.check()
         del sub
+
+
+def test_slot_server_idle_exit_relaunch_and_interleaving(golden):
+    """The single-slot path runs on a resident server kernel that leaves after
+    20 ms without requests; calls after an idle exit, after a det/sto switch
+    (server restart), around batch work on other streams and around a
+    device-wide synchronize must all return the reference's codebooks."""
+    import time
+    cfg = golden.config("cfg2")
+    agent = cfg.agent()
+    pol = DevicePolicy(agent.actor, "fp32")
+    got = {"det": [], "sto": []}
+    for s in range(12):
+        mode = "det" if s % 3 == 0 else "sto"
+        eps = None if mode == "det" else cfg["eps"][s:s + 1]
+        books, dev_ns = build_codebooks_host(pol, cfg.cell, cfg["alloc"][s:s + 1], eps)
+        assert 0 < dev_ns < 10_000_000
+        got[mode].append((s, books[0]))
+        if s == 4:
+            time.sleep(0.06)               # the server idles out
+        if s == 7:                         # batch work + a device-wide sync meanwhile
+            eng = CodebookEngine(pol, cfg.cell, max_slots=64, with_tree=True)
+            eng.run(torch.from_numpy(cfg["alloc"][:8]).cuda())
+            torch.cuda.synchronize()
+            eng.check()
+    for mode, rows in got.items():
+        flagged = _near_tie_rows(cfg, mode, NEAR_TIE["fp32"])
+        want = cfg[f"{mode}/codebook"]
+        for s, book in rows:
+            for j in np.nonzero((book[1:] != want[s][1:]).any(axis=1))[0]:
+                assert (s, int(j)) in flagged, f"{mode}: slot {s} branch {j + 1}"
+    pol.close()
 
 
 def test_cluster_actor_logits(golden):
