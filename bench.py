@@ -398,7 +398,7 @@ def run_ours(args, rank, world, local_rank):
                         + cell.num_branches * cell.num_embb * 8
                         + (cell.num_branches + 1) * cell.num_embb * 4)
     kernels = [
-        {"kernel": "K2 actor_tiled_kernel (fp32 SIMT, 4096 branch columns)", "bound": "fma",
+        {"kernel": "K2 actor_osplit_kernel (fp32 SIMT tiled, output-split warps, 4096 branch columns)", "bound": "fma",
          "ms": actor_ms, "achieved": k2_flops / (actor_ms * 1e-3) / 1e12, "peak": fma_peak,
          "unit": "TFLOP/s", "frac": k2_flops / (actor_ms * 1e-3) / 1e12 / fma_peak,
          "peak_source": "spec: 148 SMs x 128 FP32 lanes x 2 x 1965 MHz",

@@ -267,10 +267,15 @@ __device__ __forceinline__ void cluster_slot(const ActorLaunch& p, const int32_t
     const T* cur = (l & 1) ? act1 : act0;
     T* nxt = (l & 1) ? act0 : act1;
     const bool last = l == nl - 1;
+    // FUSE: the narrow head layer runs on rank 0 alone, which holds every
+    // input already: no DSMEM gather and no cluster barrier after it
+    const bool solo = FUSE && last;
+    if (solo && g != 0) break;
+    const int Gl = solo ? 1 : G, gl = solo ? 0 : g;
     const T* W = blob + L.wr_off;
     const int nvec = L.in_pad / V;
-    const int stride = G * nwarps;  // outputs are dealt round-robin: rank, then warp
-    for (int o0 = g + G * warp; o0 < L.out; o0 += stride * kLatOW) {
+    const int stride = Gl * nwarps;  // outputs are dealt round-robin: rank, then warp
+    for (int o0 = gl + Gl * warp; o0 < L.out; o0 += stride * kLatOW) {
       T acc[kLatOW][C];
 #pragma unroll
       for (int k = 0; k < kLatOW; ++k)
@@ -298,7 +303,7 @@ __device__ __forceinline__ void cluster_slot(const ActorLaunch& p, const int32_t
             for (int c = 0; c < C; ++c) acc[k][c] = fma(w[k][q], x[c], acc[k][c]);
         }
       }
-      if (o0 == g + G * warp) trace_stamp(tr, 24 + 2 * l);
+      if (o0 == gl + Gl * warp) trace_stamp(tr, 24 + 2 * l);
 #pragma unroll
       for (int k = 0; k < kLatOW; ++k)
 #pragma unroll
@@ -312,7 +317,7 @@ __device__ __forceinline__ void cluster_slot(const ActorLaunch& p, const int32_t
         if (o >= L.out) continue;  // warp-uniform
         const T bias = blob[L.b_off + o];
         if (last) {
-          T* raw = FUSE ? cluster.map_shared_rank(raw_s, 0) : static_cast<T*>(p.raw);
+          T* raw = FUSE ? raw_s : static_cast<T*>(p.raw);
 #pragma unroll
           for (int c = 0; c < C; ++c)
             if (lane == c && c < p.ncols) raw[(long long)c * L.out + o] = acc[k][c] + bias;
@@ -332,7 +337,10 @@ __device__ __forceinline__ void cluster_slot(const ActorLaunch& p, const int32_t
       }
     }
     trace_stamp(tr, 25 + 2 * l);
-    cluster.sync();
+    if (solo)
+      __syncthreads();
+    else
+      cluster.sync();
     trace_stamp(tr, 2 + l);
   }
   if constexpr (FUSE) {
