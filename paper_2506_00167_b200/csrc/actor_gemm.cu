@@ -64,6 +64,36 @@ __global__ void __launch_bounds__(256) gemm_features_kernel(const ActorLaunch p,
   }
 }
 
+// The same X0, one thread per column group (the cap branch columns of one
+// slot or Mode-T parent): every feature but k/cap is shared by the group, so
+// it is evaluated once per group instead of once per column (the element
+// kernel above spends its time on per-element index decoding); each thread
+// writes its cap consecutive columns, a warp 32*cap contiguous floats per
+// feature row.  Same float64 expressions (column_feature), same bits.
+__global__ void __launch_bounds__(256) gemm_features_group_kernel(const ActorLaunch p, float* X,
+                                                                  int ldx, int kpad) {
+  const int cap = p.cap;
+  const long long groups = (ldx + cap - 1) / cap;
+  const int in0 = p.desc.layer[0].in;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < groups;
+       g += (long long)gridDim.x * blockDim.x) {
+    const long long c0 = g * cap;
+    const bool live = c0 < p.ncols;
+    for (int i = 0; i < kpad; ++i) {
+      float* row = X + (long long)i * ldx + c0;
+      const bool shared = i != p.E;
+      const float v = (live && i < in0 && shared) ? (float)column_feature(p, (int)c0, i) : 0.f;
+      for (int k = 0; k < cap; ++k) {
+        const long long col = c0 + k;
+        if (col >= ldx) break;
+        float x = 0.f;
+        if (col < p.ncols && i < in0) x = shared ? v : (float)column_feature(p, (int)col, i);
+        row[k] = x;
+      }
+    }
+  }
+}
+
 // One layer: K rows of X (K a multiple of 16 within ldx's allocation), Wt
 // [K_w][ldw] (rows >= K_w read as zero), out outputs.  CTA tile BM outputs
 // x BN columns, 8 warps as (BM/32) x (BN/64).
@@ -119,8 +149,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
     cp_async_commit();
     const float* As = gsm + (kt % kGemmStages) * SF;
     const float* Bs = As + kGemmBK * BM;
-#pragma unroll
-    for (int kk = 0; kk < kGemmBK; ++kk) {
+    auto kstep = [&](int kk) {
       const float4 a0 = *reinterpret_cast<const float4*>(As + kk * BM + ob);
       const float4 a1 = *reinterpret_cast<const float4*>(As + kk * BM + ob + 16);
       const float4 b0 = *reinterpret_cast<const float4*>(Bs + kk * BN + cb);
@@ -131,6 +160,17 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
       for (int a = 0; a < 8; ++a)
 #pragma unroll
         for (int b = 0; b < 8; ++b) acc[a][b] = fmaf(w[a], x[b], acc[a][b]);
+    };
+    const int kk_end = Kw - kt * kGemmBK;  // the weight rows that exist
+    if (kk_end >= kGemmBK) {
+#pragma unroll
+      for (int kk = 0; kk < kGemmBK; ++kk) kstep(kk);
+    } else {
+      // zero-padded K rows (the first layer's K = 3E+3 -> multiple of 16) are
+      // skipped: their weights and inputs are 0, and adding fmaf(0, x, acc)
+      // is the identity (acc is never -0), so the bits are unchanged
+#pragma unroll 1
+      for (int kk = 0; kk < kk_end; ++kk) kstep(kk);
     }
   }
   cp_async_wait<0>();
@@ -231,7 +271,13 @@ int cyr_launch_actor_gemm(const cyr::ActorLaunch& p, void* workspace, cudaStream
   {
     const long long n = (long long)k0pad * ldx;
     const int blocks = (int)std::min<long long>((n + 255) / 256, 148ll * 16);
-    gemm_features_kernel<<<blocks, 256, 0, stream>>>(p, buf[0], ldx, k0pad);
+    if (p.x == nullptr && p.kcol == nullptr && p.cap >= 1) {
+      const long long groups = (ldx + p.cap - 1) / p.cap;
+      const int gblocks = (int)std::min<long long>((groups + 255) / 256, 148ll * 16);
+      gemm_features_group_kernel<<<gblocks, 256, 0, stream>>>(p, buf[0], ldx, k0pad);
+    } else {
+      gemm_features_kernel<<<blocks, 256, 0, stream>>>(p, buf[0], ldx, k0pad);
+    }
   }
   int cur = 0;
   for (int l = 0; l < p.desc.n_layers; ++l) {
