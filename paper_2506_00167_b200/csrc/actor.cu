@@ -849,15 +849,19 @@ __global__ void __launch_bounds__(8 * 32 + kTileProducer, 1)
     const int op = L.out_pad;
     const int rows = max(1, kTileStageBytes / (op * (int)sizeof(T)));
     const bool last = (l == nl - 1);
-    // narrow layers (the 2E-output head): 8 outputs x 2 columns per thread
-    // over all warps, as in actor_tiled_kernel
+    // narrow layers (the 2E-output head): 4 outputs x 1 column per thread
+    // when that fits the CTA (5 x 32 threads for the 20-logit head: 5 warps
+    // instead of 1.5), else 8 outputs x 2 columns as in actor_tiled_kernel
     const bool narrow = op <= 64;
-    const int ogn = (op + 7) / 8;
+    const int ogn4 = (op + 3) / 4;
+    const bool n4 = narrow && ogn4 * TC <= kThreads;
+    const int ogn = n4 ? ogn4 : (op + 7) / 8;
     constexpr int kNc = CPT > 1 ? 2 : 1;
+    const int na = n4 ? 4 : 8;  // outputs per thread
     const int my_og = narrow ? tid % ogn : 0;
-    const int my_c = narrow ? (tid / ogn) * kNc : cg * CPT;
+    const int my_c = narrow ? (n4 ? tid / ogn : (tid / ogn) * kNc) : cg * CPT;
     const bool active = narrow ? my_c < TC : wo * 32 < L.out;  // warp-uniform when wide
-    auto out_of = [&](int a) { return narrow ? my_og * 8 + a : wo * 32 + og * 8 + a; };
+    auto out_of = [&](int a) { return narrow ? my_og * na + a : wo * 32 + og * 8 + a; };
     T acc[8][CPT];
 #pragma unroll
     for (int a = 0; a < 8; ++a)
@@ -867,7 +871,7 @@ __global__ void __launch_bounds__(8 * 32 + kTileProducer, 1)
 #pragma unroll
     for (int a = 0; a < 8; ++a) {
       const int o = out_of(a);
-      bias[a] = (active && o < L.out) ? blob[L.b_off + o] : T(0);
+      bias[a] = (active && a < na && o < L.out) ? blob[L.b_off + o] : T(0);
     }
     for (int i0 = 0; i0 < L.in; i0 += rows, ++g) {
       const int buf = g % ST;
@@ -887,6 +891,17 @@ __global__ void __launch_bounds__(8 * 32 + kTileProducer, 1)
 #pragma unroll
             for (int b = 0; b < CPT; ++b) acc[a][b] = fma(w[a], x[b], acc[a][b]);
         }
+      } else if (active && n4) {
+        const T* wrow = W + my_og * 4;
+        const T* xrow = cur + (size_t)i0 * TCP + my_c;
+#pragma unroll 8
+        for (int r = 0; r < nr; ++r) {
+          T w[4];
+          ld_vec<T, 4>(wrow + (size_t)r * op, w);
+          const T x0 = xrow[(size_t)r * TCP];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) acc[a][0] = fma(w[a], x0, acc[a][0]);
+        }
       } else if (active) {
 #pragma unroll 4
         for (int r = 0; r < nr; ++r) {
@@ -905,11 +920,11 @@ __global__ void __launch_bounds__(8 * 32 + kTileProducer, 1)
       if (lane == 0) mbar_arrive(&empty[buf]);  // this warp is done with the stage
     }
     if (active) {
-      const int ncol = narrow ? kNc : CPT;
+      const int ncol = narrow ? (n4 ? 1 : kNc) : CPT;
 #pragma unroll
       for (int a = 0; a < 8; ++a) {
         const int o = out_of(a);
-        if (o >= L.out) continue;
+        if (a >= na || o >= L.out) continue;
         if constexpr (CPT % 4 == 0 && sizeof(T) == 4) {
           if (!last && !narrow) {
 #pragma unroll

@@ -4,5 +4,5 @@ mkdir -p gpurun_out
 k2() { timeout 300 env "$@" python bench.py --steps 10 --warmup 3 --latency-slots 20 --no-mode-t 2>/dev/null | python -c "
 import json,sys; d=json.loads(sys.stdin.read()); k=d['kernels'][0]; print(round(k['ms']*1e3,1), 'us', round(k['frac'],3), 'of FMA peak; value', round(d['value']))"; }
 echo "old mapping:      $(k2 CYR_TILED_OSPLIT=0)"
-for tc in 8 16 32 64; do echo "osplit TC=$tc: $(k2 CYR_OSPLIT_TC=$tc)"; done
+for tc in ${TCS:-32}; do echo "osplit TC=$tc: $(k2 CYR_OSPLIT_TC=$tc)"; done
 echo "osplit default:   $(k2 CYR_X=1)"
