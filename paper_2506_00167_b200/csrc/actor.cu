@@ -694,10 +694,14 @@ __global__ void __launch_bounds__(NW * 32 + kTileProducer, 1)
               for (int u = 0; u < V; ++u) w[c * V + u] = t[u];
             }
             ld_vec<T, CPT>(cur + (size_t)(i0 + r) * TCP + cg * CPT, x);
+            if constexpr (INPLACE) {  // 13 warps: registers capped at 128, FFMA2 pairs would spill
 #pragma unroll
-            for (int a = 0; a < 8; ++a)
+              for (int a = 0; a < 8; ++a)
 #pragma unroll
-              for (int b = 0; b < CPT; ++b) acc[a][b] = fma(w[a], x[b], acc[a][b]);
+                for (int b = 0; b < CPT; ++b) acc[a][b] = fma(w[a], x[b], acc[a][b]);
+            } else {
+              fma_tile_row<CPT>(acc, w, x);
+            }
           }
         } else if (active) {
 #pragma unroll 4
@@ -886,10 +890,7 @@ __global__ void __launch_bounds__(8 * 32 + kTileProducer, 1)
           T w[8], x[CPT];
           ld_vec<T, 8>(wrow + (size_t)r * op, w);
           ld_vec<T, CPT>(xrow + (size_t)r * TCP, x);
-#pragma unroll
-          for (int a = 0; a < 8; ++a)
-#pragma unroll
-            for (int b = 0; b < CPT; ++b) acc[a][b] = fma(w[a], x[b], acc[a][b]);
+          fma_tile_row<CPT>(acc, w, x);
         }
       } else if (active && n4) {
         const T* wrow = W + my_og * 4;

@@ -66,6 +66,59 @@ __device__ __forceinline__ double mode_t_feature(const ActorLaunch& p, int col, 
   return (double)(p.tau - 1) / (double)p.M;
 }
 
+// Packed fp32 pairs for FFMA2 (sm_100: fma.rn.f32x2, two IEEE fma.rn per
+// instruction, so each lane's result is bit-identical to fmaf): the SIMT
+// actor kernels are issue-bound, and one FFMA2 with a broadcast scalar
+// operand (ptxas folds {a, a} into the instruction) issues two FMAs.
+__device__ __forceinline__ unsigned long long f32x2_pack(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 f32x2_unpack(unsigned long long v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return make_float2(lo, hi);
+}
+// acc.{lo,hi} = fma(a, b.{lo,hi}, acc.{lo,hi})
+__device__ __forceinline__ void ffma2_bcast(unsigned long long& acc, float a, unsigned long long b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(f32x2_pack(a, a)), "l"(b));
+}
+
+// One input row of an 8-output x NC-column register tile:
+// acc[a][b] = fma(w[a], x[b], acc[a][b]); fp32 column pairs go through FFMA2.
+template <int NC>
+__device__ __forceinline__ void fma_tile_row(float (&acc)[8][NC], const float (&w)[8],
+                                             const float (&x)[NC]) {
+  if constexpr (NC % 2 == 0) {
+#pragma unroll
+    for (int q = 0; q < NC / 2; ++q) {
+      const unsigned long long xq = f32x2_pack(x[2 * q], x[2 * q + 1]);
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        unsigned long long c = f32x2_pack(acc[a][2 * q], acc[a][2 * q + 1]);
+        ffma2_bcast(c, w[a], xq);
+        const float2 v = f32x2_unpack(c);
+        acc[a][2 * q] = v.x;
+        acc[a][2 * q + 1] = v.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < NC; ++b) acc[a][b] = fmaf(w[a], x[b], acc[a][b]);
+  }
+}
+template <int NC>
+__device__ __forceinline__ void fma_tile_row(double (&acc)[8][NC], const double (&w)[8],
+                                             const double (&x)[NC]) {
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < NC; ++b) acc[a][b] = fma(w[a], x[b], acc[a][b]);
+}
+
 // Input feature i of batch column col, float64 (rounded to the actor's
 // precision by the caller):
 //   explicit x [col][in]                                      (any MLP)

@@ -17,7 +17,8 @@
 // logits as raw[col][out].
 //
 // Tile: 256 threads, 8 warps as 4 (outputs) x 2 (columns); a thread owns 8
-// outputs x 8 columns (64 accumulators), both split as {+0..3, +16/32..}
+// outputs x 8 columns (64 accumulators, packed in column pairs: 32 FFMA2 per
+// k instead of 64 FFMA — the kernel is issue-bound), both split as {+0..3, +16/32..}
 // so each of its four LDS.128 per k reads, across the warp, contiguous
 // 16-byte chunks (one shared-memory wavefront each).  K advances in 16-row
 // stages through a 3-deep cp.async ring (16 KB per stage), 2 CTAs per SM.
@@ -130,11 +131,12 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
     }
   };
 
-  float acc[8][8];
+  // accumulators as packed column pairs (FFMA2): acc2[a][q] = columns 2q, 2q+1
+  unsigned long long acc2[8][4];
 #pragma unroll
   for (int a = 0; a < 8; ++a)
 #pragma unroll
-    for (int b = 0; b < 8; ++b) acc[a][b] = 0.f;
+    for (int q = 0; q < 4; ++q) acc2[a][q] = 0ull;
 
   const int KT = K / kGemmBK;
 #pragma unroll
@@ -155,11 +157,12 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
       const float4 b0 = *reinterpret_cast<const float4*>(Bs + kk * BN + cb);
       const float4 b1 = *reinterpret_cast<const float4*>(Bs + kk * BN + cb + 32);
       const float w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float x[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      const unsigned long long x2[4] = {f32x2_pack(b0.x, b0.y), f32x2_pack(b0.z, b0.w),
+                                        f32x2_pack(b1.x, b1.y), f32x2_pack(b1.z, b1.w)};
 #pragma unroll
       for (int a = 0; a < 8; ++a)
 #pragma unroll
-        for (int b = 0; b < 8; ++b) acc[a][b] = fmaf(w[a], x[b], acc[a][b]);
+        for (int q = 0; q < 4; ++q) ffma2_bcast(acc2[a][q], w[a], x2[q]);
     };
     const int kk_end = Kw - kt * kGemmBK;  // the weight rows that exist
     if (kk_end >= kGemmBK) {
@@ -174,6 +177,15 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
     }
   }
   cp_async_wait<0>();
+  float acc[8][8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 v = f32x2_unpack(acc2[a][q]);
+      acc[a][2 * q] = v.x;
+      acc[a][2 * q + 1] = v.y;
+    }
 
   // epilogue: + bias (then ReLU); hidden -> Y[o][col], last -> raw[col][o]
 #pragma unroll
