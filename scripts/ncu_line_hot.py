@@ -11,14 +11,18 @@ cur = None
 samples = defaultdict(float)
 execd = defaultdict(float)
 text = {}
+fname = ""
 for r in rows:
+    if r and r[0] == "File Path":
+        fname = r[1].rsplit("/", 1)[-1]
+        continue
     if r and r[0] == "Line No":
         hdr = r
         continue
     if hdr is None or len(r) < 8:
         continue
     if r[0] not in ("", "-"):
-        cur = r[0]
+        cur = f"{fname}:{r[0]}"
         text[cur] = r[1]
         continue
     try:
@@ -29,4 +33,4 @@ for r in rows:
 tot = sum(samples.values())
 print(f"total samples {tot:.0f}")
 for line, v in sorted(samples.items(), key=lambda kv: -kv[1])[:top]:
-    print(f"{v:7.0f} {100*v/tot:5.1f}% exec {execd[line]:8.0f}  L{line}: {text.get(line,'')[:90]}")
+    print(f"{v:7.0f} {100*v/tot:5.1f}% exec {execd[line]:8.0f}  {line}: {text.get(line,'')[:90]}")
