@@ -54,7 +54,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         o = os.path.join(BUILD, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            jobs.append([nvcc, *ARCH, *FLAGS, "-c", s, "-o", o])
+            # CYR_NVCC_EXTRA: extra nvcc flags for A/B builds (e.g. -DNAME=VALUE)
+            extra = os.environ.get("CYR_NVCC_EXTRA", "").split()
+            jobs.append([nvcc, *ARCH, *FLAGS, *extra, "-c", s, "-o", o])
 
     def run(cmd):
         res = subprocess.run(cmd, capture_output=True, text=True)
