@@ -348,6 +348,26 @@ def test_slot_server_idle_exit_relaunch_and_interleaving(golden):
     pol.close()
 
 
+def test_slot_servers_of_two_policies_interleaved(golden):
+    """Two policies, each with its own resident slot server (two 8-CTA
+    clusters at once), called alternately: every codebook still matches the
+    reference, and closing one policy stops only its server."""
+    cfgs = [golden.config("cfg1"), golden.config("cfg2")]
+    pols = [DevicePolicy(c.agent().actor, "fp32") for c in cfgs]
+    for s in range(6):
+        for cfg, pol in zip(cfgs, pols):
+            books, _ = build_codebooks_host(pol, cfg.cell, cfg["alloc"][s:s + 1], cfg["eps"][s:s + 1])
+            want = cfg["sto/codebook"][s]
+            flagged = _near_tie_rows(cfg, "sto", NEAR_TIE["fp32"])
+            for j in np.nonzero((books[0][1:] != want[1:]).any(axis=1))[0]:
+                assert (s, int(j)) in flagged, f"{cfg.name}: slot {s} branch {j + 1}"
+    pols[0].close()
+    cfg = cfgs[1]
+    books, _ = build_codebooks_host(pols[1], cfg.cell, cfg["alloc"][:1], cfg["eps"][:1])
+    assert (books[0][0] == 0).all()
+    pols[1].close()
+
+
 def test_cluster_actor_logits(golden):
     from paper_2506_00167_b200 import _native
     for name in ("cfg1", "cfg2", "cfg5"):
