@@ -676,6 +676,40 @@ def test_mode_t_e32_matches_oracle():
     pol.close()
 
 
+@pytest.mark.parametrize("users,precision", [(5, "fp32"), (7, "fp64"), (1, "fp32")])
+def test_mode_t_odd_users_matches_oracle(users, precision):
+    """Odd E: packed node records carry one zero padding lane (Ep = E + 1).
+    Four slots at M = 5 (10,000 rows at the deepest level) exercise the warp-
+    and the lane-mapped K3 level kernels and both feature builders."""
+    from oracle import mode_t
+    from paper_2506_00167_b200 import substream
+    from paper_2506_00167_b200.core import CellConfig
+    rng = np.random.default_rng(users)
+    slots, minislots = 4, 5
+    cell = CellConfig(total_scs=120, num_embb=users, urllc_sc_len=30, minislots=minislots,
+                      rb_size=12)
+    cap = cell.num_branches
+    owners = rng.integers(0, users, size=(slots, 10))
+    allocs = np.stack([np.bincount(o, minlength=users) * 12 for o in owners]).astype(np.int32)
+    mcs = rng.integers(0, 6, size=(slots, users)).astype(np.int32)
+    eps = rng.standard_normal((slots, cap, users))
+    actor = tree.make_mode_t_actor(cell, (64, 64), substream(users, "mode-t"), final_scale=1.0)
+    pol = DevicePolicy(actor, precision)
+    got = tree.build_tree_mode_t(pol, cell, torch.from_numpy(allocs).cuda(),
+                                 torch.from_numpy(mcs).cuda(),
+                                 torch.from_numpy(eps).cuda()).cpu().numpy()
+    assert got.shape[2] == users + (users & 1)
+    assert (got[:, :, users:] == 0).all()
+    for s in range(slots):
+        want, margins = mode_t.mode_t_tree(actor.weights, actor.biases, allocs[s], mcs[s],
+                                           cell.total_scs, cell.urllc_sc_len, minislots, eps[s],
+                                           details=True)
+        taint = _taint(margins, cap, NEAR_TIE[precision])
+        diff = (got[s, :, :users] != want).any(axis=1)
+        assert not (diff & ~taint).any(), f"slot {s}: nodes differ outside near-tie subtrees"
+    pol.close()
+
+
 def test_codebook_stream_matches_engine(golden):
     """CodebookStream (two batches in flight, double-buffered, separate
     streams for K1) returns every batch's codebooks exactly as the one-shot
