@@ -25,6 +25,7 @@
 #include "actor_common.cuh"
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 
 namespace cyr {
@@ -98,12 +99,19 @@ __global__ void __launch_bounds__(256) gemm_features_group_kernel(const ActorLau
 // One layer: K rows of X (K a multiple of 16 within ldx's allocation), Wt
 // [K_w][ldw] (rows >= K_w read as zero), out outputs.  CTA tile BM outputs
 // x BN columns, 8 warps as (BM/32) x (BN/64).
-template <int BM, int BN, bool LAST>
+//
+// OPT < 8 (the narrow head, BM = 32, out <= 4*OPT): a thread owns OPT
+// consecutive outputs oy*OPT + {0..OPT-1} instead of 8 interleaved ones, so a
+// 2E = 20-logit head runs 5 outputs per thread with no padded rows (the 8-row
+// mapping spent 37.5 % of its FMAs on rows 20..31).  Same FMA chain per
+// output, same bits.
+template <int BM, int BN, bool LAST, int OPT = 8>
 __global__ void __launch_bounds__(kGemmThreads, 2)
     sgemm_layer_kernel(const float* __restrict__ Wt, int ldw, int Kw, const float* __restrict__ bias,
                        const float* __restrict__ X, int ldx, int K, int out,
                        float* __restrict__ Y, int ldy, float* __restrict__ raw, int ncols) {
   static_assert((BM / 32) * (BN / 64) == kGemmThreads / 32, "8 warps");
+  static_assert(OPT == 8 || (BM == 32 && LAST), "compact outputs: head only");
   constexpr int SF = stage_floats<BM, BN>();
   extern __shared__ __align__(16) float gsm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -152,17 +160,31 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
     const float* As = gsm + (kt % kGemmStages) * SF;
     const float* Bs = As + kGemmBK * BM;
     auto kstep = [&](int kk) {
-      const float4 a0 = *reinterpret_cast<const float4*>(As + kk * BM + ob);
-      const float4 a1 = *reinterpret_cast<const float4*>(As + kk * BM + ob + 16);
-      const float4 b0 = *reinterpret_cast<const float4*>(Bs + kk * BN + cb);
-      const float4 b1 = *reinterpret_cast<const float4*>(Bs + kk * BN + cb + 32);
-      const float w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const unsigned long long x2[4] = {f32x2_pack(b0.x, b0.y), f32x2_pack(b0.z, b0.w),
-                                        f32x2_pack(b1.x, b1.y), f32x2_pack(b1.z, b1.w)};
+      if constexpr (OPT == 8) {
+        const float4 a0 = *reinterpret_cast<const float4*>(As + kk * BM + ob);
+        const float4 a1 = *reinterpret_cast<const float4*>(As + kk * BM + ob + 16);
+        const float4 b0 = *reinterpret_cast<const float4*>(Bs + kk * BN + cb);
+        const float4 b1 = *reinterpret_cast<const float4*>(Bs + kk * BN + cb + 32);
+        const float w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const unsigned long long x2[4] = {f32x2_pack(b0.x, b0.y), f32x2_pack(b0.z, b0.w),
+                                          f32x2_pack(b1.x, b1.y), f32x2_pack(b1.z, b1.w)};
 #pragma unroll
-      for (int a = 0; a < 8; ++a)
+        for (int a = 0; a < 8; ++a)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) ffma2_bcast(acc2[a][q], w[a], x2[q]);
+          for (int q = 0; q < 4; ++q) ffma2_bcast(acc2[a][q], w[a], x2[q]);
+      } else {
+        const float4 b0 = *reinterpret_cast<const float4*>(Bs + kk * BN + cb);
+        const float4 b1 = *reinterpret_cast<const float4*>(Bs + kk * BN + cb + 32);
+        const unsigned long long x2[4] = {f32x2_pack(b0.x, b0.y), f32x2_pack(b0.z, b0.w),
+                                          f32x2_pack(b1.x, b1.y), f32x2_pack(b1.z, b1.w)};
+        float w[OPT];
+#pragma unroll
+        for (int a = 0; a < OPT; ++a) w[a] = As[kk * BM + oy * OPT + a];
+#pragma unroll
+        for (int a = 0; a < OPT; ++a)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) ffma2_bcast(acc2[a][q], w[a], x2[q]);
+      }
     };
     const int kk_end = Kw - kt * kGemmBK;  // the weight rows that exist
     if (kk_end >= kGemmBK) {
@@ -189,8 +211,8 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
 
   // epilogue: + bias (then ReLU); hidden -> Y[o][col], last -> raw[col][o]
 #pragma unroll
-  for (int a = 0; a < 8; ++a) {
-    const int o = o0 + ob + (a < 4 ? a : 12 + a);
+  for (int a = 0; a < OPT; ++a) {
+    const int o = (OPT == 8) ? o0 + ob + (a < 4 ? a : 12 + a) : o0 + oy * OPT + a;
     if (o >= out) {  // hidden: rows out..roundup16(out) are the next layer's K padding
       if (!LAST && o < ((out + 15) & ~15))
 #pragma unroll
@@ -251,12 +273,12 @@ size_t cyr_gemm_workspace_bytes(const cyr::ActorDesc& desc, long long ncols) {
 }
 
 namespace {
-template <int BM, int BN, bool LAST>
+template <int BM, int BN, bool LAST, int OPT = 8>
 int launch_layer(const float* Wt, int ldw, int Kw, const float* bias, const float* X, int ldx, int K,
                  int out, float* Y, float* raw, int ncols, cudaStream_t stream) {
   using namespace cyr;
   constexpr size_t smem = (size_t)kGemmStages * stage_floats<BM, BN>() * sizeof(float);
-  auto kern = sgemm_layer_kernel<BM, BN, LAST>;
+  auto kern = sgemm_layer_kernel<BM, BN, LAST, OPT>;
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
@@ -299,15 +321,29 @@ int cyr_launch_actor_gemm(const cyr::ActorLaunch& p, void* workspace, cudaStream
     const float* W = blob + L.w_off;
     const float* b = blob + L.b_off;
     int rc;
-    if (last && L.out <= kHeadBM)
-      rc = launch_layer<kHeadBM, kHeadBN, true>(W, L.out_pad, L.in, b, buf[cur], ldx, K, L.out,
-                                                nullptr, static_cast<float*>(p.raw), p.ncols, stream);
-    else if (last)
+    if (last && L.out <= kHeadBM) {
+      auto head = [&](auto opt) {
+        return launch_layer<kHeadBM, kHeadBN, true, decltype(opt)::value>(
+            W, L.out_pad, L.in, b, buf[cur], ldx, K, L.out, nullptr, static_cast<float*>(p.raw),
+            p.ncols, stream);
+      };
+      switch ((L.out + 3) / 4) {  // outputs per thread, no padded rows
+        case 1: rc = head(std::integral_constant<int, 1>{}); break;
+        case 2: rc = head(std::integral_constant<int, 2>{}); break;
+        case 3: rc = head(std::integral_constant<int, 3>{}); break;
+        case 4: rc = head(std::integral_constant<int, 4>{}); break;
+        case 5: rc = head(std::integral_constant<int, 5>{}); break;
+        case 6: rc = head(std::integral_constant<int, 6>{}); break;
+        case 7: rc = head(std::integral_constant<int, 7>{}); break;
+        default: rc = head(std::integral_constant<int, 8>{}); break;
+      }
+    } else if (last) {
       rc = launch_layer<kGemmBM, kGemmBN, true>(W, L.out_pad, L.in, b, buf[cur], ldx, K, L.out,
                                                 nullptr, static_cast<float*>(p.raw), p.ncols, stream);
-    else
+    } else {
       rc = launch_layer<kGemmBM, kGemmBN, false>(W, L.out_pad, L.in, b, buf[cur], ldx, K, L.out,
                                                  buf[cur ^ 1], nullptr, p.ncols, stream);
+    }
     if (rc != CYR_OK) return rc;
     cur ^= 1;
   }
