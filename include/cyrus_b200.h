@@ -27,7 +27,10 @@
  *                                       deterministic actor mean (sac.py:349)
  *   codebook  [S][cap+1][E]     int32   column j sums to j*L, column 0 zero
  *   node_state[S][nodes][Epad]  int16   Mode-R arrival-tree cumulative
- *                                       punctures, BFS order
+ *                                       punctures, BFS order;
+ *                                       Epad = roundup(E, 2) (packed 4-byte
+ *                                       words, zero padding lane for odd E);
+ *                                       16-byte-aligned base
  *   weights blob (policy create/update): per layer W (out,in) row-major
  *     float64 followed by b (out) — the PSIMMLP1 payload order
  *     (neural.py:186-196).
