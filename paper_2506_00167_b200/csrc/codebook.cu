@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(256, 4) codebook_kernel(
 // Batch K3, one lane per row (projection_lane.cuh): each warp holds
 // 32 / cap whole slots; 4 warps per CTA, no CTA barrier.
 constexpr int kLaneWarps = 4;
-constexpr int kLaneMinBlocks = 6;  // <= 85 registers: 24 warps per SM (issue-latency bound)
+constexpr int kLaneMinBlocks = 5;  // <= 102 registers: 20 warps per SM (no spills; 4/6/8 measured flat)
 
 template <typename RawT>
 __global__ void __launch_bounds__(32 * kLaneWarps) codebook_lane_kernel(

@@ -163,7 +163,7 @@ static __device__ long long fill_threshold(const Row& r, int E, double x0) {
 // (enforcer.py:91).  `group` > 0 splits the warp's rows into independent
 // calls of `group` consecutive lanes (one slot each, RPL == 1); group == 0
 // couples every row.  Returns the iteration count of this lane's call.
-template <int RPL>
+template <int RPL, bool SKIP = false>
 __device__ int coupled_bisection(double (&lo)[RPL], double (&hi)[RPL], const long long (&T)[RPL],
                                  const bool (&bis)[RPL], int group = 0) {
   // Chunks of kSpec steps run speculatively with the bracket history kept in
@@ -188,9 +188,66 @@ __device__ int coupled_bisection(double (&lo)[RPL], double (&hi)[RPL], const lon
       conv = conv && (!bis[k] || __dsub_rn(h[k], l[k]) <= __dmul_rn(kRelWidth, h[k]));
     return conv;
   };
+  // SKIP (the lane-mapped K3 of big batches and Mode-T levels, where it saves
+  // 3-4 % of the tree; on the warp-per-row paths the plain step loop measured
+  // slower than the speculative chunks): steps that provably precede the stop
+  // run without history or votes.  The
+  // bracket is a bisection in log space: ln(hi/lo) halves per step up to the
+  // rounding of one sqrt and one multiply (a relative deviation of ~1.5 ulp
+  // against a width >= 450 ulp while not converged), and the stop test needs
+  // ln(hi/lo) <~ 1e-13.  So a row cannot converge before
+  // floor(log2(ln(hi0/lo0) / 1e-13)) steps; 3 steps of margin absorb the
+  // rounding.  The warp skips the minimum of that bound over its bisecting
+  // lanes; every step it skips is computed exactly as below, so the results
+  // and the stop iteration are unchanged.
+  // (cheap bounds from the exponent and mantissa bits: with x = 2^e (1 + f),
+  // e + f <= log2 x <= e + f / ln 2)
+  auto split = [](double x, double& f) {
+    const long long b = __double_as_longlong(x);
+    f = __longlong_as_double((b & 0xfffffffffffffll) | 0x3ff0000000000000ll) - 1.0;
+    return (int)((b >> 52) & 0x7ff) - 1023;
+  };
+  int tl = kMaxIters;
+  bool anyb = false;
+#pragma unroll
+  for (int k = 0; k < RPL; ++k) {
+    if (!bis[k]) continue;
+    anyb = true;
+    int t = 0;
+    if (lo[k] > 2.3e-308 && hi[k] < 1e308) {  // normal numbers
+      double fh, fl;
+      const int eh = split(hi[k], fh), el = split(lo[k], fl);
+      // lower bound of ln(hi/lo)
+      const double lr = 0.6931471805599453 * ((double)(eh - el) + fh - fl * 1.4426950408889634);
+      if (lr > 0.0) {
+        double fy;
+        t = split(lr * 1e13, fy) - 3;  // floor(log2(lr / 1e-13)) - 3
+      }
+    }
+    tl = min(tl, max(t, 0));
+  }
+  int tskip = __reduce_min_sync(kFull, anyb ? tl : kMaxIters);
+  if (tskip >= kMaxIters || !SKIP) tskip = 0;  // no lane bisects / not enabled
+#pragma unroll 8
+  for (int t = 0; t < tskip; ++t) {
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) {
+      const double mid = __dmul_rn(sl[k], sh[k]);
+      const double root = __dsqrt_rn(mid);
+      const bool up = bis[k] && __double_as_longlong(mid) <= T[k];
+      const bool dn = bis[k] && !up;
+      lo[k] = up ? mid : lo[k];
+      sl[k] = up ? root : sl[k];
+      hi[k] = dn ? mid : hi[k];
+      sh[k] = dn ? root : sh[k];
+    }
+  }
+  // a call without bisecting rows stops at 0 (its brackets never move)
+  const bool group_bis = (__ballot_sync(kFull, anyb) & gmask) != 0u;
+
   bool frozen = false;
   int stop = kMaxIters;
-  for (int base = 0; base < kMaxIters; base += kSpec) {
+  for (int base = tskip; base < kMaxIters; base += kSpec) {
     double hl[kSpec + 1][RPL], hh[kSpec + 1][RPL];
 #pragma unroll
     for (int k = 0; k < RPL; ++k) {
@@ -239,7 +296,7 @@ __device__ int coupled_bisection(double (&lo)[RPL], double (&hi)[RPL], const lon
     }
     if (__all_sync(kFull, frozen)) break;
   }
-  return stop;
+  return group_bis ? stop : 0;
 }
 
 // m_hat lane value and row nu after the bisection (enforcer.py:98-114).

@@ -353,7 +353,7 @@ __device__ void codebook_rows_lane(const RawT* raw, long long row0, int nrows, i
   double lo[1] = {r.lo}, hi[1] = {r.hi};
   const long long tt[1] = {thr};
   const bool bis[1] = {live && r.bis};
-  const int iters = coupled_bisection<1>(lo, hi, tt, bis, cap);
+  const int iters = coupled_bisection<1, true>(lo, hi, tt, bis, cap);
   r.lo = lo[0];
   r.hi = hi[0];
   mark(4);
