@@ -171,7 +171,10 @@ __device__ int coupled_bisection(double (&lo)[RPL], double (&hi)[RPL], const lon
   // picks the exact iteration where the reference loop would have stopped
   // and rolls the bracket back to it.  The serial chain per step is one
   // DMUL and one correctly rounded sqrt.
-  constexpr int kSpec = RPL == 1 ? 8 : 1;
+#ifndef CYR_SPEC
+#define CYR_SPEC 4  // steps per speculative chunk (2 / 4 / 6 / 8 / 16 A/B: 4 best by ~1 us on the batch K3)
+#endif
+  constexpr int kSpec = RPL == 1 ? CYR_SPEC : 1;
   const int lane = threadIdx.x & 31;
   double sl[RPL], sh[RPL];
 #pragma unroll
