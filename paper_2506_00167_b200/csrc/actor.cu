@@ -246,6 +246,47 @@ __device__ __forceinline__ void cluster_slot(const ActorLaunch& p, const int32_t
 
   unsigned long long* tr = (FUSE && g == 0) ? p.trace : nullptr;
   trace_stamp(tr, 0);
+  const int nl = p.desc.n_layers;
+  // Software pipeline across layers: a warp's weight fragments (and biases)
+  // of its FIRST output group of layer l+1 are loaded while layer l's
+  // reduction, DSMEM exchange and cluster barrier run, so each layer starts
+  // with its operands in registers instead of an L2 round trip (the FMA phase
+  // of a layer was ~1.3 us of load latency for ~0.1 us of math).  Layers
+  // whose inputs exceed 2 x 32 lanes x 16 B, and later output groups, load
+  // as before.
+  T wpre[2][kLatOW][V];
+  T bpre[kLatOW];
+  int pre_layer = -1;  // the layer wpre / bpre hold (a warp without a group in
+                       // layer l does not prefetch layer l+1)
+  auto prefetch = [&](int l) {
+    pre_layer = l;
+    const LayerDesc& Lp = p.desc.layer[l];
+    const bool solo_p = FUSE && l == nl - 1;
+    const int Gp = solo_p ? 1 : G, gp = solo_p ? 0 : g;
+    const int stride_p = Gp * nwarps;
+    const int o0p = gp + Gp * warp;
+    const int nv = Lp.in_pad / V;
+    const T* Wp = blob + Lp.wr_off;
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      const int iv = lane + 32 * it;
+#pragma unroll
+      for (int k = 0; k < kLatOW; ++k) {
+        const int o = o0p + k * stride_p;
+        if (o < Lp.out && iv < nv) Vec16<T>::load(Wp + (size_t)o * Lp.in_pad + (size_t)iv * V, wpre[it][k]);
+        else
+#pragma unroll
+          for (int q = 0; q < V; ++q) wpre[it][k][q] = T(0);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kLatOW; ++k) {
+      const int o = o0p + k * stride_p;
+      bpre[k] = o < Lp.out ? blob[Lp.b_off + o] : T(0);
+    }
+  };
+  if (nl > 0) prefetch(0);  // in flight while the inputs are built and exchanged
+
   for (int idx = tid; idx < 2 * rows * C; idx += blockDim.x) act0[idx] = T(0);
   __syncthreads();
   for (int idx = tid; idx < (p.E + 1) * C; idx += blockDim.x) {
@@ -261,7 +302,6 @@ __device__ __forceinline__ void cluster_slot(const ActorLaunch& p, const int32_t
   cluster.sync();  // every CTA is live and has its input before any DSMEM store
   trace_stamp(tr, 1);
 
-  const int nl = p.desc.n_layers;
   for (int l = 0; l < nl; ++l) {
     const LayerDesc& L = p.desc.layer[l];
     const T* cur = (l & 1) ? act1 : act0;
@@ -276,21 +316,13 @@ __device__ __forceinline__ void cluster_slot(const ActorLaunch& p, const int32_t
     const int nvec = L.in_pad / V;
     const int stride = Gl * nwarps;  // outputs are dealt round-robin: rank, then warp
     for (int o0 = gl + Gl * warp; o0 < L.out; o0 += stride * kLatOW) {
+      const bool pre = o0 == gl + Gl * warp && pre_layer == l;  // operands in wpre / bpre
       T acc[kLatOW][C];
 #pragma unroll
       for (int k = 0; k < kLatOW; ++k)
 #pragma unroll
         for (int c = 0; c < C; ++c) acc[k][c] = T(0);
-      for (int iv = lane; iv < nvec; iv += 32) {
-        T w[kLatOW][V];
-#pragma unroll
-        for (int k = 0; k < kLatOW; ++k) {
-          const int o = o0 + k * stride;
-          if (o < L.out) Vec16<T>::load(W + (size_t)o * L.in_pad + (size_t)iv * V, w[k]);
-          else
-#pragma unroll
-            for (int q = 0; q < V; ++q) w[k][q] = T(0);
-        }
+      auto fma_chunk = [&](int iv, const T (&w)[kLatOW][V]) {
 #pragma unroll
         for (int q = 0; q < V; ++q) {
           const T* xr = cur + (size_t)(iv * V + q) * C;
@@ -302,7 +334,34 @@ __device__ __forceinline__ void cluster_slot(const ActorLaunch& p, const int32_t
 #pragma unroll
             for (int c = 0; c < C; ++c) acc[k][c] = fma(w[k][q], x[c], acc[k][c]);
         }
+      };
+      for (int iv = lane; iv < nvec; iv += 32) {
+        const int it = (iv - lane) >> 5;
+        if (pre && it < 2) {
+          if (it == 0) fma_chunk(iv, wpre[0]);
+          else fma_chunk(iv, wpre[1]);
+          continue;
+        }
+        T w[kLatOW][V];
+#pragma unroll
+        for (int k = 0; k < kLatOW; ++k) {
+          const int o = o0 + k * stride;
+          if (o < L.out) Vec16<T>::load(W + (size_t)o * L.in_pad + (size_t)iv * V, w[k]);
+          else
+#pragma unroll
+            for (int q = 0; q < V; ++q) w[k][q] = T(0);
+        }
+        fma_chunk(iv, w);
       }
+      T bias_k[kLatOW];
+#pragma unroll
+      for (int k = 0; k < kLatOW; ++k) {
+        const int o = o0 + k * stride;
+        bias_k[k] = pre ? bpre[k] : (o < L.out ? blob[L.b_off + o] : T(0));
+      }
+      // next layer's first group: its loads fly during this exchange + barrier
+      if (o0 == gl + Gl * warp && l + 1 < nl && !(FUSE && l + 1 == nl - 1 && g != 0))
+        prefetch(l + 1);
       if (o0 == gl + Gl * warp) trace_stamp(tr, 24 + 2 * l);
 #pragma unroll
       for (int k = 0; k < kLatOW; ++k)
@@ -315,7 +374,7 @@ __device__ __forceinline__ void cluster_slot(const ActorLaunch& p, const int32_t
       for (int k = 0; k < kLatOW; ++k) {
         const int o = o0 + k * stride;
         if (o >= L.out) continue;  // warp-uniform
-        const T bias = blob[L.b_off + o];
+        const T bias = bias_k[k];
         if (last) {
           T* raw = FUSE ? raw_s : static_cast<T*>(p.raw);
 #pragma unroll
