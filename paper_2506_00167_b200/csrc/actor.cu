@@ -460,13 +460,17 @@ __global__ void __launch_bounds__(kLatThreads, 1)
         uint32_t cmd = 0;  // 0: leave
         const unsigned long long t0 = globaltimer_ns();
         for (;;) {
-          uint32_t r;
-          asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(r) : "l"(&mb->req_seq) : "memory");
+          // req_seq and quit in ONE system-scope read (adjacent words): each
+          // probe is one PCIe round trip, so a request is seen half a probe
+          // period sooner than with two reads per probe
+          unsigned long long rq;
+          asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(rq) : "l"(&mb->req_seq) : "memory");
+          const uint32_t r = (uint32_t)rq, quit = (uint32_t)(rq >> 32);
           if (r != last) {
             cmd = r;
             break;
           }
-          if (mb->quit != 0u) break;
+          if (quit != 0u) break;
           if (globaltimer_ns() - t0 > idle_ns) break;
         }
         if (cmd != 0u) mb->t_start = globaltimer_ns();
