@@ -228,7 +228,12 @@ struct Vec16<double> {
 
 // One slot (or a few) through the cluster: K2 layers split over the CTAs,
 // K3 fused on rank 0 (FUSE).  Ranks other than 0 return after the last layer.
-template <typename T, int C, bool FUSE>
+// resident (slot server): the activation buffers were zeroed once at server
+// start and the request hand-off already synchronised the cluster, so the
+// per-call zeroing and the cluster barrier before the first DSMEM store are
+// skipped.  Rows a call does not write keep finite values of the previous
+// call (ReLU outputs) and only ever meet the zero-padded weight columns.
+template <typename T, int C, bool FUSE, bool RESIDENT = false>
 __device__ __forceinline__ void cluster_slot(const ActorLaunch& p, const int32_t* alloc,
                                              const double* eps) {
   namespace cg = cooperative_groups;
@@ -287,8 +292,10 @@ __device__ __forceinline__ void cluster_slot(const ActorLaunch& p, const int32_t
   };
   if (nl > 0) prefetch(0);  // in flight while the inputs are built and exchanged
 
-  for (int idx = tid; idx < 2 * rows * C; idx += blockDim.x) act0[idx] = T(0);
-  __syncthreads();
+  if constexpr (!RESIDENT) {
+    for (int idx = tid; idx < 2 * rows * C; idx += blockDim.x) act0[idx] = T(0);
+    __syncthreads();
+  }
   for (int idx = tid; idx < (p.E + 1) * C; idx += blockDim.x) {
     const int i = idx / C, c = idx % C;
     double v = 0.0;
@@ -299,7 +306,10 @@ __device__ __forceinline__ void cluster_slot(const ActorLaunch& p, const int32_t
     }
     act0[i * C + c] = (T)v;
   }
-  cluster.sync();  // every CTA is live and has its input before any DSMEM store
+  if constexpr (RESIDENT)
+    __syncthreads();  // own inputs visible (the hand-off barrier covered the cluster)
+  else
+    cluster.sync();  // every CTA is live and has its input before any DSMEM store
   trace_stamp(tr, 1);
 
   for (int l = 0; l < nl; ++l) {
@@ -453,6 +463,12 @@ __global__ void __launch_bounds__(kLatThreads, 1)
   __shared__ double s_eps[256];
   __shared__ uint32_t s_cmd;
   const int tid = threadIdx.x;
+  {  // zero the activation buffers once (cluster_slot<..., RESIDENT>)
+    extern __shared__ __align__(16) unsigned char smem[];
+    T* act = reinterpret_cast<T*>(smem);
+    for (int idx = tid; idx < 2 * p.desc.max_rows * C; idx += blockDim.x) act[idx] = T(0);
+    cluster.sync();
+  }
   const int n_alloc = p.S * p.E, n_eps = p.eps != nullptr ? p.S * p.cap * p.E : 0;
   for (;;) {
     if (g == 0) {
@@ -501,7 +517,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
     const uint32_t cmd = s_cmd;
     if (cmd == 0u) break;  // cluster-uniform
     last = cmd;
-    cluster_slot<T, C, true>(p, s_alloc, p.eps != nullptr ? s_eps : nullptr);
+    cluster_slot<T, C, true, true>(p, s_alloc, p.eps != nullptr ? s_eps : nullptr);
     if (g == 0) {
       __syncthreads();  // the codebook copy into the mailbox is complete
       if (tid == 0) {
