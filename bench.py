@@ -72,52 +72,214 @@ def make_cell_agent():
 
 
 # ------------------------------------------------------------- CPU baseline
-def _cpu_worker_init(weights, biases):
-    global _W, _B
-    _W, _B = weights, biases
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
-def _cpu_worker(args):
-    from oracle import arrival_tree, slot
-    allocs, eps, n, l, m = args
+def load_punctsim():
+    """The UNMODIFIED reference package (``punctsim``), pip-installed into
+    baseline/_ref, or None when it is not there.  Nothing
+    from the product package is imported on this path."""
+    if not os.path.isdir(os.path.join(REF_DIR, "punctsim")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import punctsim.core
+        import punctsim.engine
+        import punctsim.sac
+        import punctsim.scheduler
+        import punctsim.seeding
+        return punctsim
+    except Exception as exc:  # reported by the caller as the port fallback
+        log(f"punctsim not importable from {REF_DIR}: {exc}")
+        return None
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def ref_world(ps, hidden=HIDDEN):
+    """The reference's own objects for the bench workload: CellConfig,
+    make_agent on substream(0, "agent-init") (sac.py:114-127)."""
+    cell = ps.core.CellConfig(**GEOM)
+    agent = ps.sac.make_agent(cell, ps.sac.AgentHyper(actor_hidden=hidden),
+                              ps.seeding.substream(0, "agent-init"))
+    return cell, agent
+
+
+def ref_schedules(ps, cell, slots, seed):
+    """engine._synthetic_schedule (engine.py:296-302) on substream(seed,
+    "scenario"): the same schedules synthetic_inputs() hands the GPU."""
+    rng = ps.seeding.substream(seed, "scenario")
+    return [ps.engine._synthetic_schedule(cell, ps.scheduler.DEFAULT_MCS_TABLE, rng)
+            for _ in range(slots)]
+
+
+_REF: dict = {}
+
+
+def _ref_pool_init():
+    try:  # one process per core, each with single-threaded BLAS
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
+
+
+def _ref_worker(job):
+    """Slots [lo, hi) of rank block ``seed`` through the reference's own
+    ``punctsim.engine.build_codebook`` (engine.py:97-116), stochastic, with
+    the branch streams advanced to slot lo first (one (lo, E) draw per branch
+    equals lo sequential E-draws)."""
+    seed, lo, hi = job
+    ps, agent = _REF["ps"], _REF["agent"]
+    scheds = _REF["scheds"][seed]
+    cap, e = agent.cell.num_branches, agent.cell.num_embb
+    streams = ps.engine.make_streams(seed, cap)
+    if lo:
+        for j in range(1, cap + 1):
+            streams.branch[j].standard_normal((lo, e))
+    books = np.empty((hi - lo, cap + 1, e), dtype=np.int32)
     t0 = time.perf_counter()
-    for s in range(allocs.shape[0]):
-        book = slot.slot_codebook(_W, _B, allocs[s], n, l, eps[s])
-        arrival_tree.node_states(book, m)
-    return time.perf_counter() - t0, allocs.shape[0]
+    for s in range(lo, hi):
+        books[s - lo] = ps.engine.build_codebook(agent, scheds[s], streams).columns
+    return time.perf_counter() - t0, books
 
 
-def cpu_baseline(agent, cell, allocs, eps, cores=None):
-    """The oracle port (float64 numpy restatement of the reference path,
-    plus the Mode-R tree restatement) on all host cores, one process per
-    core with single-threaded BLAS.  Returns (codebooks/s, cores, wall s)."""
-    import multiprocessing as mp
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    os.environ["OMP_NUM_THREADS"] = "1"
-    cores = cores or os.cpu_count() or 1
-    cores = max(1, min(cores, allocs.shape[0]))
-    chunks = np.array_split(np.arange(allocs.shape[0]), cores)
-    jobs = [(allocs[c], eps[c], cell.total_scs, cell.urllc_sc_len, cell.minislots)
-            for c in chunks if len(c)]
-    ctx = mp.get_context("fork")
-    with ctx.Pool(len(jobs), initializer=_cpu_worker_init,
-                  initargs=(agent.actor.weights, agent.actor.biases)) as pool:
-        t0 = time.perf_counter()
-        res = pool.map(_cpu_worker, jobs)
-        wall = time.perf_counter() - t0
-    done = sum(r[1] for r in res)
-    return done / wall, len(jobs), wall
-
-
-def single_core_latency_us(agent, cell, allocs, eps, samples=64):
+def _port_worker(job):
+    """Fallback when punctsim is absent: the oracle port (float64 numpy
+    restatement of the same path, test infrastructure)."""
     from oracle import slot
-    times = []
-    for s in range(samples):
-        t0 = time.perf_counter_ns()
-        slot.slot_codebook(agent.actor.weights, agent.actor.biases, allocs[s], cell.total_scs,
-                           cell.urllc_sc_len, eps[s])
-        times.append((time.perf_counter_ns() - t0) / 1e3)
-    return float(np.median(times))
+    seed, lo, hi = job
+    w, b, allocs, eps, n, l = _REF["port"][seed]
+    t0 = time.perf_counter()
+    books = slot.batch_codebooks(w, b, allocs[lo:hi], n, l, eps[lo:hi]).astype(np.int32)
+    return time.perf_counter() - t0, books
+
+
+class ReferenceCpu:
+    """The reference's CPU path on the host cores: ``punctsim`` from
+    baseline/_ref (kind "reference") or, when it is missing, the oracle port
+    (kind "port").  One forked process per core; ``run()`` builds every
+    slot of ``blocks`` rank blocks (block r = the inputs rank r's GPU arm
+    uses, seed r) and returns (wall s, codebooks (blocks*slots, cap+1, E)).
+    The reference has no arrival tree: only the codebooks are charged to
+    it (ours also writes the Mode-R tree, so the comparison is conservative).
+    """
+
+    def __init__(self, blocks=1, slots=SLOTS, cores=None):
+        import multiprocessing as mp
+        os.environ["OPENBLAS_NUM_THREADS"] = "1"
+        os.environ["OMP_NUM_THREADS"] = "1"
+        self.ps = load_punctsim()
+        self.kind = "reference" if self.ps is not None else "port"
+        self.blocks, self.slots = blocks, slots
+        self.cores = max(1, cores or os.cpu_count() or 1)
+        if self.ps is not None:
+            cell, agent = ref_world(self.ps)
+            _REF.update(ps=self.ps, agent=agent,
+                        scheds={r: ref_schedules(self.ps, cell, slots, r) for r in range(blocks)})
+            worker = _ref_worker
+        else:
+            cell, agent = make_cell_agent()
+            port = {}
+            for r in range(blocks):
+                allocs, eps = synthetic_inputs(cell, slots, seed=r)
+                port[r] = (agent.actor.weights, agent.actor.biases, allocs, eps,
+                           cell.total_scs, cell.urllc_sc_len)
+            _REF.update(port=port)
+            worker = _port_worker
+        per_block = max(1, self.cores // blocks)
+        self.jobs = []
+        for r in range(blocks):
+            for c in np.array_split(np.arange(slots), min(per_block, slots)):
+                if len(c):
+                    self.jobs.append((r, int(c[0]), int(c[-1]) + 1))
+        self.worker = worker
+        self.pool = mp.get_context("fork").Pool(min(self.cores, len(self.jobs)),
+                                                initializer=_ref_pool_init)
+
+    def run(self):
+        t0 = time.perf_counter()
+        res = self.pool.map(self.worker, self.jobs, chunksize=1)
+        wall = time.perf_counter() - t0
+        return wall, np.concatenate([r[1] for r in res])
+
+    def close(self):
+        self.pool.terminate()
+        self.pool.join()
+
+    def describe(self):
+        what = ("punctsim.engine.build_codebook (unmodified reference, baseline/_ref)"
+                if self.kind == "reference" else
+                "oracle port (float64 numpy restatement; punctsim not installed)")
+        return (f"{self.blocks * self.slots} slots per step (cfg2 geometry, stochastic) through "
+                f"{what}, {min(self.cores, len(self.jobs))} processes with single-threaded BLAS; "
+                "codebooks only (the reference has no arrival tree)")
+
+
+def _single_core_child(q, ps_dir):
+    os.sched_setaffinity(0, {min(os.sched_getaffinity(0))})
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
+    ps = load_punctsim()
+    cell, agent = ref_world(ps)
+    scheds = ref_schedules(ps, cell, 64, 0)
+    streams = ps.engine.make_streams(0, cell.num_branches)
+    for s in range(8):
+        ps.engine.build_codebook(agent, scheds[s], streams)
+    ns = [ps.engine.build_codebook(agent, scheds[s], streams).gen_ns for s in range(64)]
+    q.put(ns)
+
+
+def single_core_reference():
+    """The reference on ONE core: (1) its own timing recipe, acceptance
+    check 10 (pkg/tests/test_acceptance.py:454-467: ``compare --ttis 60
+    --seed 3`` with OPENBLAS_NUM_THREADS=1, per-branch us from timing.csv,
+    N=780/E=10/L=300); (2) the bench geometry's per-slot gen_ns."""
+    import csv
+    import multiprocessing as mp
+    import tempfile
+    if load_punctsim() is None:
+        return None
+    out = {"cpu_model": cpu_model()}
+    cpu0 = min(os.sched_getaffinity(0))
+    with tempfile.TemporaryDirectory() as tmp:
+        env = dict(os.environ, OPENBLAS_NUM_THREADS="1", OMP_NUM_THREADS="1",
+                   PYTHONPATH=REF_DIR)
+        res = subprocess.run([sys.executable, "-m", "punctsim", "compare", "--ttis", "60",
+                              "--seed", "3", "--out", tmp], env=env, capture_output=True,
+                             text=True, preexec_fn=lambda: os.sched_setaffinity(0, {cpu0}))
+        if res.returncode == 0:
+            with open(os.path.join(tmp, "timing.csv"), newline="") as fh:
+                per_branch = np.array([float(r["per_branch_us"]) for r in csv.DictReader(fh)])
+            out["acceptance10_per_branch_us"] = {
+                "median": float(np.median(per_branch)),
+                "p90": float(np.percentile(per_branch, 90)),
+                "max": float(per_branch.max()), "ttis": int(per_branch.size),
+                "recipe": "punctsim compare --ttis 60 --seed 3, OPENBLAS_NUM_THREADS=1, one "
+                          "core (test_acceptance.py:454-467); N=780/E=10/L=300, actor 1x128"}
+    q = mp.get_context("fork").Queue()
+    p = mp.get_context("fork").Process(target=_single_core_child, args=(q, REF_DIR))
+    p.start()
+    ns = q.get(timeout=300)
+    p.join()
+    out["cfg2_slot_us"] = {"p50": float(np.median(ns)) / 1e3,
+                           "p99": float(np.percentile(ns, 99)) / 1e3, "slots": len(ns),
+                           "what": "punctsim build_codebook gen_ns, bench geometry (cfg2, 2x256, "
+                                   "stochastic), one core, single-threaded BLAS"}
+    return out
 
 
 # ------------------------------------------------------------------ clocks
@@ -200,41 +362,44 @@ def committed_traffic():
 
 # --------------------------------------------------------------- reference
 def run_reference(args, rank, world):
+    """``--impl reference``: the reference's own CPU path on the host cores
+    for the same workload (world x 1024 slots per step), rank 0 only.  This
+    process imports nothing from paper_2506_00167_b200."""
     if rank != 0:
         return 0
-    cell, agent = make_cell_agent()
-    allocs, eps = synthetic_inputs(cell, SLOTS)
-    per_step, cores = [], 0
-    for i in range(args.warmup + args.steps):
-        rate, cores, wall = cpu_baseline(agent, cell, allocs, eps)
-        if i >= args.warmup:
-            per_step.append(wall)
-    wall = float(np.mean(per_step))
-    value = SLOTS / wall
+    ref = ReferenceCpu(blocks=world)
+    try:
+        for _ in range(args.warmup):
+            ref.run()
+        walls = [ref.run()[0] for _ in range(args.steps)]
+    finally:
+        ref.close()
+    wall = float(np.mean(walls))
+    total = SLOTS * world
+    value = total / wall
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": wall * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_block(world, "none", impl="reference"),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{SLOTS} slots per step (cfg2 geometry codebook + Mode-R "
-                                   "tree restatement), all host cores"},
+        "config": config_block(world),
+        "precision": "float64 numpy (reference)",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": min(ref.cores, len(ref.jobs)),
+                         "kind": ref.kind, "sample": ref.describe(), "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def config_block(world, l2, impl="ours"):
+def config_block(world):
+    """Identical for both arms (the driver compares them)."""
     return {"workload": "cfg3: 1024 independent slots per rank (N=780, E=10, L=195, cap 4, "
-                        "M=7), actor 2x256, stochastic, Mode-R arrival tree"
-                        + (", NCCL codebook all-gather" if world > 1 else ""),
+                        "M=7), actor 2x256 random-init, stochastic; GPU arm also writes the "
+                        "Mode-R arrival tree" + (", NCCL codebook all-gather" if world > 1 else ""),
             "slots_per_rank": SLOTS, "global_batch": SLOTS * world, "cells": SLOTS * world,
-            "actor": "2x256",
-            "precision": ("fp32 actor / fp64 projection" if impl == "ours"
-                          else "float64 numpy (oracle port of the reference)"),
-            "parallelism": f"cell-sharded x{world}", "l2": l2}
+            "actor": "2x256", "parallelism": f"cell-sharded x{world}",
+            "l2": "GPU arm: flushed (256 MiB write) between timed steps; CPU arm: n/a"}
 
 
 # -------------------------------------------------------------------- ours
@@ -424,15 +589,14 @@ def run_ours(args, rank, world, local_rank):
         kernels.append({k: roofline[k] for k in ("kernel", "bound", "achieved", "peak", "unit",
                                                  "frac")} | {"ms": roofline["kernel_ms"]})
 
-    cores_rate, cores, cpu_wall = cpu_baseline(agent, cell, allocs, eps) if world == 1 else \
-        (None, None, None)
-    core1 = single_core_latency_us(agent, cell, allocs, eps) if world == 1 else None
+    cpu = cpu_leg(eng.codebooks, agent, cell, allocs, eps) if world == 1 else None
     line = {
         "metric": METRIC, "value": total / (mean_ms * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "fp32", "data": "synthetic",
-        "config": config_block(world, "flushed (256 MiB write) between timed steps"),
+        "config": config_block(world),
+        "precision": f"{args.precision} actor / fp64 projection",
         "e2e": {"value": total / mean_e2e, "unit": UNIT,
                 "h2d_bytes_per_step": int(allocs.nbytes + eps.nbytes),
                 "d2h_bytes_per_step": int(SLOTS * (cell.num_branches + 1) * cell.num_embb * 4),
@@ -448,16 +612,47 @@ def run_ours(args, rank, world, local_rank):
         "cfg4_strong": strong,
         "roofline": roofline,
         "kernels": kernels,
-        "cpu_baseline": None if cores_rate is None else {
-            "value": cores_rate, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{SLOTS} slots (one step's workload) over {cores} processes, "
-                      f"{cpu_wall:.2f} s wall; oracle float64 restatement + Mode-R tree",
-            "single_core_slot_us": core1},
+        "cpu_baseline": None if cpu is None else cpu[0],
+        "parity": None if cpu is None else cpu[1],
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks.summary(),
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def cpu_leg(gpu_books, agent, cell, allocs, eps, reps=3):
+    """rank 0, N=1: the reference's CPU path (ReferenceCpu) on all host cores
+    over this step's 1024 slots, timed over ``reps`` passes, and its
+    codebooks compared with the GPU's (the timed steps' output).  Mismatched
+    rows are classified with the oracle's Huntington-Hill boundary margin
+    (allowed only below 1e-5 under fp32 logits)."""
+    ref = ReferenceCpu(blocks=1)
+    try:
+        ref.run()  # warm the workers
+        runs = [ref.run() for _ in range(reps)]
+    finally:
+        ref.close()
+    wall = float(np.mean([r[0] for r in runs]))
+    want = runs[-1][1]
+    got = gpu_books[:SLOTS].cpu().numpy()
+    diff = (got != want).any(axis=2)          # (slots, cap+1) rows
+    near = 0
+    if diff.any():
+        from oracle import slot
+        for s in np.flatnonzero(diff.any(axis=1)):
+            _, info = slot.slot_codebook(agent.actor.weights, agent.actor.biases, allocs[s],
+                                         cell.total_scs, cell.urllc_sc_len, eps[s], details=True)
+            for j in np.flatnonzero(diff[s]):
+                near += int(j >= 1 and info["margin"][j - 1] < 1e-5)
+    cpu = {"value": SLOTS / wall, "unit": UNIT, "cores": min(ref.cores, len(ref.jobs)),
+           "kind": ref.kind, "sample": ref.describe() + f"; mean of {reps} passes",
+           "cpu_model": cpu_model(), "single_core": single_core_reference()}
+    parity = {"against": ref.kind, "slots": int(got.shape[0]),
+              "rows": int(diff.size - got.shape[0]), "mismatched": int(diff.sum()),
+              "near_tie_logged": near, "mismatched_outside_near_tie": int(diff.sum()) - near,
+              "rule": "codebook rows bit-exact except rows whose reference HH margin < 1e-5"}
+    return cpu, parity
 
 
 def mode_t_run(cell, hidden, slots, reps=3, fp32_reps=None):
@@ -497,6 +692,7 @@ def mode_t_run(cell, hidden, slots, reps=3, fp32_reps=None):
                      "note": "whole tree time (actor + K3 + features) over actor FLOPs"}
         pol.close()
     same = (states["fp32"] == states["bf16_tc"]).all(axis=2)
+    out["_slot0"] = {k: v[0] for k, v in states.items()}
     out.update({"actor": "x".join(str(h) for h in hidden), "slots": slots,
                 "cell": {"N": cell.total_scs, "E": cell.num_embb, "L": cell.urllc_sc_len,
                          "cap": cell.num_branches, "M": cell.minislots},
@@ -559,13 +755,15 @@ def mode_t_sharded(world, rank, dev, reps=3):
     return res
 
 
-def mode_t_cpu(cell, hidden, sample_levels, seed=11):
+def mode_t_cpu(cell, hidden, sample_levels, gpu_slot0=None, seed=11):
     """The Mode-T oracle (float64 numpy: the reference's actor, head and
-    enforcer per node) timed on a sampled subtree — levels 1..sample_levels
-    of one slot — and scaled by parents (one coupled enforcement and cap
-    actor columns each) to the full tree.  Mode T has no reference
-    implementation; this is the port's cost."""
-    from dataclasses import replace
+    enforcer per node) on a sampled subtree — levels 1..sample_levels of
+    slot 0 of the same tree the GPU built — timed and scaled by parents (one
+    coupled enforcement and cap actor columns each) to the full tree.  Mode
+    T has no reference implementation; this is the port's cost (SURVEY
+    §8(d)).  With ``gpu_slot0`` ({precision: node states}) the sampled
+    nodes are also compared: fp32 must match outside subtrees under a
+    near-tie decision (margin < 1e-5); bf16 reports its agreement."""
     from oracle import mode_t
     from paper_2506_00167_b200 import substream, tree
     actor = tree.make_mode_t_actor(cell, hidden, substream(0, "mode-t"))
@@ -575,16 +773,36 @@ def mode_t_cpu(cell, hidden, sample_levels, seed=11):
     sample_parents = sum(r ** t for t in range(sample_levels))
     full_parents = sum(r ** t for t in range(cell.minislots))
     t0 = time.perf_counter()
-    mode_t.mode_t_tree(actor.weights, actor.biases, allocs[0], mcs[0], cell.total_scs,
-                       cell.urllc_sc_len, sample_levels, eps[0])
+    want, margins = mode_t.mode_t_tree(actor.weights, actor.biases, allocs[0], mcs[0],
+                                       cell.total_scs, cell.urllc_sc_len, cell.minislots, eps[0],
+                                       details=True, stop_level=sample_levels)
     wall = time.perf_counter() - t0
     per_parent = wall / sample_parents
-    return {"sample": f"levels 1..{sample_levels} of one slot ({sample_parents} parents, "
-                      f"{sample_parents * cell.num_branches} actor columns), one process",
-            "sample_s": wall, "per_parent_ms": per_parent * 1e3,
-            "est_s_per_tree_one_core": per_parent * full_parents,
-            "est_trees_per_s_all_cores": (os.cpu_count() or 1) / (per_parent * full_parents),
-            "cores": os.cpu_count() or 1, "kind": "port (estimate: per-parent cost x parents)"}
+    out = {"sample": f"levels 1..{sample_levels} of slot 0 ({sample_parents} parents, "
+                     f"{sample_parents * cell.num_branches} actor columns), one process",
+           "sample_s": wall, "per_parent_ms": per_parent * 1e3,
+           "est_s_per_tree_one_core": per_parent * full_parents,
+           "est_trees_per_s_all_cores": (os.cpu_count() or 1) / (per_parent * full_parents),
+           "cores": os.cpu_count() or 1, "kind": "port (estimate: per-parent cost x parents)"}
+    if gpu_slot0:
+        taint, t = np.zeros(1, dtype=bool), []
+        for lvl in margins:                  # nodes whose path crosses a near-tie
+            child = np.repeat(taint, r).reshape(-1, r)
+            child[:, 1:] |= lvl < 1e-5
+            taint = child.ravel()
+            t.append(taint)
+        taint = np.concatenate(t)
+        n = want.shape[0]
+        par = {"nodes_checked": int(n), "near_tie_nodes": int(taint.sum())}
+        for prec, st in gpu_slot0.items():
+            diff = (st[:n, :want.shape[1]] != want).any(axis=1)
+            if prec == "fp32":
+                par["fp32_mismatched"] = int(diff.sum())
+                par["fp32_mismatched_outside_near_tie"] = int((diff & ~taint).sum())
+            else:
+                par[f"{prec}_agreement_vs_oracle"] = float(1.0 - diff.mean())
+        out["parity"] = par
+    return out
 
 
 def mode_t_all(cell):
@@ -593,8 +811,8 @@ def mode_t_all(cell):
     cfg5 = CellConfig(780, 16, 130)
     out = {"cfg2": mode_t_run(cell, HIDDEN, 32),
            "cfg5": mode_t_run(cfg5, (1024, 1024, 1024), 1, reps=3, fp32_reps=1)}
-    out["cfg2"]["cpu"] = mode_t_cpu(cell, HIDDEN, 4)
-    out["cfg5"]["cpu"] = mode_t_cpu(cfg5, (1024, 1024, 1024), 3)
+    out["cfg2"]["cpu"] = mode_t_cpu(cell, HIDDEN, 4, out["cfg2"].pop("_slot0"))
+    out["cfg5"]["cpu"] = mode_t_cpu(cfg5, (1024, 1024, 1024), 3, out["cfg5"].pop("_slot0"))
     return out
 
 

@@ -19,9 +19,11 @@ from . import mlp, projection
 
 
 def mode_t_tree(weights, biases, alloc, mcs, total_scs: int, sc_len: int, minislots: int,
-                eps=None, mcs_scale: float = 5.0, details: bool = False):
+                eps=None, mcs_scale: float = 5.0, details: bool = False, stop_level=None):
     """alloc, mcs: (E,); eps: (cap, E) or None.  Returns node states (nodes, E)
-    in BFS order (levels 1..M) and, with ``details``, per-level margins."""
+    in BFS order (levels 1..M) and, with ``details``, per-level margins.
+    ``stop_level`` < M stops after that level (the top of the same tree: the
+    features still use M)."""
     alloc = np.asarray(alloc, dtype=np.float64)
     users = alloc.size
     cap = total_scs // sc_len
@@ -30,7 +32,7 @@ def mode_t_tree(weights, biases, alloc, mcs, total_scs: int, sc_len: int, minisl
     arrivals = np.zeros(1, dtype=np.int64)
     levels, margins = [], []
     mcs_feat = np.asarray(mcs, dtype=np.float64) / mcs_scale
-    for tau in range(1, minislots + 1):
+    for tau in range(1, (stop_level or minislots) + 1):
         npar = parents.shape[0]
         cols = npar * cap
         x = np.empty((3 * users + 3, cols))

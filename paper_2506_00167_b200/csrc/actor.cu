@@ -538,16 +538,14 @@ int launch_slot_server(const ActorLaunch& p, int G, SlotMailbox* mb, uint32_t la
   const size_t smem = (2ull * p.desc.max_rows * C + (size_t)C * 2 * p.E) * sizeof(T);
   if (smem + 4096 > (size_t)kSmemLimit) return CYR_UNSUPPORTED;
   auto kern = slot_server_kernel<T, C>;
-  static int configured_smem = -1;
-  if ((int)smem > configured_smem) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return CYR_CUDA_ERROR;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-        cudaSuccess)
-      return CYR_CUDA_ERROR;
-    configured_smem = (int)smem;
-  }
+  static AttrCache configured;
+  if (!ensure_func_attr(configured, (int)smem, [&] {
+        return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem) == cudaSuccess &&
+               cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                   cudaSuccess;
+      }))
+    return CYR_CUDA_ERROR;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(G);
   cfg.blockDim = dim3(kLatThreads);
@@ -570,16 +568,14 @@ int launch_actor_cluster(const ActorLaunch& p, int G, cudaStream_t stream,
   const size_t smem = (2ull * p.desc.max_rows * C + (FUSE ? (size_t)C * 2 * p.E : 0)) * sizeof(T);
   if (smem > (size_t)kSmemLimit) return CYR_UNSUPPORTED;
   auto kern = actor_cluster_kernel<T, C, FUSE>;
-  static int configured_smem = -1;  // attributes are per function: set once
-  if ((int)smem > configured_smem) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return CYR_CUDA_ERROR;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-        cudaSuccess)
-      return CYR_CUDA_ERROR;
-    configured_smem = (int)smem;
-  }
+  static AttrCache configured;
+  if (!ensure_func_attr(configured, (int)smem, [&] {
+        return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem) == cudaSuccess &&
+               cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                   cudaSuccess;
+      }))
+    return CYR_CUDA_ERROR;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(G);
   cfg.blockDim = dim3(kLatThreads);
@@ -836,13 +832,12 @@ int launch_actor_tiled(const ActorLaunch& p, cudaStream_t stream) {
                       (INPLACE ? 1ull : 2ull) * p.desc.max_width * TCP * sizeof(T);
   if (smem > (size_t)kSmemLimit) return CYR_UNSUPPORTED;
   auto kern = actor_tiled_kernel<T, TC, NW, INPLACE>;
-  static int configured = -1;
-  if ((int)smem > configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return CYR_CUDA_ERROR;
-    configured = (int)smem;
-  }
+  static AttrCache configured;
+  if (!ensure_func_attr(configured, (int)smem, [&] {
+        return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem) == cudaSuccess;
+      }))
+    return CYR_CUDA_ERROR;
   const int blocks = (p.ncols + TC - 1) / TC;
   kern<<<blocks, NW * 32 + kTileProducer, smem, stream>>>(p);
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
@@ -1053,13 +1048,12 @@ int launch_actor_osplit(const ActorLaunch& p, cudaStream_t stream) {
                       2ull * p.desc.max_width * TCP * sizeof(T);
   if (smem > (size_t)kSmemLimit) return CYR_UNSUPPORTED;
   auto kern = actor_osplit_kernel<T, CPT>;
-  static int configured = -1;
-  if ((int)smem > configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return CYR_CUDA_ERROR;
-    configured = (int)smem;
-  }
+  static AttrCache configured;
+  if (!ensure_func_attr(configured, (int)smem, [&] {
+        return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem) == cudaSuccess;
+      }))
+    return CYR_CUDA_ERROR;
   const int blocks = (p.ncols + TC - 1) / TC;
   kern<<<blocks, 8 * 32 + kTileProducer, smem, stream>>>(p);
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;

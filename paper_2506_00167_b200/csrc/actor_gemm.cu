@@ -279,13 +279,12 @@ int launch_layer(const float* Wt, int ldw, int Kw, const float* bias, const floa
   using namespace cyr;
   constexpr size_t smem = (size_t)kGemmStages * stage_floats<BM, BN>() * sizeof(float);
   auto kern = sgemm_layer_kernel<BM, BN, LAST, OPT>;
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return CYR_CUDA_ERROR;
-    configured = true;
-  }
+  static AttrCache configured;
+  if (!ensure_func_attr(configured, (int)smem, [&] {
+        return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem) == cudaSuccess;
+      }))
+    return CYR_CUDA_ERROR;
   const dim3 grid((unsigned)((ncols + BN - 1) / BN), (unsigned)((out + BM - 1) / BM));
   kern<<<grid, kGemmThreads, smem, stream>>>(Wt, ldw, Kw, bias, X, ldx, K, out, Y, ldx, raw, ncols);
   return CYR_OK;

@@ -602,13 +602,13 @@ int cyr_launch_actor_tc(const cyr::ActorDesc& desc, const unsigned char* tc_blob
   p.epad = epad;
   p.mcs_scale = mcs_scale;
   const size_t smem = cyr_tc_smem_bytes();
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(cyr::actor_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-      return CYR_CUDA_ERROR;
-    configured = true;
-  }
+  static cyr::AttrCache configured;
+  if (!cyr::ensure_func_attr(configured, (int)smem, [&] {
+        return cudaFuncSetAttribute(cyr::actor_tc_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem) == cudaSuccess;
+      }))
+    return CYR_CUDA_ERROR;
   const int blocks = (p.ncols + cyr::kTcM - 1) / cyr::kTcM;
   cyr::actor_tc_kernel<<<blocks, cyr::kTcThreads, smem, stream>>>(p);
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
@@ -670,10 +670,9 @@ int cyr_launch_actor_tc_layer(const cyr::ActorDesc& desc, const unsigned char* t
   const size_t fixed = 1024 + (first ? 2 * cyr::kWideImage : 0) +
                        (last ? 0 : eg * 2 * cyr::kWideImage) +
                        (4 * cyr::kWideMaxSlots + 16) * 8 + 16;
-  static int max_smem = 0, sms = 0;
-  if (!max_smem) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+  int max_smem = 0, sms = 0;
+  {
+    const int dev = cyr::current_device_ordinal();
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }

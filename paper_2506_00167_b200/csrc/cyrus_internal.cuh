@@ -273,3 +273,34 @@ int cyr_launch_actor_tc_layer(const cyr::ActorDesc& desc, const unsigned char* t
                               int parents, long long nodes_per_slot, long long parent_off,
                               int epad, double mcs_scale, cudaStream_t stream,
                               int parent_base = 0);
+
+// ------------------------------------------------ per-device attribute cache
+// cudaFuncSetAttribute is per (function, device): a process that drives two
+// GPUs must configure each.  ``cache`` is a zero-initialised static array of
+// one entry per device ordinal; it holds the largest value configured there
+// plus one.  ``set()`` runs under a process-wide lock, so two threads never
+// shrink an attribute under each other's launch.
+#include <atomic>
+#include <mutex>
+namespace cyr {
+constexpr int kMaxDevices = 64;
+using AttrCache = std::atomic<int>[kMaxDevices];
+
+inline int current_device_ordinal() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  return d;
+}
+
+template <typename Set>
+inline bool ensure_func_attr(AttrCache& cache, int want, Set&& set) {
+  std::atomic<int>& c = cache[current_device_ordinal()];
+  if (c.load(std::memory_order_acquire) > want) return true;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (c.load(std::memory_order_relaxed) > want) return true;
+  if (!set()) return false;
+  c.store(want + 1, std::memory_order_release);
+  return true;
+}
+}  // namespace cyr
