@@ -34,6 +34,19 @@
  *   weights blob (policy create/update): per layer W (out,in) row-major
  *     float64 followed by b (out) — the PSIMMLP1 payload order
  *     (neural.py:186-196).
+ *
+ * Threading
+ *   - every entry point taking a cyr_policy serialises on a per-policy
+ *     mutex: two host threads may call build_codebook (cyr_codebook_host) on
+ *     one policy concurrently and each gets its own slot's codebook (the
+ *     reference's numpy path is reentrant for a shared, read-only agent);
+ *     different policies run concurrently;
+ *   - device-wide synchronisation inside the library (weight updates,
+ *     destroy, buffer growth) first tells every resident slot server in the
+ *     process to leave, so it waits for real work only, never for a server's
+ *     idle timeout;
+ *   - cyr_policy_update / cyr_policy_sync wait for every launch on the device
+ *     before overwriting weights (no in-flight launch reads torn weights).
  */
 #ifndef CYRUS_B200_H
 #define CYRUS_B200_H
@@ -90,6 +103,22 @@ int cyr_policy_destroy(cyr_policy* policy);
  * (e.g. before timing other work on the device).  CYR_SLOT_SERVER=0 selects
  * the per-call graph launch instead. */
 int cyr_policy_quiesce(cyr_policy* policy);
+/* Stop every resident slot server of the process now (e.g. before a
+ * device-wide cudaDeviceSynchronize in the caller). */
+int cyr_quiesce_all(void);
+/* The reference's in-place weight semantics (Adam mutates agent.actor,
+ * neural.py:122-141) without a host-side compare on the call path: register
+ * the caller's host arrays (flatten order W0, b0, W1, b1, ...; float64,
+ * C-contiguous; counts = out*in, out, ...) — they are published now and
+ * must stay valid until unregistered (n = 0) or destroy.  Every
+ * cyr_codebook_host call then memcmp's them against the published snapshot
+ * WHILE the device computes, and on a difference republishes and recomputes
+ * (the answer always reflects the weights at call time). */
+int cyr_policy_watch(cyr_policy* policy, const double* const* arrays, const int64_t* counts,
+                     int32_t n);
+/* Compare the watched arrays now; republish when they changed
+ * (*changed = 1).  For the device batch entry points, which do not check. */
+int cyr_policy_sync(cyr_policy* policy, int32_t* changed);
 int cyr_policy_info(const cyr_policy* policy, int32_t* num_users, int32_t* n_sizes,
                     int32_t* precision);
 

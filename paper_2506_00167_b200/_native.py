@@ -34,6 +34,9 @@ SIGNATURES = {
     "cyr_policy_load": (_c_int, [ctypes.POINTER(_vp), _cp, _c_i32]),
     "cyr_policy_destroy": (_c_int, [_vp]),
     "cyr_policy_quiesce": (_c_int, [_vp]),
+    "cyr_quiesce_all": (_c_int, []),
+    "cyr_policy_watch": (_c_int, [_vp, _vp, _vp, _c_i32]),
+    "cyr_policy_sync": (_c_int, [_vp, _pi32]),
     "cyr_policy_info": (_c_int, [_vp, _pi32, _pi32, _pi32]),
     "cyr_actor_forward_device": (_c_int, [_vp, _vp, _c_i32, _c_i32, _c_i32, _vp, _vp]),
     "cyr_codebook_from_raw_device": (

@@ -18,6 +18,8 @@
 #include <cstring>
 #include <ctime>
 #include <map>
+#include <mutex>
+#include <set>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -93,6 +95,10 @@ unsigned long long* cyr_trace_buffer() {
 }
 
 struct cyr_policy {
+  // one caller at a time per policy (include/cyrus_b200.h "Threading"):
+  // every entry point that touches the host path, the slot server, the
+  // weights or the grown scratch buffers holds it
+  mutable std::recursive_mutex mu;
   int precision = CYR_FP32;
   std::vector<int> sizes;
   int E = 0;
@@ -146,15 +152,55 @@ struct cyr_policy {
     cyr::SlotMailbox* mb_dev = nullptr;  // its device alias
     cudaStream_t stream = nullptr;
     cudaEvent_t exited = nullptr;        // recorded after each server launch
-    bool running = false;
+    std::atomic<bool> running{false};
     std::tuple<int, int, int, int> key{};
     uint32_t seq = 0;                    // last request issued (== served, between calls)
   } srv;
+  // "check" weight sync in C (cyr_policy_watch): the caller's host arrays
+  // in flatten order (W0, b0, W1, b1, ... float64) and the snapshot last
+  // published from them; compared with memcmp while the device works
+  struct Watch {
+    std::vector<const double*> ptr;
+    std::vector<size_t> count;
+    std::vector<double> snap;
+  } watch;
 };
 
 extern "C" {
 static void slot_server_stop(cyr_policy* p);
 }
+
+// ---- process-wide registry of policies with a slot-server mailbox ----
+// A resident server holds its SMs until it idles out (20 ms), so a
+// device-wide synchronisation (cudaDeviceSynchronize, or cudaFree, which
+// implies one) would wait for every server in the process.  Before any such
+// call the library signals every registered server to leave now.  The
+// signal is only the mailbox's quit word (no policy lock is taken, so no
+// lock-order cycle); a request already posted is served before the server
+// sees it, and an owner whose server left relaunches it on its next call.
+namespace {
+std::mutex g_srv_mu;
+std::set<cyr_policy*> g_srv_policies;
+
+void stop_all_servers() {
+  std::lock_guard<std::mutex> lock(g_srv_mu);
+  std::vector<cyr_policy*> sig;
+  for (cyr_policy* q : g_srv_policies)
+    if (q->srv.running.load()) {
+      reinterpret_cast<volatile uint32_t*>(&q->srv.mb->quit)[0] = 1u;
+      sig.push_back(q);
+    }
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  for (cyr_policy* q : sig) cudaEventSynchronize(q->srv.exited);
+  for (cyr_policy* q : sig) reinterpret_cast<volatile uint32_t*>(&q->srv.mb->quit)[0] = 0u;
+}
+
+// every device-wide synchronisation inside the library goes through here
+cudaError_t device_sync_quiet() {
+  stop_all_servers();
+  return cudaDeviceSynchronize();
+}
+}  // namespace
 
 namespace {
 
@@ -241,6 +287,8 @@ int upload(cyr_policy* p, const double* blob) {
 }
 
 void release_host_path(cyr_policy* p) {
+  slot_server_stop(p);  // it writes p->cb_d
+  if (p->alloc_d || p->pin) stop_all_servers();  // the cudaFrees below synchronise the device
   for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
   p->graphs.clear();
   for (auto& kv : p->fused) {
@@ -337,6 +385,7 @@ int launch_actor_policy(const cyr_policy* p, const int32_t* alloc, int S, int N,
       cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
       cudaStreamIsCapturing(st, &cs);
       if (cs != cudaStreamCaptureStatusNone) return CYR_UNSUPPORTED;
+      if (p->wide_act_d) stop_all_servers();  // cudaFree synchronises the device
       cudaFree(p->wide_act_d);
       p->wide_act_d = nullptr;
       p->wide_act_bytes = 0;
@@ -357,6 +406,7 @@ int launch_actor_policy(const cyr_policy* p, const int32_t* alloc, int S, int N,
       cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
       cudaStreamIsCapturing(st, &cs);
       if (cs == cudaStreamCaptureStatusNone) {
+        if (p->wide_act_d) stop_all_servers();
         cudaFree(p->wide_act_d);
         p->wide_act_d = nullptr;
         p->wide_act_bytes = 0;
@@ -537,6 +587,7 @@ int cyr_mlp_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
 int cyr_mlp_forward_device(const cyr_policy* p, const double* x, int32_t cols, void* out,
                            void* stream) {
   if (!p || cols < 0 || (cols > 0 && (!x || !out))) return CYR_BAD_ARG;
+  std::lock_guard<std::recursive_mutex> lock(p->mu);
   const int rc = cyr_launch_actor_columns(simt_precision(p), p->desc, p->blob_d, nullptr, nullptr,
                                           x, cols, p->E, 1, 1, out, p->sm_count,
                                           static_cast<cudaStream_t>(stream));
@@ -548,6 +599,7 @@ int cyr_policy_actions_device(const cyr_policy* p, const int32_t* alloc, const i
                               const double* eps, int32_t R, int32_t N, int32_t L, int64_t* grants,
                               double* log_pi, double* b_out, int32_t* status, void* stream) {
   if (!p || p->generic || p->mode_t) return CYR_BAD_ARG;
+  std::lock_guard<std::recursive_mutex> lock(p->mu);
   int cap = 0;
   int rc = check_geometry(R, p->E, N, L, &cap);
   if (rc != CYR_OK) return rc;
@@ -579,11 +631,87 @@ int cyr_policy_actions_device(const cyr_policy* p, const int32_t* alloc, const i
   return rc;
 }
 
+namespace {
+// stop the policy's server, then wait for every launch that may still read
+// the old weights (the library's streams and the caller's: device-wide, with
+// every resident server told to leave first so the wait is only real work)
+int quiesce_for_upload(cyr_policy* p) {
+  slot_server_stop(p);
+  CYR_CUDA(device_sync_quiet());
+  return CYR_OK;
+}
+
+size_t blob_count(const cyr_policy* p) {
+  size_t n = 0;
+  for (size_t l = 0; l + 1 < p->sizes.size(); ++l)
+    n += (size_t)p->sizes[l] * p->sizes[l + 1] + p->sizes[l + 1];
+  return n;
+}
+
+// any watched host array differs from the snapshot last published from it
+bool watch_changed(const cyr_policy* p) {
+  const auto& w = p->watch;
+  size_t off = 0;
+  for (size_t i = 0; i < w.ptr.size(); ++i) {
+    if (std::memcmp(w.ptr[i], w.snap.data() + off, w.count[i] * sizeof(double)) != 0) return true;
+    off += w.count[i];
+  }
+  return false;
+}
+
+// snapshot the watched arrays and publish them
+int watch_republish(cyr_policy* p) {
+  auto& w = p->watch;
+  size_t off = 0;
+  for (size_t i = 0; i < w.ptr.size(); ++i) {
+    std::memcpy(w.snap.data() + off, w.ptr[i], w.count[i] * sizeof(double));
+    off += w.count[i];
+  }
+  const int rc = quiesce_for_upload(p);
+  return rc != CYR_OK ? rc : upload(p, w.snap.data());
+}
+}  // namespace
+
 int cyr_policy_update(cyr_policy* p, const double* weights_blob) {
   if (!p || !weights_blob) return CYR_BAD_ARG;
-  slot_server_stop(p);
-  CYR_CUDA(cudaDeviceSynchronize());  // no launch may still read the old weights
+  std::lock_guard<std::recursive_mutex> lock(p->mu);
+  const int rc = quiesce_for_upload(p);
+  if (rc != CYR_OK) return rc;
+  if (!p->watch.ptr.empty())  // an explicit publish is the new snapshot
+    std::memcpy(p->watch.snap.data(), weights_blob, p->watch.snap.size() * sizeof(double));
   return upload(p, weights_blob);
+}
+
+int cyr_policy_watch(cyr_policy* p, const double* const* arrays, const int64_t* counts,
+                     int32_t n) {
+  if (!p || n < 0 || (n > 0 && (!arrays || !counts))) return CYR_BAD_ARG;
+  std::lock_guard<std::recursive_mutex> lock(p->mu);
+  auto& w = p->watch;
+  if (n == 0) {
+    w.ptr.clear();
+    w.count.clear();
+    w.snap.clear();
+    return CYR_OK;
+  }
+  // flatten order: W_l (out*in) then b_l (out) for every layer
+  if ((size_t)n != 2 * (p->sizes.size() - 1)) return CYR_BAD_ARG;
+  for (int i = 0; i < n; ++i) {
+    const size_t l = (size_t)i / 2;
+    const int64_t want = i % 2 == 0 ? (int64_t)p->sizes[l] * p->sizes[l + 1] : p->sizes[l + 1];
+    if (counts[i] != want || !arrays[i]) return CYR_BAD_ARG;
+  }
+  w.ptr.assign(arrays, arrays + n);
+  w.count.assign(counts, counts + n);
+  w.snap.assign(blob_count(p), 0.0);
+  return watch_republish(p);
+}
+
+int cyr_policy_sync(cyr_policy* p, int32_t* changed) {
+  if (!p) return CYR_BAD_ARG;
+  std::lock_guard<std::recursive_mutex> lock(p->mu);
+  const bool c = !p->watch.ptr.empty() && watch_changed(p);
+  if (changed) *changed = c ? 1 : 0;
+  return c ? watch_republish(p) : CYR_OK;
 }
 
 int cyr_policy_load(cyr_policy** out, const char* path, int32_t precision) {
@@ -629,18 +757,31 @@ int cyr_policy_load(cyr_policy** out, const char* path, int32_t precision) {
 
 int cyr_policy_quiesce(cyr_policy* p) {
   if (!p) return CYR_BAD_ARG;
+  std::lock_guard<std::recursive_mutex> lock(p->mu);
   slot_server_stop(p);
+  return CYR_OK;
+}
+
+int cyr_quiesce_all(void) {
+  stop_all_servers();
   return CYR_OK;
 }
 
 int cyr_policy_destroy(cyr_policy* p) {
   if (!p) return CYR_OK;
-  slot_server_stop(p);
-  if (p->srv.stream) cudaStreamDestroy(p->srv.stream);
-  if (p->srv.exited) cudaEventDestroy(p->srv.exited);
-  if (p->srv.mb) cudaFreeHost(p->srv.mb);
-  cudaDeviceSynchronize();
-  release_host_path(p);
+  {
+    std::lock_guard<std::recursive_mutex> lock(p->mu);
+    slot_server_stop(p);
+    {
+      std::lock_guard<std::mutex> reg(g_srv_mu);  // nobody signals its mailbox from here on
+      g_srv_policies.erase(p);
+    }
+    device_sync_quiet();  // no launch still reads the policy's buffers
+    if (p->srv.stream) cudaStreamDestroy(p->srv.stream);
+    if (p->srv.exited) cudaEventDestroy(p->srv.exited);
+    if (p->srv.mb) cudaFreeHost(p->srv.mb);
+    release_host_path(p);
+  }
   if (p->stream) cudaStreamDestroy(p->stream);
   if (p->ev0) cudaEventDestroy(p->ev0);
   if (p->ev1) cudaEventDestroy(p->ev1);
@@ -662,6 +803,7 @@ int cyr_policy_info(const cyr_policy* p, int32_t* num_users, int32_t* n_sizes, i
 int cyr_actor_forward_device(const cyr_policy* p, const int32_t* alloc, int32_t S, int32_t N,
                              int32_t cap, void* raw, void* stream) {
   if (!p || p->mode_t || (S > 0 && (!alloc || !raw)) || N <= 0 || cap < 1) return CYR_BAD_ARG;
+  std::lock_guard<std::recursive_mutex> lock(p->mu);
   const int rc = launch_actor_policy(p, alloc, S, N, cap, raw, static_cast<cudaStream_t>(stream));
   if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
   return rc;
@@ -691,6 +833,7 @@ int cyr_codebook_device(const cyr_policy* p, const int32_t* alloc, const double*
                         int32_t N, int32_t L, int32_t* codebook, void* raw_workspace,
                         int32_t* status, void* stream) {
   if (!p || p->mode_t) return CYR_BAD_ARG;
+  std::lock_guard<std::recursive_mutex> lock(p->mu);
   int cap = 0;
   int rc = check_geometry(S, p->E, N, L, &cap);
   if (rc != CYR_OK) return rc;
@@ -730,12 +873,12 @@ static unsigned long long slot_server_idle_ns() {
 // synchronises the whole device, and before the policy changes)
 static void slot_server_stop(cyr_policy* p) {
   auto& sv = p->srv;
-  if (!sv.running) return;
+  if (!sv.running.load()) return;
   sv.mb->quit = 1u;
   std::atomic_thread_fence(std::memory_order_seq_cst);
   cudaEventSynchronize(sv.exited);
   sv.mb->quit = 0u;
-  sv.running = false;
+  sv.running.store(false);
 }
 
 static int slot_server_launch(cyr_policy* p, bool det, int S, int N, int L, int cap) {
@@ -748,7 +891,7 @@ static int slot_server_launch(cyr_policy* p, bool det, int S, int N, int L, int 
     return rc;
   }
   CYR_CUDA(cudaEventRecord(sv.exited, sv.stream));
-  sv.running = true;
+  sv.running.store(true);
   return CYR_OK;
 }
 
@@ -758,7 +901,7 @@ static int slot_server_launch(cyr_policy* p, bool det, int S, int N, int L, int 
 // request served).  CYR_UNSUPPORTED: geometry outside the server's range.
 static int slot_server_call(cyr_policy* p, const std::tuple<int, int, int, int>& key,
                             const int32_t* alloc, const double* eps, int S, int N, int L, int cap,
-                            int32_t* codebook, int64_t* device_ns) {
+                            int32_t* codebook, int64_t* device_ns, bool* stale) {
   auto& sv = p->srv;
   const int E = p->E;
   if (S * (cap + 1) * E > 512 || S * E > 256 || S * cap * E > 256) return CYR_UNSUPPORTED;
@@ -769,14 +912,17 @@ static int slot_server_call(cyr_policy* p, const std::tuple<int, int, int, int>&
     CYR_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&sv.mb_dev), sv.mb, 0));
     CYR_CUDA(cudaStreamCreateWithFlags(&sv.stream, cudaStreamNonBlocking));
     CYR_CUDA(cudaEventCreateWithFlags(&sv.exited, cudaEventDisableTiming));
+    std::lock_guard<std::mutex> reg(g_srv_mu);
+    g_srv_policies.insert(p);
   }
   const bool det = (eps == nullptr);
-  if (sv.running && sv.key != key) slot_server_stop(p);
-  if (sv.running && cudaEventQuery(sv.exited) == cudaSuccess) sv.running = false;  // idled out
+  if (sv.running.load() && sv.key != key) slot_server_stop(p);
+  if (sv.running.load() && cudaEventQuery(sv.exited) == cudaSuccess)
+    sv.running.store(false);  // idled out (or told to leave by stop_all_servers)
   std::memcpy(sv.mb->alloc, alloc, (size_t)S * E * 4);
   if (!det) std::memcpy(sv.mb->eps, eps, (size_t)S * cap * E * 8);
   sv.mb->status = CYR_OK;
-  if (!sv.running) {
+  if (!sv.running.load()) {
     const int rc = slot_server_launch(p, det, S, N, L, cap);
     if (rc != CYR_OK) return rc;
     sv.key = key;
@@ -786,6 +932,10 @@ static int slot_server_call(cyr_policy* p, const std::tuple<int, int, int, int>&
   std::atomic_thread_fence(std::memory_order_release);
   sv.mb->req_seq = next;
   host_stamp(1);
+  // "check" weight sync: compare the caller's host weights with the
+  // published snapshot while the cluster computes (~20 us of device work
+  // hides the memcmp); a stale answer is recomputed by the caller
+  if (stale) *stale = !p->watch.ptr.empty() && watch_changed(p);
   const auto t0 = std::chrono::steady_clock::now();
   for (unsigned spin = 1;; ++spin) {
     if (sv.mb->done_seq == next) break;
@@ -812,8 +962,10 @@ static int slot_server_call(cyr_policy* p, const std::tuple<int, int, int, int>&
   return CYR_OK;
 }
 
-int cyr_codebook_host(cyr_policy* p, const int32_t* alloc, const double* eps, int32_t S,
-                      int32_t N, int32_t L, int32_t* codebook, int64_t* device_ns) {
+static int codebook_host_once(cyr_policy* p, const int32_t* alloc, const double* eps, int32_t S,
+                              int32_t N, int32_t L, int32_t* codebook, int64_t* device_ns,
+                              bool* stale) {
+  if (stale) *stale = false;
   if (!p || p->mode_t || !alloc || !codebook) return CYR_BAD_ARG;
   int cap = 0;
   int rc = check_geometry(S, p->E, N, L, &cap);
@@ -846,10 +998,10 @@ int cyr_codebook_host(cyr_policy* p, const int32_t* alloc, const double* eps, in
   if (fused && slot_server_enabled()) {
     // latency path: the resident slot server (no launch per call)
     host_stamp(0);
-    const int src = slot_server_call(p, key, alloc, eps, S, N, L, cap, codebook, device_ns);
+    const int src = slot_server_call(p, key, alloc, eps, S, N, L, cap, codebook, device_ns, stale);
     if (src != CYR_UNSUPPORTED) return src;
   }
-  if (p->srv.running) slot_server_stop(p);  // the batch paths below synchronise streams
+  if (p->srv.running.load()) slot_server_stop(p);  // the batch paths below synchronise streams
   if (fused) {
     // latency path: ONE cluster launch (K2 + K3), inputs by value in the
     // launch parameters, codebook + status written straight to mapped pages
@@ -913,6 +1065,7 @@ int cyr_codebook_host(cyr_policy* p, const int32_t* alloc, const double* eps, in
       CYR_CUDA(cudaGraphLaunch(fit->second.exec, st));
       host_stamp(3);
     }
+    if (stale) *stale = !p->watch.ptr.empty() && watch_changed(p);  // overlaps the kernel
     CYR_CUDA(cudaEventSynchronize(p->ev1));
     host_stamp(4);
     const int32_t code = *reinterpret_cast<volatile int32_t*>(p->pin_status);
@@ -961,6 +1114,7 @@ int cyr_codebook_host(cyr_policy* p, const int32_t* alloc, const double* eps, in
     it = p->graphs.emplace(key, exec).first;
   }
   CYR_CUDA(cudaGraphLaunch(it->second, p->stream));
+  if (stale) *stale = !p->watch.ptr.empty() && watch_changed(p);  // overlaps the graph
   CYR_CUDA(cudaStreamSynchronize(p->stream));
   if (*p->pin_status != CYR_OK) return *p->pin_status;
   std::memcpy(codebook, p->pin_cb, (size_t)S * (cap + 1) * E * 4);
@@ -970,6 +1124,20 @@ int cyr_codebook_host(cyr_policy* p, const int32_t* alloc, const double* eps, in
     *device_ns = (int64_t)std::llround((double)ms * 1e6);
   }
   return CYR_OK;
+}
+
+int cyr_codebook_host(cyr_policy* p, const int32_t* alloc, const double* eps, int32_t S,
+                      int32_t N, int32_t L, int32_t* codebook, int64_t* device_ns) {
+  if (!p) return CYR_BAD_ARG;
+  std::lock_guard<std::recursive_mutex> lock(p->mu);
+  bool stale = false;
+  int rc = codebook_host_once(p, alloc, eps, S, N, L, codebook, device_ns, &stale);
+  if (stale) {  // the watched host weights changed in place: republish and recompute
+    const int r2 = watch_republish(p);
+    if (r2 != CYR_OK) return r2;
+    rc = codebook_host_once(p, alloc, eps, S, N, L, codebook, device_ns, nullptr);
+  }
+  return rc;
 }
 
 int cyr_enforce_batch_device(const double* b, const double* caps, const int64_t* demand,
@@ -1159,6 +1327,7 @@ int cyr_tree_mode_t_shard_device(const cyr_policy* p, const int32_t* alloc, cons
                                  int64_t count, int16_t* node_state, void* workspace,
                                  int32_t* status, void* stream) {
   if (!p || !p->mode_t) return CYR_BAD_ARG;
+  std::lock_guard<std::recursive_mutex> lock(p->mu);
   int cap = 0;
   int rc = check_geometry(S, p->E, N, L, &cap);
   if (rc != CYR_OK) return rc;

@@ -183,42 +183,115 @@ class DeviceMlp:
 
 
 class _Published:
-    __slots__ = ("policy", "snapshot", "actor_ref")
+    """A published actor (or MLP) and how its host weights are watched."""
+
+    __slots__ = ("policy", "actor_ref", "arrays", "watched", "snapshot")
 
     def __init__(self, actor, policy):
         self.policy = policy
         self.actor_ref = weakref.ref(actor)
-        self.snapshot = _snapshot(actor)
+        self.arrays = None      # the registered host arrays (identity + keep-alive)
+        self.watched = False    # registered with cyr_policy_watch (C-side compare)
+        self.snapshot = None    # Python-side snapshot for arrays C cannot watch
 
 
-def _snapshot(actor):
-    return [w.copy() for w in actor.weights] + [b.copy() for b in actor.biases]
+def _arrays(actor) -> list:
+    out = []
+    for w, b in zip(actor.weights, actor.biases):
+        out.append(w)
+        out.append(b)
+    return out
 
 
-def _same(actor, snap) -> bool:
-    arrays = list(actor.weights) + list(actor.biases)
-    if len(arrays) != len(snap):
-        return False
-    return all(a.shape == s.shape and np.array_equal(a, s) for a, s in zip(arrays, snap))
+def _watchable(arrays) -> bool:
+    return all(isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous
+               for a in arrays)
+
+
+def _snapshot(arrays):
+    return [a.copy() for a in arrays]
+
+
+def _same(arrays, snap) -> bool:
+    return len(arrays) == len(snap) and all(
+        a.shape == s.shape and np.array_equal(a, s) for a, s in zip(arrays, snap))
+
+
+def _watch(entry, arrays) -> None:
+    """Register the host arrays with the C library (publishes them now);
+    from then on every cyr_codebook_host call compares them with the
+    published snapshot while the device computes (include/cyrus_b200.h)."""
+    lib = _native.lib()
+    if _watchable(arrays):
+        n = len(arrays)
+        ptrs = (ctypes.c_void_p * n)(*[a.ctypes.data for a in arrays])
+        counts = np.asarray([a.size for a in arrays], dtype=np.int64)
+        _native.check(lib.cyr_policy_watch(entry.policy.handle, ptrs, counts.ctypes.data, n),
+                      "weight watch")
+        entry.watched, entry.snapshot = True, None
+    else:  # e.g. float32 or strided arrays: compare on the host instead
+        if entry.watched:
+            _native.check(lib.cyr_policy_watch(entry.policy.handle, None, None, 0))
+        entry.policy.update(_Params(arrays))
+        entry.watched, entry.snapshot = False, _snapshot(arrays)
+    entry.arrays = tuple(arrays)
+
+
+class _Params:
+    def __init__(self, arrays):
+        self.weights, self.biases = list(arrays[0::2]), list(arrays[1::2])
+
+
+def _sync(entry, actor, deferred: bool) -> None:
+    """"check" mode: the device copy follows in-place host updates.  Array
+    identity is checked here (cheap); contents are compared in C — inside
+    the codebook call itself when ``deferred`` (overlapped with the device
+    work), else now (cyr_policy_sync)."""
+    arrays = _arrays(actor)
+    reg = entry.arrays
+    if reg is None or len(reg) != len(arrays) or any(a is not b for a, b in zip(arrays, reg)):
+        _watch(entry, arrays)
+    elif entry.watched:
+        if not deferred:
+            _native.check(_native.lib().cyr_policy_sync(entry.policy.handle, None), "weight sync")
+    elif not _same(arrays, entry.snapshot):
+        entry.policy.update(_Params(arrays))
+        entry.snapshot = _snapshot(arrays)
+
+
+def _unwatch(entry) -> None:
+    if entry.watched:
+        _native.check(_native.lib().cyr_policy_watch(entry.policy.handle, None, None, 0))
+    entry.watched, entry.arrays, entry.snapshot = False, None, None
 
 
 _PUBLISHED: dict = {}
 
 
-def policy_for(agent, precision: str | None = None) -> DevicePolicy:
-    """Device policy for ``agent.actor`` (published on first use)."""
-    precision = precision or _DEFAULT_PRECISION
-    actor = agent.actor
-    key = (id(actor), precision)
-    entry = _PUBLISHED.get(key)
-    if entry is None or entry.actor_ref() is not actor:
-        entry = _Published(actor, DevicePolicy(actor, precision))
-        _PUBLISHED[key] = entry
-        weakref.finalize(actor, _PUBLISHED.pop, key, None)
-    elif _SYNC_MODE == "check" and not _same(actor, entry.snapshot):
-        entry.policy.update(actor)
-        entry.snapshot = _snapshot(actor)
+def _lookup(table, params, precision, make, deferred):
+    key = (id(params), precision)
+    entry = table.get(key)
+    if entry is None or entry.actor_ref() is not params:
+        entry = _Published(params, make(params, precision))
+        table[key] = entry
+        weakref.finalize(params, table.pop, key, None)
+        if _SYNC_MODE == "check":
+            _watch(entry, _arrays(params))
+    elif _SYNC_MODE == "check":
+        _sync(entry, params, deferred)
+    elif entry.watched:
+        _unwatch(entry)
     return entry.policy
+
+
+def policy_for(agent, precision: str | None = None, *, deferred: bool = False) -> DevicePolicy:
+    """Device policy for ``agent.actor`` (published on first use).  In the
+    default "check" mode the device copy follows in-place host updates
+    (Adam, neural.py:122-141).  ``deferred``: the caller's next call is
+    ``cyr_codebook_host``, which compares the weights itself while the
+    device computes (build_codebook)."""
+    return _lookup(_PUBLISHED, agent.actor, precision or _DEFAULT_PRECISION, DevicePolicy,
+                   deferred)
 
 
 _PUBLISHED_MLP: dict = {}
@@ -226,25 +299,19 @@ _PUBLISHED_MLP: dict = {}
 
 def mlp_for(params, precision: str | None = None) -> DeviceMlp:
     """Device copy of any MlpParams (e.g. ``agent.target1``), published on
-    first use and re-published after an in-place change in "check" mode."""
-    precision = precision or _DEFAULT_PRECISION
-    key = (id(params), precision)
-    entry = _PUBLISHED_MLP.get(key)
-    if entry is None or entry.actor_ref() is not params:
-        entry = _Published(params, DeviceMlp(params, precision))
-        _PUBLISHED_MLP[key] = entry
-        weakref.finalize(params, _PUBLISHED_MLP.pop, key, None)
-    elif _SYNC_MODE == "check" and not _same(params, entry.snapshot):
-        entry.policy.update(params)
-        entry.snapshot = _snapshot(params)
-    return entry.policy
+    first use and kept in sync with in-place changes in "check" mode."""
+    return _lookup(_PUBLISHED_MLP, params, precision or _DEFAULT_PRECISION, DeviceMlp, False)
 
 
 def publish(agent, precision: str | None = None) -> DevicePolicy:
     """Force a re-publish of ``agent.actor`` (use after training steps in
     "manual" sync mode)."""
     policy = policy_for(agent, precision)
-    key = (id(agent.actor), precision or _DEFAULT_PRECISION)
     policy.update(agent.actor)
-    _PUBLISHED[key].snapshot = _snapshot(agent.actor)
     return policy
+
+
+def quiesce_all() -> None:
+    """Stop every resident slot server of the process (before a device-wide
+    ``torch.cuda.synchronize()`` that should not wait for their idle exit)."""
+    _native.check(_native.lib().cyr_quiesce_all(), "quiesce")

@@ -25,6 +25,7 @@ from __future__ import annotations
 
 import ctypes
 import time
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -97,15 +98,19 @@ _BITGENS: dict = {}
 
 
 def branch_bitgens(streams, cap: int) -> tuple:
-    """bitgen_t addresses of streams.branch[1..cap] (cached per Streams)."""
+    """bitgen_t addresses of streams.branch[1..cap] (cached per Streams
+    object; the entry goes when the Streams object does)."""
     branch = streams.branch
-    entry = _BITGENS.get(id(streams))
+    key = id(streams)
+    entry = _BITGENS.get(key)
     if entry is not None and entry[0] is branch and all(
             branch.get(j) is g for j, g in enumerate(entry[1], start=1)):
         return entry[2]
     gens = tuple(branch[j] for j in range(1, cap + 1))
     addrs = tuple(g.bit_generator.ctypes.bit_generator.value for g in gens)
-    _BITGENS[id(streams)] = (branch, gens, addrs)
+    if entry is None:
+        weakref.finalize(streams, _BITGENS.pop, key, None)
+    _BITGENS[key] = (branch, gens, addrs)
     return addrs
 
 
@@ -117,7 +122,9 @@ def build_codebook(agent, schedule, streams, deterministic: bool = False, *,
     cap = cell.num_branches
     users = cell.num_embb
     if _fastpath is not None:
-        pol = policy if policy is not None else policy_for(agent, precision)
+        # weights are compared with the published copy inside the C call,
+        # overlapped with the device work ("check" mode, device.py)
+        pol = policy if policy is not None else policy_for(agent, precision, deferred=True)
         bitgens = None if deterministic else branch_bitgens(streams, cap)
         status, columns, gen_ns, dev_ns = _fastpath.codebook(
             pol.handle.value, schedule.alloc, bitgens, cell.total_scs, cell.urllc_sc_len, users)
@@ -127,7 +134,7 @@ def build_codebook(agent, schedule, streams, deterministic: bool = False, *,
     if alloc.shape != (users,):
         raise ValueError("input must be (input_dim, batch)")
     t0 = time.perf_counter_ns()
-    pol = policy if policy is not None else policy_for(agent, precision)
+    pol = policy if policy is not None else policy_for(agent, precision, deferred=True)
     eps = None
     if not deterministic:
         eps = np.empty((cap, users))
@@ -173,8 +180,8 @@ class CodebookEngine:
     (S, cap, E) float64 or None) and enqueues K2 -> K3 (-> K1 when
     ``with_tree``) on the current torch stream without synchronising;
     results land in ``self.codebooks`` / ``self.node_state``.
-    ``check()`` synchronises and raises the reference's exception for a
-    failing slot.
+    ``check()`` synchronises the stream of the last ``run`` (not the whole
+    device) and raises the reference's exception for a failing slot.
     """
 
     def __init__(self, policy: DevicePolicy, cell, max_slots: int, with_tree: bool = False,
@@ -212,7 +219,9 @@ class CodebookEngine:
             raise ValueError("more slots than the engine was sized for")
         if eps is not None and tuple(eps.shape[1:]) != (self.cap, self.users):
             raise ValueError("eps must be (S, cap, E)")
-        st = _native.stream_handle(stream)
+        torch = self.torch
+        self._stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        st = self._stream.cuda_stream
         cell = self.cell
         _native.check(lib.cyr_actor_forward_device(
             self.policy.handle, alloc.data_ptr(), s, cell.total_scs, self.cap,
@@ -229,10 +238,15 @@ class CodebookEngine:
         return self.codebooks[:s]
 
     def check(self) -> None:
-        self.torch.cuda.synchronize(self.device)
+        stream = getattr(self, "_stream", None)
+        if stream is None:
+            return
+        stream.synchronize()
         code = int(self.status[0].item())
         if code:
-            self.status.zero_()
+            with self.torch.cuda.stream(stream):
+                self.status.zero_()
+            stream.synchronize()
             _native.check(code, "codebook batch")
 
     def run_host(self, alloc_pinned, eps_pinned=None, out_pinned=None, stream=None):
@@ -251,6 +265,19 @@ class CodebookEngine:
         return out_pinned
 
 
+@dataclass
+class StreamBatch:
+    """Handle of one ``CodebookStream.submit``."""
+
+    ready: object          # event: codebooks are on the host
+    tree_ready: object     # event: the batch's node states are in HBM (or None)
+    engine: CodebookEngine
+    out: object            # pinned host codebooks (S, cap+1, E)
+    node_state: object     # device node states (S, nodes, Ep) of this batch, or None
+    slots: int
+    inputs: tuple          # device inputs, kept alive until their stream consumed them
+
+
 class CodebookStream:
     """Slot-after-slot O-DU serving loop on one GPU (the batch API a
     scheduler calls every slot).
@@ -261,10 +288,12 @@ class CodebookStream:
     arrival tree, left in HBM) when ``with_tree``.  Two batches are in
     flight: batch i+1's upload and actor/enforcement are issued while batch
     i's tree expansion and download run, on separate CUDA streams, with the
-    device buffers double-buffered.  ``wait(handle)`` returns ``out_pinned``
-    once that batch's codebooks are on the host, raising the reference's
-    exception for a failing slot.  Nothing is skipped: every batch does all
-    of its H2D, kernels and D2H.
+    device buffers — codebooks AND node states — double-buffered per batch.
+    ``wait(handle)`` returns ``out_pinned`` once that batch's codebooks are
+    on the host, raising the reference's exception for a failing slot.
+    ``tree(handle)`` waits for that batch's K1 and returns its node states
+    (valid until the second ``submit`` after it reuses the buffer set).
+    Nothing is skipped: every batch does all of its H2D, kernels and D2H.
     """
 
     def __init__(self, policy: DevicePolicy, cell, max_slots: int, with_tree: bool = True,
@@ -276,20 +305,26 @@ class CodebookStream:
         eng = self.engines[0]
         self.cell, self.cap, self.users, self.device = cell, eng.cap, eng.users, eng.device
         self.with_tree = with_tree
-        self.node_state = None
+        self.node_states = [None, None]
         if with_tree:
             from . import tree as _tree
             _tree.check_tree_geometry(cell)
-            self.node_state = torch.empty(
-                (int(max_slots), _tree.num_nodes(self.cap, cell.minislots),
-                 _tree.state_stride(self.users)), dtype=torch.int16, device=eng.device)
+            shape = (int(max_slots), _tree.num_nodes(self.cap, cell.minislots),
+                     _tree.state_stride(self.users))
+            self.node_states = [torch.empty(shape, dtype=torch.int16, device=eng.device)
+                                for _ in range(2)]
         self.s_main = torch.cuda.Stream(device=eng.device)  # uploads, K2, K3, downloads
         self.s_tree = torch.cuda.Stream(device=eng.device)  # K1
         self.free = [torch.cuda.Event() for _ in range(2)]  # buffer set reusable
         self.count = 0
         self.waited = 0
 
-    def submit(self, alloc_pinned, eps_pinned=None, out_pinned=None):
+    @property
+    def node_state(self):
+        """Node states of the most recent batch's buffer set (compatibility)."""
+        return self.node_states[(self.count - 1) % 2] if self.count else self.node_states[0]
+
+    def submit(self, alloc_pinned, eps_pinned=None, out_pinned=None) -> StreamBatch:
         torch = self.torch
         if self.count - self.waited >= 2:
             raise RuntimeError("at most two batches in flight: wait() for the oldest first")
@@ -301,7 +336,7 @@ class CodebookStream:
             out_pinned = torch.empty((s, self.cap + 1, self.users), dtype=torch.int32,
                                      pin_memory=True)
         main = self.s_main
-        main.wait_event(self.free[b])  # the tree of the batch that last used set b read it
+        main.wait_event(self.free[b])  # the tree of the batch that last used set b is done
         with torch.cuda.stream(main):
             alloc_d = alloc_pinned.to(eng.device, non_blocking=True)
             eps_d = None if eps_pinned is None else eps_pinned.to(eng.device, non_blocking=True)
@@ -311,27 +346,40 @@ class CodebookStream:
             out_pinned.copy_(eng.codebooks[:s], non_blocking=True)
             ready = torch.cuda.Event()
             ready.record(main)
+        tree_ready, states = None, None
         if self.with_tree:
+            states = self.node_states[b]
             tree_stream = self.s_tree
             tree_stream.wait_event(books)
             _native.check(_native.lib().cyr_tree_expand_device(
                 eng.codebooks.data_ptr(), s, self.users, self.cap, self.cell.minislots,
-                self.node_state.data_ptr(), tree_stream.cuda_stream), "tree")
+                states.data_ptr(), tree_stream.cuda_stream), "tree")
+            tree_ready = torch.cuda.Event()
+            tree_ready.record(tree_stream)
             self.free[b].record(tree_stream)
         else:
             self.free[b].record(main)
-        # keep the device inputs alive until their stream has consumed them
-        return (ready, eng, out_pinned, alloc_d, eps_d)
+        return StreamBatch(ready, tree_ready, eng, out_pinned,
+                           None if states is None else states[:s], s, (alloc_d, eps_d))
 
-    def wait(self, handle):
-        ready, eng, out_pinned, _, _ = handle
-        ready.synchronize()
+    def wait(self, handle: StreamBatch):
+        handle.ready.synchronize()
         self.waited += 1
+        eng = handle.engine
         code = int(eng.status[0].item())
         if code:
-            eng.status.zero_()
+            with self.torch.cuda.stream(self.s_main):
+                eng.status.zero_()
             _native.check(code, "codebook stream")
-        return out_pinned
+        return handle.out
+
+    def tree(self, handle: StreamBatch):
+        """Block until the batch's arrival tree is written; its node states
+        (S, nodes, Ep) int16 on the device."""
+        if handle.tree_ready is None:
+            raise ValueError("this stream was built with_tree=False")
+        handle.tree_ready.synchronize()
+        return handle.node_state
 
     def drain(self):
         """Block until every submitted batch (trees included) has finished."""

@@ -711,9 +711,11 @@ def test_mode_t_odd_users_matches_oracle(users, precision):
 
 
 def test_codebook_stream_matches_engine(golden):
-    """CodebookStream (two batches in flight, double-buffered, separate
-    streams for K1) returns every batch's codebooks exactly as the one-shot
-    engine does, and the tree of the last batch equals expand_tree's."""
+    """CodebookStream (two batches in flight, double-buffered codebooks AND
+    node states, separate streams for K1) returns every batch's codebooks
+    exactly as the one-shot engine does, and every batch's own tree (read
+    through ``tree(handle)`` while the next batch runs) equals
+    expand_tree's."""
     from paper_2506_00167_b200 import CodebookStream
     cfg = golden.config("cfg2")
     agent = cfg.agent()
@@ -724,18 +726,19 @@ def test_codebook_stream_matches_engine(golden):
     want = [ref.run(torch.from_numpy(a).cuda(), torch.from_numpy(e).cuda()).cpu().numpy()
             for a, e in batches]
     st = CodebookStream(pol, cfg.cell, max_slots=16, with_tree=True)
-    outs, pending = [], None
+    outs, trees, pending = [], [], None
     for a, e in batches:
         h = st.submit(torch.from_numpy(a).pin_memory(), torch.from_numpy(e).pin_memory())
         if pending is not None:
             outs.append(st.wait(pending).numpy().copy())
+            trees.append(st.tree(pending).clone())
         pending = h
     outs.append(st.wait(pending).numpy().copy())
+    trees.append(st.tree(pending).clone())
     st.drain()
-    for got, w in zip(outs, want):
+    for got, w, t in zip(outs, want, trees):
         assert np.array_equal(got, w)
-    last = tree.expand_tree(torch.from_numpy(want[-1]).cuda(), cfg.cell)
-    assert torch.equal(st.node_state[:16], last)
+        assert torch.equal(t, tree.expand_tree(torch.from_numpy(w).cuda(), cfg.cell))
     with pytest.raises(RuntimeError):
         a, e = batches[0]
         st.submit(torch.from_numpy(a).pin_memory(), torch.from_numpy(e).pin_memory())
