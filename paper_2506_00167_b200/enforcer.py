@@ -31,7 +31,7 @@ def _validate_projection(b, caps, demand):
     if (b < 0).any() or (caps < 0).any() or (demand < 0).any():
         raise ValueError("b, caps and demand must be non-negative")
     if (demand > caps.sum(axis=1) + 1e-9).any():
-        raise InfeasibleDemandError("demand exceeds total capacity")
+        raise _native.infeasible_error_class()("demand exceeds total capacity")
     return b, caps, demand
 
 
@@ -93,7 +93,7 @@ def apportion_batch(m_hat, caps, demand) -> np.ndarray:
     if np.any(demand < 0):
         raise ValueError("demand must be non-negative")
     if np.any(demand > caps.sum(axis=1)):
-        raise InfeasibleDemandError("demand exceeds total capacity")
+        raise _native.infeasible_error_class()("demand exceeds total capacity")
     rows, users = m_hat.shape
     want = np.zeros(rows, dtype=np.int64)
     want[:] = np.asarray(demand, dtype=np.int64)
@@ -119,7 +119,7 @@ def enforce_batch(b, caps, demands, with_details: bool = False):
     demands = np.asarray(demands, dtype=np.int64)
     b, caps, _ = _validate_projection(b, caps, demands.astype(np.float64))
     if np.any(demands > caps.sum(axis=1)):
-        raise InfeasibleDemandError("demand exceeds total capacity")
+        raise _native.infeasible_error_class()("demand exceeds total capacity")
     if b.shape[0] == 0:
         grants = np.zeros(b.shape, dtype=np.int64)
         return (grants, {}) if with_details else grants
