@@ -210,6 +210,18 @@ int cyr_mlp_create(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
  * out [cols][out] in the object's element type (float / double). */
 int cyr_mlp_forward_device(const cyr_policy* mlp, const double* x, int32_t cols, void* out,
                            void* stream);
+/* load_mlp (neural.py:211-225) of any PSIMMLP1 network file (a critic or
+ * target critic of an agent directory, sac.py:374-393) into a device MLP. */
+int cyr_mlp_load(cyr_policy** out, const char* path, int32_t precision);
+/* The sampling half of sac.actor_objective_grads (sac.py:265-270): actor on
+ * (alloc row, k) columns, tanh-Gaussian sample with its log-density
+ * (neural.py:153-165) and action_to_scs (neural.py:181-183) — WITHOUT the
+ * feasibility projection.  alloc [R][E] int32, k [R] int32 in 1..cap,
+ * eps [R][E] float64 (NULL: deterministic mean, log_pi 0) -> b_out [R][E]
+ * float64, log_pi [R] float64 (may be NULL), status [1]. */
+int cyr_policy_sample_device(const cyr_policy* policy, const int32_t* alloc, const int32_t* k,
+                             const double* eps, int32_t R, int32_t N, int32_t L, double* b_out,
+                             double* log_pi, int32_t* status, void* stream);
 
 /* ---- erasure LDPC peeling (decodability model "erasure_ldpc", §8(f) f2) --- */
 /* phy.peel_decode (phy.py:125-143) for B erasure patterns on one code graph

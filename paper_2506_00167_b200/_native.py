@@ -61,6 +61,9 @@ SIGNATURES = {
                                            _vp, _vp, _vp]),
     "cyr_mlp_create": (_c_int, [ctypes.POINTER(_vp), _vp, _c_i32, _vp, _c_i32]),
     "cyr_mlp_forward_device": (_c_int, [_vp, _vp, _c_i32, _vp, _vp]),
+    "cyr_mlp_load": (_c_int, [ctypes.POINTER(_vp), _cp, _c_i32]),
+    "cyr_policy_sample_device": (_c_int, [_vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i32, _vp, _vp,
+                                          _vp, _vp]),
     "cyr_tree_score_device": (_c_int, [_vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32,
                                        _vp, _vp, _vp, _vp]),
     "cyr_pf_schedule_device": (_c_int, [_vp, _vp, _c_i32, _c_i32, ctypes.c_double, _c_i32, _c_i32,

@@ -672,6 +672,37 @@ int watch_republish(cyr_policy* p) {
 }
 }  // namespace
 
+int cyr_policy_sample_device(const cyr_policy* p, const int32_t* alloc, const int32_t* k,
+                             const double* eps, int32_t R, int32_t N, int32_t L, double* b_out,
+                             double* log_pi, int32_t* status, void* stream) {
+  if (!p || p->generic || p->mode_t) return CYR_BAD_ARG;
+  std::lock_guard<std::recursive_mutex> lock(p->mu);
+  int cap = 0;
+  int rc = check_geometry(R, p->E, N, L, &cap);
+  if (rc != CYR_OK) return rc;
+  if (R == 0) return CYR_OK;
+  if (!alloc || !k || !b_out || !status) return CYR_BAD_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int E = p->E;
+  const size_t raw_b = ((size_t)R * 2 * E * p->elem + 255) / 256 * 256;
+  const size_t mat_b = ((size_t)R * E * 8 + 255) / 256 * 256;
+  unsigned char* ws = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&ws), raw_b + mat_b + (size_t)R * 8, st) !=
+      cudaSuccess)
+    return cuda_fail(cudaGetLastError(), "cudaMallocAsync(sample)");
+  double* caps = reinterpret_cast<double*>(ws + raw_b);
+  int64_t* demand = reinterpret_cast<int64_t*>(ws + raw_b + mat_b);
+  const int prec = simt_precision(p);
+  rc = cyr_launch_actor_columns(prec, p->desc, p->blob_d, alloc, k, nullptr, R, E, N, cap, ws,
+                                p->sm_count, st);
+  if (rc == CYR_OK)
+    rc = cyr_launch_actions_head(prec, ws, alloc, k, eps, R, E, L, b_out, caps, demand, log_pi,
+                                 status, st);
+  cudaFreeAsync(ws, st);
+  if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+  return rc;
+}
+
 int cyr_policy_update(cyr_policy* p, const double* weights_blob) {
   if (!p || !weights_blob) return CYR_BAD_ARG;
   std::lock_guard<std::recursive_mutex> lock(p->mu);
@@ -714,7 +745,20 @@ int cyr_policy_sync(cyr_policy* p, int32_t* changed) {
   return c ? watch_republish(p) : CYR_OK;
 }
 
+namespace {
+int load_checkpoint(cyr_policy** out, const char* path, int32_t precision, bool generic);
+}
+
 int cyr_policy_load(cyr_policy** out, const char* path, int32_t precision) {
+  return load_checkpoint(out, path, precision, false);
+}
+
+int cyr_mlp_load(cyr_policy** out, const char* path, int32_t precision) {
+  return load_checkpoint(out, path, precision, true);
+}
+
+namespace {
+int load_checkpoint(cyr_policy** out, const char* path, int32_t precision, bool generic) {
   if (!out || !path) return CYR_BAD_ARG;
   FILE* fh = std::fopen(path, "rb");
   if (!fh) {
@@ -752,8 +796,9 @@ int cyr_policy_load(cyr_policy** out, const char* path, int32_t precision) {
   if (data.size() > base + 8 * count) return fail("trailing bytes");
   std::vector<double> blob(count);
   std::memcpy(blob.data(), data.data() + base, 8 * count);  // little-endian host
-  return cyr_policy_create(out, sizes.data(), (int32_t)n_sizes, blob.data(), precision);
+  return policy_create_impl(out, sizes.data(), (int32_t)n_sizes, blob.data(), precision, generic);
 }
+}  // namespace
 
 int cyr_policy_quiesce(cyr_policy* p) {
   if (!p) return CYR_BAD_ARG;

@@ -142,6 +142,22 @@ class DeviceMlp:
                                                    _native.PRECISIONS[precision]), "mlp create")
         self._h = h
 
+    @classmethod
+    def from_checkpoint(cls, path, precision: str | None = None) -> "DeviceMlp":
+        """Publish a PSIMMLP1 network file (a critic / target critic of an
+        agent directory, sac.py:374-393) through the C loader."""
+        precision = precision or _DEFAULT_PRECISION
+        if precision == "bf16_tc":
+            precision = "fp32"
+        h = ctypes.c_void_p()
+        _native.check(_native.lib().cyr_mlp_load(ctypes.byref(h), os.fsencode(str(path)),
+                                                 _native.PRECISIONS[precision]), f"load {path}")
+        self = cls.__new__(cls)
+        self.precision = precision
+        self._h = h
+        self.sizes = list(load_mlp(path).sizes)
+        return self
+
     @property
     def handle(self):
         if self._h is None:

@@ -86,6 +86,9 @@ class SacAgent:
     critic2: MlpParams = None
     target1: MlpParams = None
     target2: MlpParams = None
+    adam_actor: "AdamState" = None     # optimiser states (sac.py:106-108; checkpoints only)
+    adam_c1: "AdamState" = None
+    adam_c2: "AdamState" = None
     extras: dict = field(default_factory=dict)
 
     @property
@@ -106,7 +109,8 @@ def make_agent(cell, cfg: AgentHyper, rng: np.random.Generator) -> SacAgent:
     c1 = init_mlp(critic_sizes, rng)
     c2 = init_mlp(critic_sizes, rng)
     return SacAgent(cell=cell, cfg=cfg, actor=actor, critic1=c1, critic2=c2,
-                    target1=c1.copy(), target2=c2.copy())
+                    target1=c1.copy(), target2=c2.copy(), adam_actor=AdamState.zeros_like(actor),
+                    adam_c1=AdamState.zeros_like(c1), adam_c2=AdamState.zeros_like(c2))
 
 
 def load_mlp(path) -> MlpParams:
@@ -143,6 +147,119 @@ def save_mlp(path, params: MlpParams) -> None:
         for w, b in zip(params.weights, params.biases):
             fh.write(np.ascontiguousarray(w, "<f8").tobytes())
             fh.write(np.ascontiguousarray(b, "<f8").tobytes())
+
+
+ADAM_MAGIC = b"PSIMADM1"
+
+
+@dataclass
+class AdamState:
+    """Adam moments per parameter (neural.py:87-121); checkpointed, not used
+    by the codebook path."""
+
+    m_w: list
+    v_w: list
+    m_b: list
+    v_b: list
+    t: int = 0
+
+    @classmethod
+    def zeros_like(cls, params: MlpParams) -> "AdamState":
+        return cls([np.zeros_like(w) for w in params.weights],
+                   [np.zeros_like(w) for w in params.weights],
+                   [np.zeros_like(b) for b in params.biases],
+                   [np.zeros_like(b) for b in params.biases], 0)
+
+
+def save_adam(path, state: AdamState, sizes) -> None:
+    """``PSIMADM1``: magic, u32 version, u32 n, n×u32 sizes, u64 step, then
+    m_w, v_w, m_b, v_b (row-major LE float64) — neural.py:228-236."""
+    sizes = [int(x) for x in sizes]
+    with open(path, "wb") as fh:
+        fh.write(ADAM_MAGIC)
+        fh.write(struct.pack("<II", MLP_FORMAT_VERSION, len(sizes)))
+        fh.write(struct.pack(f"<{len(sizes)}I", *sizes))
+        fh.write(struct.pack("<Q", int(state.t)))
+        for group in (state.m_w, state.v_w, state.m_b, state.v_b):
+            for arr in group:
+                fh.write(np.ascontiguousarray(arr, "<f8").tobytes())
+
+
+def load_adam(path, sizes) -> AdamState:
+    """Read a ``PSIMADM1`` optimiser state (neural.py:239-259), with the
+    reference's checks and messages."""
+    sizes = [int(x) for x in sizes]
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    if blob[:8] != ADAM_MAGIC:
+        raise ValueError(f"{path}: not an optimiser checkpoint")
+    version, n_sizes = struct.unpack_from("<II", blob, 8)
+    if version != MLP_FORMAT_VERSION:
+        raise ValueError(f"{path}: unsupported format version {version}")
+    stored = list(struct.unpack_from(f"<{n_sizes}I", blob, 16))
+    if stored != sizes:
+        raise ValueError(f"{path}: layer sizes do not match network")
+    off = 16 + 4 * n_sizes
+    (t,) = struct.unpack_from("<Q", blob, off)
+    off += 8
+    w_shapes = [(o, i) for i, o in zip(sizes[:-1], sizes[1:])]
+    b_shapes = [(o,) for o in sizes[1:]]
+    groups = []
+    for shapes in (w_shapes, w_shapes, b_shapes, b_shapes):
+        arrs = []
+        for shape in shapes:
+            count = int(np.prod(shape))
+            if off + 8 * count > len(blob):
+                raise ValueError("checkpoint truncated")
+            arrs.append(np.frombuffer(blob, "<f8", count, off).reshape(shape).copy())
+            off += 8 * count
+        groups.append(arrs)
+    if off != len(blob):
+        raise ValueError(f"{path}: trailing bytes")
+    return AdamState(*groups, t=int(t))
+
+
+NET_FILES = ("actor", "critic1", "critic2", "target1", "target2")
+
+
+def save_agent(directory, agent) -> None:
+    """One PSIMMLP1 file per network plus three PSIMADM1 optimiser states
+    (sac.py:361-371)."""
+    from pathlib import Path
+    directory = Path(directory)
+    directory.mkdir(parents=True, exist_ok=True)
+    nets = (agent.actor, agent.critic1, agent.critic2, agent.target1, agent.target2)
+    for name, net in zip(NET_FILES, nets):
+        save_mlp(directory / f"{name}.net", net)
+    for name, attr, net in (("actor", "adam_actor", agent.actor),
+                            ("critic1", "adam_c1", agent.critic1),
+                            ("critic2", "adam_c2", agent.critic2)):
+        state = getattr(agent, attr, None) or AdamState.zeros_like(net)
+        save_adam(directory / f"{name}.adam", state, net.sizes)
+
+
+def load_agent_host(directory, cell, cfg: AgentHyper) -> SacAgent:
+    """sac.load_agent (sac.py:374-393) on the host: the five networks with
+    the reference's presence and shape checks, and the optimiser states."""
+    from pathlib import Path
+    directory = Path(directory)
+    nets = {}
+    for name in NET_FILES:
+        path = directory / f"{name}.net"
+        if not path.exists():
+            raise FileNotFoundError(f"checkpoint file missing: {path}")
+        nets[name] = load_mlp(path)
+    e = cell.num_embb
+    if nets["actor"].sizes[0] != e + 1 or nets["actor"].sizes[-1] != 2 * e:
+        raise ValueError("actor checkpoint does not match cell dimensions")
+    if nets["critic1"].sizes[0] != 2 * e + 1:
+        raise ValueError("critic checkpoint does not match cell dimensions")
+    agent = SacAgent(cell=cell, cfg=cfg, actor=nets["actor"], critic1=nets["critic1"],
+                     critic2=nets["critic2"], target1=nets["target1"], target2=nets["target2"])
+    agent.adam_actor = load_adam(directory / "actor.adam", nets["actor"].sizes)
+    agent.adam_c1 = load_adam(directory / "critic1.adam", nets["critic1"].sizes)
+    agent.adam_c2 = load_adam(directory / "critic2.adam", nets["critic2"].sizes)
+    return agent
 
 
 def flatten_actor(actor) -> tuple[list, np.ndarray]:

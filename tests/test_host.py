@@ -101,3 +101,33 @@ def test_fastpath_noise_is_bit_identical_to_generator_draws():
     assert engine.branch_bitgens(a, 4) is addrs          # cached
     a.branch[2] = b.branch[2]
     assert engine.branch_bitgens(a, 4)[1] != addrs[1]    # re-derived after a swap
+
+
+def test_agent_checkpoint_roundtrip_matches_reference_bytes(tmp_path):
+    """f3 on the host: the reference-written agent directory loads with the
+    reference's digests, and save_agent writes byte-identical files."""
+    import json
+    import os
+    from paper_2506_00167_b200 import AgentHyper, CellConfig
+    from paper_2506_00167_b200.policy import NET_FILES, load_agent_host, save_agent
+    from tests.golden_util import weights_digest
+    golden = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    z = dict(np.load(os.path.join(golden, "agent_golden.npz")))
+    m = json.loads(str(z["meta_json"]))
+    cell = CellConfig(m["total_scs"], m["num_embb"], m["urllc_sc_len"], m["minislots"], 12)
+    hyper = AgentHyper(actor_hidden=tuple(m["actor_hidden"]),
+                       critic_hidden=tuple(m["critic_hidden"]), batch=m["batch"])
+    agent = load_agent_host(os.path.join(golden, "agent_ckpt"), cell, hyper)
+    assert weights_digest(agent.actor) == m["actor_sha256"]
+    assert agent.adam_actor.t == m["adam_t"]
+    save_agent(tmp_path, agent)
+    names = [f"{n}.net" for n in NET_FILES] + ["actor.adam", "critic1.adam", "critic2.adam"]
+    for name in names:
+        with open(os.path.join(golden, "agent_ckpt", name), "rb") as a, \
+                open(tmp_path / name, "rb") as b:
+            assert a.read() == b.read(), name
+    with pytest.raises(ValueError):
+        load_agent_host(os.path.join(golden, "agent_ckpt"),
+                        CellConfig(780, 4, 195, 7, 12), hyper)
+    with pytest.raises(FileNotFoundError):
+        load_agent_host(tmp_path / "missing", cell, hyper)
