@@ -589,7 +589,16 @@ def run_ours(args, rank, world, local_rank):
         kernels.append({k: roofline[k] for k in ("kernel", "bound", "achieved", "peak", "unit",
                                                  "frac")} | {"ms": roofline["kernel_ms"]})
 
-    cpu = cpu_leg(eng.codebooks, agent, cell, allocs, eps) if world == 1 else None
+    cpu = None
+    if world == 1:
+        # the optional bf16 tcgen05 actor on the same 1024 slots: its decision
+        # agreement with the reference rides on the CPU leg
+        pol_tc = DevicePolicy(agent.actor, "bf16_tc")
+        eng_tc = CodebookEngine(pol_tc, cell, max_slots=SLOTS, device=dev)
+        tc_books = eng_tc.run(alloc_d, eps_d).clone()
+        eng_tc.check()
+        pol_tc.close()
+        cpu = cpu_leg(eng.codebooks, agent, cell, allocs, eps, {"bf16_tc": tc_books})
     line = {
         "metric": METRIC, "value": total / (mean_ms * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms,
@@ -621,7 +630,7 @@ def run_ours(args, rank, world, local_rank):
     return 0
 
 
-def cpu_leg(gpu_books, agent, cell, allocs, eps, reps=3):
+def cpu_leg(gpu_books, agent, cell, allocs, eps, other_books=None, reps=3):
     """rank 0, N=1: the reference's CPU path (ReferenceCpu) on all host cores
     over this step's 1024 slots, timed over ``reps`` passes, and its
     codebooks compared with the GPU's (the timed steps' output).  Mismatched
@@ -652,6 +661,10 @@ def cpu_leg(gpu_books, agent, cell, allocs, eps, reps=3):
               "rows": int(diff.size - got.shape[0]), "mismatched": int(diff.sum()),
               "near_tie_logged": near, "mismatched_outside_near_tie": int(diff.sum()) - near,
               "rule": "codebook rows bit-exact except rows whose reference HH margin < 1e-5"}
+    for label, books in (other_books or {}).items():
+        b = books[:SLOTS].cpu().numpy()
+        parity[f"{label}_row_agreement_vs_reference"] = float(
+            (b[:, 1:] == want[:, 1:]).all(axis=2).mean())
     return cpu, parity
 
 

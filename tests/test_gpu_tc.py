@@ -1,10 +1,13 @@
 """GPU: the optional bf16 tcgen05 actor (precision "bf16_tc").
 
 Not a parity path: bf16 operands change logits at the 1e-3 level, so
-decisions are compared with the fp32 SIMT path as an AGREEMENT RATE
-(BASELINE configs[4]: "fp32 SIMT vs bf16 tcgen05 path with
-decision-agreement rate").  The logits must still be close to fp32 and the
-integer outputs must satisfy every feasibility contract.
+decisions are compared as an AGREEMENT RATE (BASELINE configs[4]: "fp32
+SIMT vs bf16 tcgen05 path with decision-agreement rate") — against the fp32
+path AND against the reference (golden codebooks frozen from punctsim; the
+Mode-T oracle for trees).  Gates sit just below the
+measured rates (a packing/swizzle bug that scrambles a few percent of the
+decisions fails them).  The logits must be close to fp32 and the integer
+outputs must satisfy every feasibility contract.
 """
 
 import json
@@ -82,7 +85,30 @@ def test_tc_codebook_agreement_and_feasibility(golden, name):
     rate = float(rows.mean())
     print(f"[bf16_tc] {name}: codebook-row agreement with fp32 = {rate:.4f}")
     _record(f"mode_r/{name}", rate)
-    assert rate > (0.95 if name == "cfg2" else 0.5)
+    # measured 0.9993 (cfg2) / 0.925 (stress, final-scale 1.0: trained-like logits)
+    assert rate >= (0.995 if name == "cfg2" else 0.90)
+
+
+@pytest.mark.parametrize("name,floor", [("cfg2", 0.99), ("cfg1", 0.99), ("stress", 0.88),
+                                        ("cfg5", 0.99)])
+def test_tc_codebooks_agree_with_reference(golden, name, floor):
+    """bf16 tcgen05 codebooks on the reference's own golden inputs (tiled to
+    >= 1024 branch columns so the tensor-core path runs) against the
+    codebooks the unmodified reference produced for them."""
+    cfg = golden.config(name)
+    agent = cfg.agent()
+    allocs, eps, want = cfg["alloc"], cfg["eps"], cfg["sto/codebook"]
+    reps = -(-1024 // (allocs.shape[0] * cfg.cell.num_branches))
+    al = np.tile(allocs, (reps, 1)).astype(np.int32)
+    ep = np.tile(eps, (reps, 1, 1))
+    eng = CodebookEngine(DevicePolicy(agent.actor, "bf16_tc"), cfg.cell, max_slots=al.shape[0])
+    got = eng.run(torch.from_numpy(al).cuda(), torch.from_numpy(ep).cuda())
+    eng.check()
+    got = got.cpu().numpy()[:allocs.shape[0]]
+    rate = float((got[:, 1:] == want[:, 1:]).all(axis=2).mean())
+    print(f"[bf16_tc] {name}: codebook-row agreement with the reference = {rate:.4f}")
+    _record(f"mode_r_vs_reference/{name}", rate)
+    assert rate >= floor
 
 
 def test_tc_mode_t_agreement(golden):
@@ -108,7 +134,18 @@ def test_tc_mode_t_agreement(golden):
     # levels with < 1024 columns (2 slots: levels 1-4) run fp32 SIMT and agree exactly
     four = tree.level_offsets(4, 7)[4]
     assert same[:, :four].all()
-    assert rate > 0.5
+    assert rate >= 0.97 and leaf_rate >= 0.97   # measured 0.984 / 0.983
+    # against the Mode-T oracle (the reference's actor, head and enforcer per
+    # node, float64): levels 1..5 of slot 0 (level 5 runs the tensor cores)
+    from oracle import mode_t
+    want = mode_t.mode_t_tree(actor.weights, actor.biases, allocs[0], mcs[0],
+                              cfg.cell.total_scs, cfg.cell.urllc_sc_len, 7, eps[0],
+                              stop_level=5)
+    n = want.shape[0]
+    ora = float((states["bf16_tc"][0, :n, :e] == want).all(axis=1).mean())
+    print(f"[bf16_tc] mode-T cfg2 levels 1-5: agreement with the oracle {ora:.4f}")
+    _record("mode_t_vs_oracle/cfg2_levels1_5", ora)
+    assert ora >= 0.97
 
 
 def test_tc_wide_mode_t_cfg5(golden):
@@ -130,7 +167,16 @@ def test_tc_wide_mode_t_cfg5(golden):
     rate = float(same.mean())
     print(f"[bf16_tc] mode-T cfg5: node agreement {rate:.4f}")
     _record("mode_t/cfg5_nodes", rate)
-    assert rate > 0.5
+    assert rate >= 0.995   # measured 1.0
+    from oracle import mode_t
+    want = mode_t.mode_t_tree(actor.weights, actor.biases, allocs[0], mcs[0],
+                              cfg.cell.total_scs, cfg.cell.urllc_sc_len, 7, eps[0],
+                              stop_level=3)
+    n = want.shape[0]
+    ora = float((states["bf16_tc"][0, :n, :e] == want).all(axis=1).mean())
+    print(f"[bf16_tc] mode-T cfg5 levels 1-3: agreement with the oracle {ora:.4f}")
+    _record("mode_t_vs_oracle/cfg5_levels1_3", ora)
+    assert ora >= 0.99
     # every child satisfies the per-level column contract against its parent
     l = cfg.meta["urllc_sc_len"]
     st = states["bf16_tc"][0, :, :e].astype(np.int64)
