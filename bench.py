@@ -818,12 +818,97 @@ def mode_t_cpu(cell, hidden, sample_levels, gpu_slot0=None, seed=11):
     return out
 
 
+def mode_t_cfg3(cell, hidden, total=SLOTS, chunk=32):
+    """BASELINE configs[2] in Mode T: 1024 independent slots, each with its
+    full north-star tree (actor on every node state), processed as
+    ``total / chunk`` tree batches back to back (the deepest level of one
+    32-slot batch is 2M actor columns; 1024 at once would need ~65 GB of
+    activation images).  Throughput per precision, CUDA events."""
+    import torch
+    from paper_2506_00167_b200 import DevicePolicy, substream, tree
+    actor = tree.make_mode_t_actor(cell, hidden, substream(0, "mode-t"))
+    allocs, eps = synthetic_inputs(cell, total, seed=12)
+    mcs = np.random.default_rng(12).integers(0, 6, size=allocs.shape).astype(np.int32)
+    al, mc, ep = (torch.from_numpy(x).cuda() for x in (allocs, mcs, eps))
+    cols = sum((cell.num_branches + 1) ** t for t in range(cell.minislots)) * cell.num_branches
+    sizes = tree.mode_t_sizes(cell, hidden)
+    flops = 2.0 * cols * total * sum(i * o for i, o in zip(sizes[:-1], sizes[1:]))
+    out = {"slots": total, "chunk_slots": chunk, "actor": "x".join(map(str, hidden)),
+           "nodes_per_slot": int(tree.num_nodes(cell.num_branches, cell.minislots)),
+           "actor_gflop": flops / 1e9}
+    for prec in ("bf16_tc", "fp32"):
+        pol = DevicePolicy(actor, prec)
+        buf = tree.build_tree_mode_t(pol, cell, al[:chunk], mc[:chunk], ep[:chunk])
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for c0 in range(0, total, chunk):
+            tree.build_tree_mode_t(pol, cell, al[c0:c0 + chunk], mc[c0:c0 + chunk],
+                                   ep[c0:c0 + chunk], out=buf)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        eff = flops / (ms * 1e-3) / 1e12
+        peak = 148 * 128 * 2 * 1965e6 / 1e12 if prec == "fp32" else measured_peak_bf16()
+        out[prec] = {"ms_for_1024_trees": ms, "trees_per_s": total / (ms * 1e-3),
+                     "actor_tflops_effective": eff, "effective_frac_of_peak": eff / peak}
+        pol.close()
+    return out
+
+
+def mode_t_latency(reps=60):
+    """One slot's whole Mode-T tree (cfg1: 3,279 nodes; cfg2: 97,655 nodes),
+    fp32 actor, against the 125 us numerology-3 budget: host-observed (call
+    to tree on the device, synchronised) and CUDA-event device time."""
+    import torch
+    from paper_2506_00167_b200 import CellConfig, DevicePolicy, substream, tree
+    out = {"budget_us": BUDGET_US}
+    for name, cell in (("cfg1", CellConfig(780, 4, 300)), ("cfg2", CellConfig(780, 10, 195))):
+        actor = tree.make_mode_t_actor(cell, HIDDEN, substream(0, "mode-t"))
+        allocs, eps = synthetic_inputs(cell, reps, seed=13)
+        mcs = np.random.default_rng(13).integers(0, 6, size=allocs.shape).astype(np.int32)
+        al, mc, ep = (torch.from_numpy(x).cuda() for x in (allocs, mcs, eps))
+        for prec in ("fp32", "bf16_tc"):
+            pol = DevicePolicy(actor, prec)
+            buf = tree.build_tree_mode_t(pol, cell, al[:1], mc[:1], ep[:1])
+            ws = torch.empty(max(1, pol_ws(pol, cell)), dtype=torch.uint8, device="cuda")
+            torch.cuda.synchronize()
+            host, dev = [], []
+            for r in range(reps):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                t0 = time.perf_counter_ns()
+                a.record()
+                tree.build_tree_mode_t(pol, cell, al[r:r + 1], mc[r:r + 1], ep[r:r + 1], out=buf,
+                                       workspace=ws)
+                b.record()
+                b.synchronize()
+                host.append((time.perf_counter_ns() - t0) / 1e3)
+                dev.append(a.elapsed_time(b) * 1e3)
+            out[f"{name}_{prec}"] = {"host_p50": float(np.median(host)),
+                                     "host_p99": float(np.percentile(host, 99)),
+                                     "device_p50": float(np.median(dev)),
+                                     "nodes": int(tree.num_nodes(cell.num_branches, 7))}
+            pol.close()
+    out["note"] = ("Mode T has no reference counterpart; bf16_tc runs the tensor cores only on "
+                   "levels of >= 1024 actor columns (cfg2 levels 6-7)")
+    return out
+
+
+def pol_ws(pol, cell, slots=1):
+    from paper_2506_00167_b200 import _native
+    return _native.lib().cyr_tree_mode_t_workspace_bytes(pol.handle, slots, cell.num_branches,
+                                                         cell.minislots)
+
+
 def mode_t_all(cell):
-    """cfg2 geometry (32 slots per tree batch) and the cfg5 large tree (configs[4])."""
+    """cfg2 geometry (32 slots per tree batch), cfg3 (1024 slots), the cfg5
+    large tree (configs[4]) and single-slot tree latency."""
     from paper_2506_00167_b200 import CellConfig
     cfg5 = CellConfig(780, 16, 130)
     out = {"cfg2": mode_t_run(cell, HIDDEN, 32),
            "cfg5": mode_t_run(cfg5, (1024, 1024, 1024), 1, reps=3, fp32_reps=1)}
+    out["cfg3"] = mode_t_cfg3(cell, HIDDEN)
+    out["latency"] = mode_t_latency()
     out["cfg2"]["cpu"] = mode_t_cpu(cell, HIDDEN, 4, out["cfg2"].pop("_slot0"))
     out["cfg5"]["cpu"] = mode_t_cpu(cfg5, (1024, 1024, 1024), 3, out["cfg5"].pop("_slot0"))
     return out

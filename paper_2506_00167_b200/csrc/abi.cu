@@ -350,6 +350,17 @@ constexpr long long kTcLayerCols = 32768;
 
 int simt_precision(const cyr_policy* p) { return p->precision == CYR_FP64 ? CYR_FP64 : CYR_FP32; }
 
+// narrow bf16 actors: the fused persistent tcgen05 MLP (actor_tc.cu) for
+// batches of >= kTcMinCols columns; CYR_TC_FUSED=0 restores the previous
+// one-CTA kernel / layer-by-layer split (A/B)
+bool use_tc_fused(const cyr_policy* p) {
+  static const bool on = [] {
+    const char* e = getenv("CYR_TC_FUSED");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on && p->tc_ok && !p->tc_wide && cyr_tc_fused_applies(p->desc, p->tc_npad);
+}
+
 // activation ping-pong bytes of the wide tensor-core actor for `cols` columns
 size_t wide_act_bytes(const cyr_policy* p, long long cols) {
   if (!p->tc_layers) return 0;
@@ -376,6 +387,11 @@ int launch_actor_wide(const cyr_policy* p, const int32_t* alloc, int S, int N, i
 // Mode-R actor for S slots with the policy's precision choice
 int launch_actor_policy(const cyr_policy* p, const int32_t* alloc, int S, int N, int cap, void* raw,
                         cudaStream_t st) {
+  if (use_tc_fused(p) && (long long)S * cap >= kTcMinCols)
+    return cyr_launch_actor_tc_fused(p->desc, p->tc_blob_d, p->tc_off, p->tc_npad,
+                                     static_cast<const float*>(p->blob_d), alloc, S, p->E, N, cap,
+                                     static_cast<float*>(raw), 0, nullptr, nullptr, 0, 0, 0, 0, 0,
+                                     0, 1.0, p->sm_count, st);
   if (p->tc_wide || (p->tc_layers && (long long)S * cap >= kTcLayerCols)) {
     // wide: any batch (the SIMT path streams MBs of weights per launch);
     // narrow: big batches
@@ -1403,7 +1419,13 @@ int cyr_tree_mode_t_shard_device(const cyr_policy* p, const int32_t* alloc, cons
     const long long par_off = prev_off < 0 ? -1 : prev_off + base;
     // K2: the actor on every (parent, branch) column of this level
     const long long cols = (long long)S * parents * cap;
-    if (p->tc_wide || (p->tc_layers && cols >= kTcLayerCols)) {
+    if (use_tc_fused(p) && cols >= kTcMinCols) {
+      rc = cyr_launch_actor_tc_fused(p->desc, p->tc_blob_d, p->tc_off, p->tc_npad,
+                                     static_cast<const float*>(p->blob_d), alloc, S, p->E, N, cap,
+                                     static_cast<float*>(workspace), 1, mcs, node_state, M, tau,
+                                     (int)parents, nodes, par_off, epad, mcs_scale, p->sm_count,
+                                     st, (int)base);
+    } else if (p->tc_wide || (p->tc_layers && cols >= kTcLayerCols)) {
       long long widest = 1;
       for (int t = 1; t < M; ++t) widest *= R;
       unsigned char* act = static_cast<unsigned char*>(workspace) +

@@ -19,9 +19,11 @@
 // The last layer's epilogue writes fp32 logits raw[col][2E] for K3.
 // Widths <= 256 (N of one MMA, 256 TMEM columns); wider actors use SIMT.
 #include "cyrus_internal.cuh"
+#include "actor_common.cuh"
 #include "cyrus_b200.h"
 
 #include <cuda_bf16.h>
+#include <cstdio>
 
 namespace cyr {
 
@@ -306,6 +308,398 @@ __global__ void __launch_bounds__(kTcThreads, 1) actor_tc_kernel(const TcLaunch 
   if (warp == 0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  }
+}
+
+// ------------------------------------------------------------ fused narrow
+// Narrow 3-layer actors (Mode T cfg1/cfg2: [3E+3, <=256, <=256, 2E]) on big
+// levels: ONE persistent kernel, one CTA per SM, every weight resident in
+// shared memory for the whole launch (W1 32 KB + W2 128 KB + W3 16 KB at
+// cfg2, loaded once by TMA), and the hidden activations never leave the SM:
+//
+//   features (smem, SW128)  --MMA1-->  D1 (TMEM, fp32)  --epi1-->  A2 (TMEM, bf16)
+//   A2 (TMEM)               --MMA2-->  D2 (TMEM)        --epi2-->  A3 (TMEM, bf16)
+//   A3 (TMEM)               --MMA3-->  D3 (TMEM)        --epi3-->  raw logits (HBM)
+//
+// MMA2 / MMA3 read their A operand straight from tensor memory
+// (tcgen05.mma ... [d], [a_tmem], b_desc: lane = batch column, column c =
+// K elements 2c, 2c+1), so the layer-by-layer path's 3 x 1 GB of HBM
+// activation images at the deepest cfg2 level become on-chip traffic.
+// TMEM (512 columns): D1 / D2 at [0, 256), A2 at [256, 384), A3 at [384, 512),
+// D3 at [256, 256 + N3) (A2 is dead once MMA2 has completed).
+// Roles:
+//   warps 0-15  epilogues: warp w reads TMEM lane quarter w % 4 and column
+//               part w / 4 of D1 / D2 (packed bias add, ReLU folded into the
+//               bf16x2 convert, tcgen05.st); warps 0-3 also run the head
+//               epilogue (bias, fp32 logits); each part arrives on its own
+//               barrier (a2p / a3p);
+//   warps 8..   feature builders: kFusedGroups groups of 4 warps, group g
+//               building the blocks i = g (mod groups) into A1 tile g (two
+//               groups: each has two blocks' time to build one);
+//   last warp   lane 0 issues the weight TMA and every MMA.
+// Each block's chain MMA1 -> epi1 -> MMA2 -> epi2 -> MMA3 -> epi3 is
+// serial; block b + 1's MMA1 is issued right after block b's MMA3, so it
+// overlaps the head epilogue, and the features are never on the critical path.
+// A second block in flight would need a second 256-column fp32 accumulator:
+// TMEM (512 columns) holds D + A2 + A3 of one block and no more.
+// Measured (scripts/fused_probe.py, 2M Mode-R columns, event timing): 852 us
+// vs 937 us for the layer-by-layer kernels; per block the tensor pipe is busy
+// ~4.7k of ~15k cycles (printf profile, CYR_FUSED_PROF): MMA2 2.9k, the
+// N = 32 head 1.3k (16 K steps, instruction-overhead bound), MMA1 0.5k; the
+// rest is the epilogue hand-offs.  A/B knobs (compile-time): CYR_FUSED_EPI
+// (8 / 16 epilogue warps: 16), CYR_FUSED_NSPLIT (MMA2 in N halves: slower),
+// CYR_FUSED_PERPART (MMA2 K steps per landed part: slower), CYR_FUSED_FADD2.
+#ifndef CYR_FUSED_GROUPS
+#define CYR_FUSED_GROUPS 1
+#endif
+#ifndef CYR_FUSED_EPI
+#define CYR_FUSED_EPI 16
+#endif
+constexpr int kFusedGroups = CYR_FUSED_GROUPS;     // feature-builder groups of 4 warps
+constexpr int kFusedEpi = CYR_FUSED_EPI;           // epilogue warps (8 or 16)
+constexpr int kFusedParts = kFusedEpi / 4;         // column parts per TMEM lane quarter
+constexpr int kFusedMmaWarp = kFusedEpi + 4 * kFusedGroups;
+constexpr int kFusedThreads = 32 * (kFusedMmaWarp + 1);
+constexpr int kFusedA2Col = 256, kFusedA3Col = 384, kFusedD3Col = 256;
+
+__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                          uint32_t idesc, int accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
+}
+
+struct FusedLayout {  // shared-memory carve-up (bytes from the 1024-aligned base)
+  uint32_t w_off[3], w_bytes[3], feat, bias, bars, total;
+};
+
+__host__ __device__ inline FusedLayout fused_layout(const ActorDesc& d, const int* npad) {
+  FusedLayout f{};
+  uint32_t off = 0;
+  for (int l = 0; l < 3; ++l) {
+    f.w_off[l] = off;
+    f.w_bytes[l] = (uint32_t)((d.layer[l].in + 63) / 64) * (uint32_t)npad[l] * 128u;
+    off += (f.w_bytes[l] + 1023u) & ~1023u;
+  }
+  f.feat = off;
+  off += (kFusedGroups < 2 ? 2 : kFusedGroups) * kTcM * 128;
+  f.bias = off;
+  off += (uint32_t)(npad[0] + npad[1] + npad[2]) * 4u;
+  off = (off + 7u) & ~7u;
+  f.bars = off;
+  off += 32 * 8 + 16;
+  f.total = off + 1024;  // alignment slack
+  return f;
+}
+
+// hidden-layer epilogue: D (fp32, TMEM cols [d_col, d_col + n)) -> bias, ReLU
+// -> bf16 pairs into A (TMEM cols [a_col, a_col + n / 2)); this warp's lane
+// quarter, column part `part` (of kFusedParts) of n
+__device__ __forceinline__ void fused_hidden_epi(uint32_t tmem, int quarter, int part, int n,
+                                                 int d_col, int a_col, const float* bias) {
+  const uint32_t lanes = (uint32_t)(quarter * 32) << 16;
+  const int c0 = part * (n / kFusedParts), c1 = c0 + n / kFusedParts;
+  for (int n0 = c0; n0 < c1; n0 += 32) {
+    uint32_t r[32];
+    tc_ld32(tmem + lanes + (uint32_t)(d_col + n0), r);
+    // per column pair: one packed fp32 add of the bias pair (add.rn.f32x2,
+    // bit-identical to two FADDs) and one convert with the ReLU folded in
+    // (cvt.rn.relu.bf16x2.f32: max(x, 0) then round, low half = even K)
+    const unsigned long long* b2 = reinterpret_cast<const unsigned long long*>(bias + n0);
+    uint32_t w[16];
+#ifndef CYR_FUSED_FADD2
+#define CYR_FUSED_FADD2 1
+#endif
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (!CYR_FUSED_FADD2) {
+        float v0 = __uint_as_float(r[2 * j]) + bias[n0 + 2 * j];
+        float v1 = __uint_as_float(r[2 * j + 1]) + bias[n0 + 2 * j + 1];
+        v0 = v0 > 0.f ? v0 : 0.f;
+        v1 = v1 > 0.f ? v1 : 0.f;
+        const __nv_bfloat162 pr = __floats2bfloat162_rn(v0, v1);
+        w[j] = *reinterpret_cast<const uint32_t*>(&pr);
+        continue;
+      }
+      unsigned long long v;
+      asm("add.rn.f32x2 %0, %1, %2;" : "=l"(v) : "l"(f32x2_pack(__uint_as_float(r[2 * j]),
+                                                               __uint_as_float(r[2 * j + 1]))),
+          "l"(b2[j]));
+      const float2 f = f32x2_unpack(v);
+      asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(w[j]) : "f"(f.y), "f"(f.x));
+    }
+    tc_st16(tmem + lanes + (uint32_t)(a_col + n0 / 2), w);
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const TcLaunch p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  const FusedLayout f = fused_layout(p.desc, p.tc_npad);
+  unsigned char* feat = base + f.feat;
+  float* sbias = reinterpret_cast<float*>(base + f.bias);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + f.bars);
+  uint64_t* wbar = bars;          // weights resident
+  uint64_t* ffull = bars + 1;     // [NB <= 4] feature tile ready (4 builder warps)
+  uint64_t* ffree = bars + 5;     // [NB] feature tile consumed (MMA1 commit)
+  uint64_t* d1full = bars + 9;    // MMA1 complete
+  uint64_t* a2p = bars + 10;      // [kFusedParts] epi1 part p complete (its 4 warps): the
+                                  // A2 K columns of part p are in TMEM, its D1 columns drained
+  uint64_t* d2full = bars + 14;   // [2] MMA2 complete, N half 0 / 1
+  uint64_t* a3p = bars + 16;      // [kFusedParts] epi2 part p complete
+  uint64_t* d3full = bars + 20;   // MMA3 complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n1 = p.tc_npad[0], n2 = p.tc_npad[1], n3 = p.tc_npad[2];
+  const int nblocks = (p.ncols + kTcM - 1) / kTcM;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 32) {
+    mbar_init(wbar, 1);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&ffull[i], 4);
+      mbar_init(&ffree[i], 1);
+    }
+    mbar_init(d1full, 1);
+    for (int q = 0; q < kFusedParts; ++q) {
+      mbar_init(&a2p[q], 4);
+      mbar_init(&a3p[q], 4);
+    }
+    mbar_init(&d2full[0], 1);
+    mbar_init(&d2full[1], 1);
+    mbar_init(d3full, 1);
+    fence_mbar_init();
+  }
+  {  // biases (fp32) -> shared, zero past each layer's width
+    const int nb[3] = {n1, n2, n3};
+    int o = 0;
+    for (int l = 0; l < 3; ++l) {
+      const int out = p.desc.layer[l].out;
+      const float* b = p.bias + p.desc.layer[l].b_off;
+      for (int i = tid; i < nb[l]; i += blockDim.x) sbias[o + i] = i < out ? b[i] : 0.f;
+      o += nb[l];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const float* bias1 = sbias;
+  const float* bias2 = sbias + n1;
+  const float* bias3 = sbias + n1 + n2;
+
+  constexpr int NB = kFusedGroups < 2 ? 2 : kFusedGroups;  // A1 tiles in flight
+  if (warp == kFusedMmaWarp) {
+    // ---------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t total = f.w_bytes[0] + f.w_bytes[1] + f.w_bytes[2];
+      mbar_expect_tx(wbar, total);
+      for (int l = 0; l < 3; ++l)
+        for (uint32_t c = 0; c < f.w_bytes[l]; c += 16384u) {
+          const uint32_t nbytes = min(16384u, f.w_bytes[l] - c);
+          bulk_g2s(base + f.w_off[l] + c, p.tc_blob + p.tc_off[l] + c, nbytes, wbar);
+        }
+      mbar_wait(wbar, 0);
+      tc_fence_after();
+      const uint32_t id1 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n1 >> 3) << 17) |
+                           ((uint32_t)(kTcM >> 4) << 24);
+#ifndef CYR_FUSED_NSPLIT
+#define CYR_FUSED_NSPLIT 0
+#endif
+      // CYR_FUSED_NSPLIT=1: MMA2 in two N halves, so the epilogue of half 0
+      // overlaps the MMAs of half 1 (A/B: slower, the halves read A2 twice)
+      constexpr int NH = CYR_FUSED_NSPLIT ? 2 : 1;
+      const uint32_t id2 = (1u << 4) | (1u << 7) | (1u << 10) |
+                           ((uint32_t)(n2 / NH >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
+      const uint32_t id3 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n3 >> 3) << 17) |
+                           ((uint32_t)(kTcM >> 4) << 24);
+      const uint32_t w1 = smem_u32(base + f.w_off[0]), w2 = smem_u32(base + f.w_off[1]),
+                     w3 = smem_u32(base + f.w_off[2]);
+      const uint32_t t2 = (uint32_t)n2 * 128u, t3 = (uint32_t)n3 * 128u;  // bytes per k tile
+      int i = 0;
+      for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
+        const int fb = i % NB;
+        const uint32_t ph = (uint32_t)(i & 1);
+#ifdef CYR_FUSED_PROF
+        const long long pt0 = clock64();
+#endif
+        mbar_wait(&ffull[fb], (uint32_t)((i / NB) & 1));
+        tc_fence_after();
+#ifdef CYR_FUSED_PROF
+        const long long pt1 = clock64();
+#endif
+        const uint32_t a1 = smem_u32(feat + fb * kTcM * 128);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          tc_mma(tmem, umma_desc_sw128(a1 + ks * 32), umma_desc_sw128(w1 + ks * 32), id1,
+                 ks > 0 ? 1 : 0);
+        tc_commit(&ffree[fb]);
+        tc_commit(d1full);
+#ifdef CYR_FUSED_PROF
+        const long long pt2 = clock64();
+#endif
+#ifdef CYR_FUSED_PROF
+        const long long pt3 = clock64();
+#endif
+        // MMA2's K steps of part q start as soon as epi1 part q has written
+        // them (the first parts finish well before the last)
+#ifndef CYR_FUSED_PERPART
+#define CYR_FUSED_PERPART 0
+#endif
+        // per part (A/B): CYR_FUSED_PERPART=1 starts K steps as parts land;
+        // 0 waits for every part before the first MMA
+        const int k2 = CYR_FUSED_PERPART ? n1 / 16 / kFusedParts : n1 / 16;
+        const int k3 = CYR_FUSED_PERPART ? n2 / 16 / kFusedParts : n2 / 16;
+        for (int h = 0; h < NH; ++h) {  // rows [h * n2/2, ...) of W2 start (n2/2/8) * 1 KB in
+          const uint32_t wb = w2 + (uint32_t)h * (uint32_t)(n2 / 16) * 1024u;
+          for (int ks = 0; ks < n1 / 16; ++ks) {
+            if (h == 0 && ks % k2 == 0) {
+              for (int q = ks / k2 * (kFusedParts * k2 * 16 / n1);
+                   q < (ks / k2 + 1) * (kFusedParts * k2 * 16 / n1); ++q)
+                mbar_wait(&a2p[q], ph);
+              tc_fence_after();
+            }
+            tc_mma_ts(tmem + (uint32_t)(h * (n2 / NH)), tmem + (uint32_t)(kFusedA2Col + ks * 8),
+                      umma_desc_sw128(wb + (uint32_t)(ks >> 2) * t2 + (uint32_t)(ks & 3) * 32),
+                      id2, ks > 0 ? 1 : 0);
+          }
+          tc_commit(&d2full[h]);
+        }
+        if (NH == 1) tc_commit(&d2full[1]);
+#ifdef CYR_FUSED_PROF
+        const long long pt4 = clock64();
+#endif
+#ifdef CYR_FUSED_PROF
+        const long long pt5 = clock64();
+#endif
+        for (int ks = 0; ks < n2 / 16; ++ks) {
+          if (ks % k3 == 0) {  // epi2 part q: its A3 K columns written, its D2 columns drained
+            for (int q = ks / k3 * (kFusedParts * k3 * 16 / n2);
+                 q < (ks / k3 + 1) * (kFusedParts * k3 * 16 / n2); ++q)
+              mbar_wait(&a3p[q], ph);
+            tc_fence_after();
+          }
+          tc_mma_ts(tmem + kFusedD3Col, tmem + (uint32_t)(kFusedA3Col + ks * 8),
+                    umma_desc_sw128(w3 + (uint32_t)(ks >> 2) * t3 + (uint32_t)(ks & 3) * 32), id3,
+                    ks > 0 ? 1 : 0);
+        }
+        tc_commit(d3full);
+#ifdef CYR_FUSED_PROF
+        const long long pt6 = clock64();
+        if (blockIdx.x == 0 && i >= 20 && i < 24)
+          printf("MMA blk %d: wait feat %lld, mma1 %lld, wait a2 %lld, mma2 %lld, wait a3 %lld, mma3 %lld\n",
+                 i, pt1 - pt0, pt2 - pt1, pt3 - pt2, pt4 - pt3, pt5 - pt4, pt6 - pt5);
+#endif
+      }
+    }
+    __syncwarp();
+  } else if (warp >= kFusedEpi) {
+    // ---------------------------------------------------- feature builders
+    const int grp = (warp - kFusedEpi) >> 2, row = (tid - 32 * kFusedEpi) & 127;
+    int i = 0;
+    for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
+      const int fb = i % NB;
+      if (kFusedGroups > 1 && fb != grp) continue;
+      if (i >= NB) mbar_wait(&ffree[fb], (uint32_t)(((i / NB) - 1) & 1));
+      tc_feature_tile(p, b * kTcM + row, 0, feat + fb * kTcM * 128, row);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ffull[fb]);
+    }
+  } else {
+    // ------------------------------------------------------------ epilogues
+    const int quarter = warp & 3, part = warp >> 2;
+    const int row = quarter * 32 + lane;  // TMEM lane = column within the block
+    const int out3 = p.desc.layer[2].out;
+    int i = 0;
+    for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
+      const uint32_t ph = (uint32_t)(i & 1);
+#ifdef CYR_FUSED_PROF
+      const long long q0 = clock64();
+#endif
+      mbar_wait(d1full, ph);
+      tc_fence_after();
+#ifdef CYR_FUSED_PROF
+      const long long q1 = clock64();
+#endif
+      fused_hidden_epi(tmem, quarter, part, n1, 0, kFusedA2Col, bias1);
+#ifdef CYR_FUSED_PROF
+      const long long q2 = clock64();
+#endif
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a2p[part]);
+      mbar_wait(&d2full[part >= kFusedParts / 2 ? 1 : 0], ph);
+      tc_fence_after();
+#ifdef CYR_FUSED_PROF
+      const long long q3 = clock64();
+#endif
+      fused_hidden_epi(tmem, quarter, part, n2, 0, kFusedA3Col, bias2);
+#ifdef CYR_FUSED_PROF
+      const long long q4 = clock64();
+#endif
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a3p[part]);
+      mbar_wait(d3full, ph);
+      tc_fence_after();
+#ifdef CYR_FUSED_PROF
+      const long long q5 = clock64();
+      if (blockIdx.x == 0 && i >= 20 && i < 24 && lane == 0 && (warp == 0 || warp == kFusedEpi - 1))
+        printf("EPI w%d blk %d: wait d1 %lld, epi1 %lld, wait d2 %lld, epi2 %lld, wait d3 %lld\n",
+               warp, i, q1 - q0, q2 - q1, q3 - q2, q4 - q3, q5 - q4);
+#endif
+      if (part == 0) {
+        const int col = b * kTcM + row;
+        const uint32_t lanes = (uint32_t)(quarter * 32) << 16;
+        for (int n0 = 0; n0 < n3; n0 += 16) {
+          uint32_t r[16];
+          tc_ld16(tmem + lanes + (uint32_t)(kFusedD3Col + n0), r);
+          if (col < p.ncols) {
+            float* dst = p.raw + (long long)col * out3;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (n0 + j < out3) dst[n0 + j] = __uint_as_float(r[j]) + bias3[n0 + j];
+          }
+        }
+      }
+      tc_fence_before();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
 
@@ -695,5 +1089,69 @@ int cyr_launch_actor_tc_layer(const cyr::ActorDesc& desc, const unsigned char* t
   else if (eg == 2) CYR_WIDE(false, false, 2);
   else CYR_WIDE(false, false, 1);
 #undef CYR_WIDE
+  return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
+}
+
+// the fused narrow kernel applies: 3 layers, first K <= 64, hidden widths
+// padded to multiples of 64 (<= 256), head <= 64 outputs, fits shared memory
+bool cyr_tc_fused_applies(const cyr::ActorDesc& desc, const int* tc_npad) {
+  if (desc.n_layers != 3 || desc.layer[0].in > 64) return false;
+  for (int l = 0; l < 2; ++l)  // hidden widths: whole 32-column epilogue chunks per part
+    if (tc_npad[l] > 256 || tc_npad[l] % (32 * cyr::kFusedParts) != 0) return false;
+  if (tc_npad[2] > 64) return false;
+  int max_smem = 0;
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                         cyr::current_device_ordinal());
+  return cyr::fused_layout(desc, tc_npad).total <= (uint32_t)max_smem;
+}
+
+int cyr_launch_actor_tc_fused(const cyr::ActorDesc& desc, const unsigned char* tc_blob,
+                              const long long* tc_off, const int* tc_npad, const float* bias_blob,
+                              const int32_t* alloc, int S, int E, int N, int cap, float* raw,
+                              int mode_t, const int32_t* mcs, const int16_t* node, int M, int tau,
+                              int parents, long long nodes_per_slot, long long parent_off,
+                              int epad, double mcs_scale, int sm_count, cudaStream_t stream,
+                              int parent_base) {
+  if (!cyr_tc_fused_applies(desc, tc_npad)) return CYR_UNSUPPORTED;
+  cyr::TcLaunch p{};
+  p.desc = desc;
+  for (int l = 0; l < desc.n_layers; ++l) {
+    p.tc_off[l] = tc_off[l];
+    p.tc_npad[l] = tc_npad[l];
+  }
+  p.tc_blob = tc_blob;
+  p.bias = bias_blob;
+  p.alloc = alloc;
+  p.raw = raw;
+  p.S = S;
+  p.E = E;
+  p.N = N;
+  p.cap = cap;
+  const long long ncols = mode_t ? (long long)S * parents * cap : (long long)S * cap;
+  if (ncols <= 0) return CYR_OK;
+  if (ncols >= (1ll << 31)) return CYR_UNSUPPORTED;
+  p.ncols = (int)ncols;
+  p.mode_t = mode_t;
+  p.node = node;
+  p.mcs = mcs;
+  p.nodes_per_slot = nodes_per_slot;
+  p.parent_off = parent_off;
+  p.parents = parents;
+  p.parent_base = parent_base;
+  p.tau = tau;
+  p.M = M;
+  p.epad = epad;
+  p.mcs_scale = mcs_scale;
+  const size_t smem = cyr::fused_layout(desc, tc_npad).total;
+  static cyr::AttrCache configured;
+  if (!cyr::ensure_func_attr(configured, (int)smem, [&] {
+        return cudaFuncSetAttribute(cyr::actor_tc_fused_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem) == cudaSuccess;
+      }))
+    return CYR_CUDA_ERROR;
+  const int nblocks = (p.ncols + cyr::kTcM - 1) / cyr::kTcM;
+  const int grid = std::min(nblocks, std::max(1, sm_count));
+  cyr::actor_tc_fused_kernel<<<grid, cyr::kFusedThreads, smem, stream>>>(p);
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
 }

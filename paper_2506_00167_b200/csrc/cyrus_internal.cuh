@@ -265,6 +265,14 @@ int cyr_launch_actor_tc(const cyr::ActorDesc& desc, const unsigned char* tc_blob
                         int mode_t, const int32_t* mcs, const int16_t* node, int M, int tau,
                         int parents, long long nodes_per_slot, long long parent_off, int epad,
                         double mcs_scale, cudaStream_t stream, int parent_base = 0);
+bool cyr_tc_fused_applies(const cyr::ActorDesc& desc, const int* tc_npad);
+int cyr_launch_actor_tc_fused(const cyr::ActorDesc& desc, const unsigned char* tc_blob,
+                              const long long* tc_off, const int* tc_npad, const float* bias_blob,
+                              const int32_t* alloc, int S, int E, int N, int cap, float* raw,
+                              int mode_t, const int32_t* mcs, const int16_t* node, int M, int tau,
+                              int parents, long long nodes_per_slot, long long parent_off,
+                              int epad, double mcs_scale, int sm_count, cudaStream_t stream,
+                              int parent_base = 0);
 int cyr_launch_actor_tc_layer(const cyr::ActorDesc& desc, const unsigned char* tc_blob,
                               long long w_off, int npad, int l, const float* bias_blob,
                               const int32_t* alloc, int S, int E, int N, int cap, float* raw,

@@ -188,3 +188,31 @@ def test_tc_wide_mode_t_cfg5(golden):
         assert (grants[:, 0] == 0).all()
         for k in range(1, 7):
             assert (grants[:, k].sum(axis=1) == k * l).all()
+
+
+def test_fused_tc_mlp_equals_layer_path(golden):
+    """The fused persistent tcgen05 MLP (bf16 operands in SMEM and TMEM, fp32
+    accumulation) against the previous one-CTA / layer-by-layer kernels
+    (CYR_TC_FUSED=0, read once per process, hence a subprocess): same bf16
+    operands, same K order per accumulator, so the logits must be equal to
+    fp32 rounding of the bias add."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, %r);"
+        "from tests.golden_util import Golden; from tests.test_gpu_tc import _inputs, _logits;"
+        "from paper_2506_00167_b200 import DevicePolicy;"
+        "cfg = Golden.load().config('cfg2'); a, _ = _inputs(cfg, 2000);"
+        "x = _logits(DevicePolicy(cfg.agent().actor, 'bf16_tc'), cfg.cell, a);"
+        "np.save(sys.argv[1], x)" % ROOT)
+    outs = {}
+    for flag in ("1", "0"):
+        path = os.path.join(ROOT, "gpurun_out", f"fused_{flag}.npy")
+        os.makedirs(os.path.dirname(path), exist_ok=True)
+        env = dict(os.environ, CYR_TC_FUSED=flag)
+        subprocess.run([sys.executable, "-c", code, path], env=env, check=True, cwd=ROOT)
+        outs[flag] = np.load(path)
+    scale = np.abs(outs["0"]).max(axis=1, keepdims=True)
+    worst = float((np.abs(outs["1"] - outs["0"]) / scale).max())
+    print(f"[bf16_tc] fused vs layer path: worst |dlogit|/max|col| = {worst:.2e}")
+    assert worst < 1e-6
