@@ -300,6 +300,16 @@ def _lookup(table, params, precision, make, deferred):
     return entry.policy
 
 
+def fast_entry(actor, precision: str | None = None):
+    """The published entry of ``actor`` when the drop-in call can skip
+    ``policy_for`` ("check" mode with the arrays registered in C): the C
+    fast path then checks the arrays' identity itself.  None otherwise."""
+    e = _PUBLISHED.get((id(actor), precision or _DEFAULT_PRECISION))
+    if e is None or not e.watched or _SYNC_MODE != "check" or e.actor_ref() is not actor:
+        return None
+    return e
+
+
 def policy_for(agent, precision: str | None = None, *, deferred: bool = False) -> DevicePolicy:
     """Device policy for ``agent.actor`` (published on first use).  In the
     default "check" mode the device copy follows in-place host updates

@@ -31,6 +31,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native
+from . import device as _device
 from .device import DevicePolicy, policy_for
 from .seeding import substream
 
@@ -97,21 +98,30 @@ def draw_branch_noise(streams, cap: int, num_users: int, slots: int = 1) -> np.n
 _BITGENS: dict = {}
 
 
-def branch_bitgens(streams, cap: int) -> tuple:
-    """bitgen_t addresses of streams.branch[1..cap] (cached per Streams
-    object; the entry goes when the Streams object does)."""
-    branch = streams.branch
+def _bitgen_entry(streams, cap: int) -> tuple:
+    """(branch dict, generators of j = 1..cap, their bitgen_t addresses),
+    cached per Streams object (the entry goes when the Streams object
+    does); the C fast path re-checks the generators' identity every call."""
     key = id(streams)
     entry = _BITGENS.get(key)
-    if entry is not None and entry[0] is branch and all(
+    branch = streams.branch
+    if entry is not None and entry[0] is branch and len(entry[1]) == cap and all(
             branch.get(j) is g for j, g in enumerate(entry[1], start=1)):
-        return entry[2]
+        return entry
     gens = tuple(branch[j] for j in range(1, cap + 1))
     addrs = tuple(g.bit_generator.ctypes.bit_generator.value for g in gens)
-    if entry is None:
+    if key not in _BITGENS:
         weakref.finalize(streams, _BITGENS.pop, key, None)
-    _BITGENS[key] = (branch, gens, addrs)
-    return addrs
+    entry = _BITGENS[key] = (branch, gens, addrs)
+    return entry
+
+
+def branch_bitgens(streams, cap: int) -> tuple:
+    """bitgen_t addresses of streams.branch[1..cap]."""
+    return _bitgen_entry(streams, cap)[2]
+
+
+_STALE_ARRAYS, _STALE_GENS = -100, -101
 
 
 def build_codebook(agent, schedule, streams, deterministic: bool = False, *,
@@ -119,17 +129,43 @@ def build_codebook(agent, schedule, streams, deterministic: bool = False, *,
     """All branches of one slot on the GPU: actor, head, KL projection,
     Huntington-Hill — one coupled enforcement per slot (engine.py:97-116)."""
     cell = agent.cell
+    if _fastpath is not None:
+        # per-call bookkeeping in C: the registered weight arrays must still
+        # be the actor's (identity), the branch generators the cached ones;
+        # contents are compared by the library while the device computes
+        actor = agent.actor
+        branch = None if deterministic else streams.branch
+        for _ in range(3):
+            arrays = None
+            if policy is not None:
+                pol = policy
+            else:
+                entry = _device.fast_entry(actor, precision)
+                if entry is None:
+                    pol = policy_for(agent, precision, deferred=True)
+                    entry = _device.fast_entry(actor, precision)
+                else:
+                    pol = entry.policy
+                if entry is not None:
+                    arrays = entry.arrays
+            gens = addrs = None
+            if branch is not None:
+                _, gens, addrs = _bitgen_entry(streams, cell.num_branches)
+            status, columns, gen_ns, dev_ns = _fastpath.codebook2(
+                pol.handle.value, schedule.alloc, branch, gens, addrs, cell.total_scs,
+                cell.urllc_sc_len, cell.num_embb, actor.weights, actor.biases, arrays)
+            if status == _STALE_ARRAYS:
+                policy_for(agent, precision, deferred=True)   # re-register (republishes)
+                continue
+            if status == _STALE_GENS:
+                _BITGENS.pop(id(streams), None)
+                continue
+            if status:
+                _native.check(status, "build_codebook")
+            return Codebook(columns=columns, gen_ns=gen_ns, device_ns=dev_ns)
+        raise RuntimeError("build_codebook: weight arrays or branch generators keep changing")
     cap = cell.num_branches
     users = cell.num_embb
-    if _fastpath is not None:
-        # weights are compared with the published copy inside the C call,
-        # overlapped with the device work ("check" mode, device.py)
-        pol = policy if policy is not None else policy_for(agent, precision, deferred=True)
-        bitgens = None if deterministic else branch_bitgens(streams, cap)
-        status, columns, gen_ns, dev_ns = _fastpath.codebook(
-            pol.handle.value, schedule.alloc, bitgens, cell.total_scs, cell.urllc_sc_len, users)
-        _native.check(status, "build_codebook")
-        return Codebook(columns=columns, gen_ns=gen_ns, device_ns=dev_ns)
     alloc = np.ascontiguousarray(schedule.alloc, dtype=np.int32)
     if alloc.shape != (users,):
         raise ValueError("input must be (input_dim, batch)")

@@ -115,6 +115,7 @@ def test_device_sync_does_not_wait_for_server_idle(golden):
     sched = _schedules(cfg, 1)[0]
     streams = make_streams(0, cfg.cell.num_branches)
     critic = DeviceMlp(agent.target1, "fp32")
+    torch.cuda.synchronize()  # torch's own lazy CUDA init stays out of the timed sync below
     for _ in range(5):
         build_codebook(agent, sched, streams)            # server resident now
         t0 = time.perf_counter()
@@ -143,3 +144,19 @@ def test_policy_destroy_while_another_server_runs(golden):
     assert build_codebook(a1, sched, make_streams(3, cfg.cell.num_branches)).columns == \
         build_codebook(a1, sched, make_streams(3, cfg.cell.num_branches)).columns
     policy_for(a1).quiesce()
+
+
+def test_replaced_branch_generator_is_used(golden):
+    """The C fast path checks that every streams.branch[j] is still the
+    generator it cached; a replaced generator is picked up (its draws)."""
+    cfg = golden.config("cfg2")
+    agent = cfg.agent()
+    sched = _schedules(cfg, 1)[0]
+    a = make_streams(1, cfg.cell.num_branches)
+    b = make_streams(1, cfg.cell.num_branches)
+    assert build_codebook(agent, sched, a).columns == build_codebook(agent, sched, b).columns
+    other = make_streams(9, cfg.cell.num_branches)
+    a.branch[2] = other.branch[2]
+    b.branch[2] = make_streams(9, cfg.cell.num_branches).branch[2]
+    assert build_codebook(agent, sched, a).columns == build_codebook(agent, sched, b).columns
+    policy_for(agent).quiesce()
