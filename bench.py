@@ -964,6 +964,16 @@ def latency_run(agent, cell, allocs, n, pol_batch=None, dev=None):
     st = _time_calls_updating(agent, scheds, streams, max(200, n // 20))
     out["stochastic_weights_changing"] = st
     policy_for(agent).quiesce()
+    # republish cost alone (cyr_policy_update: device-wide quiesce, raw copy,
+    # on-device pack of every layout), the 2x256 fp32 actor
+    ups = []
+    for _ in range(50):
+        t0 = time.perf_counter_ns()
+        policy_for(agent).update(agent.actor)
+        ups.append((time.perf_counter_ns() - t0) / 1e3)
+    out["republish_us"] = {"p50": float(np.median(ups)), "max": float(np.max(ups)),
+                           "what": "DevicePolicy.update (cyr_policy_update), 2x256 fp32 actor, "
+                                   "idle device"}
     if pol_batch is not None:
         out["stochastic_under_batch_load"] = _latency_under_load(agent, cell, scheds, streams,
                                                                  pol_batch, allocs, dev,

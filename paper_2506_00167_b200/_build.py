@@ -23,7 +23,7 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build", "cyrus_b200")
 LIB = os.path.join(PKG, "libcyrus_b200.so")
 SOURCES = ("abi.cu", "actor.cu", "actor_gemm.cu", "actor_tc.cu", "codebook.cu", "tree.cu",
-           "scheduler.cu", "ldpc.cu")
+           "scheduler.cu", "ldpc.cu", "pack.cu")
 HEADERS = ("cyrus_internal.cuh", "projection.cuh", "projection_lane.cuh", "actor_common.cuh")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

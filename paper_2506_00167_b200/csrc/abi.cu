@@ -39,6 +39,8 @@ int cuda_fail(cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
   } while (0)
 
+int simt_precision_of(int precision) { return precision == CYR_FP64 ? CYR_FP64 : CYR_FP32; }
+
 int sm_count_of_current_device() {
   static int cache[64] = {0};
   int dev = 0;
@@ -120,6 +122,8 @@ struct cyr_policy {
   bool tc_layers = false;            // layer-by-layer kernels usable (wide, or narrow big levels)
   int tc_act_k = 0;                  // widest hidden width rounded to 64
   mutable unsigned char* wide_act_d = nullptr;  // Mode-R activation scratch (grown on demand)
+  double* raw_stage_d = nullptr;     // raw float64 weights blob (device staging for pack.cu)
+  cudaStream_t up_stream = nullptr;  // weight uploads
   mutable size_t wide_act_bytes = 0;
   int sm_count = 148;
   // host path
@@ -162,7 +166,8 @@ struct cyr_policy {
   struct Watch {
     std::vector<const double*> ptr;
     std::vector<size_t> count;
-    std::vector<double> snap;
+    double* snap = nullptr;  // pinned: the upload DMA reads it directly
+    size_t snap_n = 0;
   } watch;
 };
 
@@ -204,85 +209,28 @@ cudaError_t device_sync_quiet() {
 
 namespace {
 
-// W (out,in) row-major float64 + b -> Wt [in][out_pad] + b in the policy dtype
-template <typename T>
-void pack_blob(const cyr_policy& p, const double* src, std::vector<T>& dst) {
-  dst.assign(p.blob_elems, T(0));
-  const int vec = 16 / (int)sizeof(T);
-  size_t off = 0;
-  for (int l = 0; l < p.desc.n_layers; ++l) {
-    const cyr::LayerDesc& L = p.desc.layer[l];
-    for (int o = 0; o < L.out; ++o)
-      for (int i = 0; i < L.in; ++i)
-        dst[L.w_off + (size_t)i * L.out_pad + o] = (T)src[off + (size_t)o * L.in + i];
-    for (int o = 0; o < L.out; ++o)
-      for (int i = 0; i < L.in; ++i)
-        dst[L.wr_off + (size_t)o * L.in_pad + i] = (T)src[off + (size_t)o * L.in + i];
-    for (int o = 0; o < L.out; ++o) {
-      const int oo = o % L.pw, g = L.pw / 8, v = vec;
-      const int og = oo % g, a = oo / g;
-      const int pos = L.pw > 64 ? (a / v) * g * v + og * v + a % v : oo;
-      for (int i = 0; i < L.in; ++i)
-        dst[L.wp_off + ((size_t)(o / L.pw) * L.in + i) * L.pw + pos] =
-            (T)src[off + (size_t)o * L.in + i];
-    }
-    off += (size_t)L.out * L.in;
-    for (int o = 0; o < L.out; ++o) dst[L.b_off + o] = (T)src[off + o];
-    off += L.out;
-  }
+size_t blob_count(const cyr_policy* p) {
+  size_t n = 0;
+  for (size_t l = 0; l + 1 < p->sizes.size(); ++l)
+    n += (size_t)p->sizes[l] * p->sizes[l + 1] + p->sizes[l + 1];
+  return n;
 }
 
-uint16_t f32_to_bf16_rne(float f) {
-  uint32_t u;
-  std::memcpy(&u, &f, 4);
-  if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fc0;
-  u += 0x7fffu + ((u >> 16) & 1u);
-  return (uint16_t)(u >> 16);
-}
-
-// per layer: ceil(in/64) K-major SWIZZLE_128B tiles of [npad x 64] bf16 —
-// the exact shared-memory image tcgen05.mma reads (actor_tc.cu)
-void pack_tc(const cyr_policy& p, const double* src, std::vector<uint8_t>& dst) {
-  dst.assign(p.tc_bytes, 0);
-  size_t off = 0;
-  for (int l = 0; l < p.desc.n_layers; ++l) {
-    const cyr::LayerDesc& L = p.desc.layer[l];
-    const size_t tile_bytes = (size_t)p.tc_npad[l] * 128;
-    const int kt = (L.in + 63) / 64;
-    for (int n = 0; n < L.out; ++n)
-      for (int k = 0; k < L.in; ++k) {
-        const int t = k / 64, kk = k % 64;
-        const int chunk = (kk * 2) >> 4;
-        // layers of one n tile (npad <= 256): k tiles of npad rows back to back
-        // (the narrow kernel's layout, also read by the wide kernel);
-        // wider layers: [n tile of 256][k tile][256 rows]
-        const bool multi = p.tc_npad[l] > 256;
-        const int nt = multi ? n / 256 : 0, r = multi ? n % 256 : n;
-        const size_t tile = multi ? ((size_t)nt * kt + t) * (256 * 128) : t * tile_bytes;
-        const size_t byte = (size_t)p.tc_off[l] + tile + (size_t)(r >> 3) * 1024 + (r & 7) * 128 +
-                            ((chunk ^ (r & 7)) << 4) + ((kk * 2) & 15);
-        const uint16_t v = f32_to_bf16_rne((float)src[off + (size_t)n * L.in + k]);
-        std::memcpy(&dst[byte], &v, 2);
-      }
-    off += (size_t)L.out * L.in + L.out;
-  }
-}
-
+// Publish a weights blob (reference layout, host memory): one async copy of
+// the raw float64 blob into device staging (a true DMA when `blob` is the
+// pinned watch snapshot) and one kernel that scatters it into every device
+// layout (pack.cu), ordered on the policy's upload stream.
 int upload(cyr_policy* p, const double* blob) {
-  if (p->tc_ok || p->tc_wide) {
-    std::vector<uint8_t> h;
-    pack_tc(*p, blob, h);
-    CYR_CUDA(cudaMemcpy(p->tc_blob_d, h.data(), h.size(), cudaMemcpyHostToDevice));
-  }
-  if (p->precision == CYR_FP64) {
-    std::vector<double> h;
-    pack_blob(*p, blob, h);
-    CYR_CUDA(cudaMemcpy(p->blob_d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
-  } else {
-    std::vector<float> h;
-    pack_blob(*p, blob, h);
-    CYR_CUDA(cudaMemcpy(p->blob_d, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
-  }
+  const size_t n = blob_count(p);
+  if (!p->up_stream) CYR_CUDA(cudaStreamCreateWithFlags(&p->up_stream, cudaStreamNonBlocking));
+  if (!p->raw_stage_d) CYR_CUDA(cudaMalloc(reinterpret_cast<void**>(&p->raw_stage_d), n * 8));
+  CYR_CUDA(cudaMemcpyAsync(p->raw_stage_d, blob, n * 8, cudaMemcpyHostToDevice, p->up_stream));
+  const bool tc = p->tc_ok || p->tc_wide;
+  const int rc = cyr_launch_pack_policy(p->desc, simt_precision_of(p->precision), p->raw_stage_d,
+                                        p->blob_d, tc ? p->tc_blob_d : nullptr, p->tc_off,
+                                        p->tc_npad, p->up_stream);
+  if (rc != CYR_OK) return cuda_fail(cudaGetLastError(), "pack_kernel");
+  CYR_CUDA(cudaStreamSynchronize(p->up_stream));
   return CYR_OK;
 }
 
@@ -348,7 +296,7 @@ constexpr long long kTcMinCols = 1024;  // below: the MLP is not a dense GEMM
 // epilogues, HBM activations) beat the one-CTA-runs-all-layers kernel
 constexpr long long kTcLayerCols = 32768;
 
-int simt_precision(const cyr_policy* p) { return p->precision == CYR_FP64 ? CYR_FP64 : CYR_FP32; }
+int simt_precision(const cyr_policy* p) { return simt_precision_of(p->precision); }
 
 // narrow bf16 actors: the fused persistent tcgen05 MLP (actor_tc.cu) for
 // batches of >= kTcMinCols columns; CYR_TC_FUSED=0 restores the previous
@@ -575,6 +523,8 @@ int policy_create_impl(cyr_policy** out, const int32_t* sizes, int32_t n_sizes,
     }
   }
   cudaError_t e = cudaMalloc(&p->blob_d, off * p->elem);
+  if (e == cudaSuccess) e = cudaMemset(p->blob_d, 0, off * p->elem);  // padding stays zero
+  if (e == cudaSuccess && p->tc_blob_d) e = cudaMemset(p->tc_blob_d, 0, p->tc_bytes);
   if (e != cudaSuccess) {
     delete p;
     return cuda_fail(e, "cudaMalloc(policy)");
@@ -657,19 +607,13 @@ int quiesce_for_upload(cyr_policy* p) {
   return CYR_OK;
 }
 
-size_t blob_count(const cyr_policy* p) {
-  size_t n = 0;
-  for (size_t l = 0; l + 1 < p->sizes.size(); ++l)
-    n += (size_t)p->sizes[l] * p->sizes[l + 1] + p->sizes[l + 1];
-  return n;
-}
 
 // any watched host array differs from the snapshot last published from it
 bool watch_changed(const cyr_policy* p) {
   const auto& w = p->watch;
   size_t off = 0;
   for (size_t i = 0; i < w.ptr.size(); ++i) {
-    if (std::memcmp(w.ptr[i], w.snap.data() + off, w.count[i] * sizeof(double)) != 0) return true;
+    if (std::memcmp(w.ptr[i], w.snap + off, w.count[i] * sizeof(double)) != 0) return true;
     off += w.count[i];
   }
   return false;
@@ -680,11 +624,11 @@ int watch_republish(cyr_policy* p) {
   auto& w = p->watch;
   size_t off = 0;
   for (size_t i = 0; i < w.ptr.size(); ++i) {
-    std::memcpy(w.snap.data() + off, w.ptr[i], w.count[i] * sizeof(double));
+    std::memcpy(w.snap + off, w.ptr[i], w.count[i] * sizeof(double));
     off += w.count[i];
   }
   const int rc = quiesce_for_upload(p);
-  return rc != CYR_OK ? rc : upload(p, w.snap.data());
+  return rc != CYR_OK ? rc : upload(p, w.snap);
 }
 }  // namespace
 
@@ -725,7 +669,7 @@ int cyr_policy_update(cyr_policy* p, const double* weights_blob) {
   const int rc = quiesce_for_upload(p);
   if (rc != CYR_OK) return rc;
   if (!p->watch.ptr.empty())  // an explicit publish is the new snapshot
-    std::memcpy(p->watch.snap.data(), weights_blob, p->watch.snap.size() * sizeof(double));
+    std::memcpy(p->watch.snap, weights_blob, p->watch.snap_n * sizeof(double));
   return upload(p, weights_blob);
 }
 
@@ -737,7 +681,6 @@ int cyr_policy_watch(cyr_policy* p, const double* const* arrays, const int64_t* 
   if (n == 0) {
     w.ptr.clear();
     w.count.clear();
-    w.snap.clear();
     return CYR_OK;
   }
   // flatten order: W_l (out*in) then b_l (out) for every layer
@@ -749,7 +692,11 @@ int cyr_policy_watch(cyr_policy* p, const double* const* arrays, const int64_t* 
   }
   w.ptr.assign(arrays, arrays + n);
   w.count.assign(counts, counts + n);
-  w.snap.assign(blob_count(p), 0.0);
+  if (!w.snap) {
+    w.snap_n = blob_count(p);
+    CYR_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&w.snap), w.snap_n * sizeof(double),
+                           cudaHostAllocPortable));
+  }
   return watch_republish(p);
 }
 
@@ -849,6 +796,9 @@ int cyr_policy_destroy(cyr_policy* p) {
   cudaFree(p->blob_d);
   cudaFree(p->tc_blob_d);
   cudaFree(p->wide_act_d);
+  cudaFree(p->raw_stage_d);
+  if (p->up_stream) cudaStreamDestroy(p->up_stream);
+  if (p->watch.snap) cudaFreeHost(p->watch.snap);
   delete p;
   return CYR_OK;
 }

@@ -265,6 +265,9 @@ int cyr_launch_actor_tc(const cyr::ActorDesc& desc, const unsigned char* tc_blob
                         int mode_t, const int32_t* mcs, const int16_t* node, int M, int tau,
                         int parents, long long nodes_per_slot, long long parent_off, int epad,
                         double mcs_scale, cudaStream_t stream, int parent_base = 0);
+int cyr_launch_pack_policy(const cyr::ActorDesc& desc, int precision, const double* raw_d,
+                           void* blob_d, unsigned char* tc_blob_d, const long long* tc_off,
+                           const int* tc_npad, cudaStream_t stream);
 bool cyr_tc_fused_applies(const cyr::ActorDesc& desc, const int* tc_npad);
 int cyr_launch_actor_tc_fused(const cyr::ActorDesc& desc, const unsigned char* tc_blob,
                               const long long* tc_off, const int* tc_npad, const float* bias_blob,
