@@ -590,15 +590,34 @@ def run_ours(args, rank, world, local_rank):
                                                  "frac")} | {"ms": roofline["kernel_ms"]})
 
     cpu = None
+    other_prec = None
     if world == 1:
-        # the optional bf16 tcgen05 actor on the same 1024 slots: its decision
-        # agreement with the reference rides on the CPU leg
-        pol_tc = DevicePolicy(agent.actor, "bf16_tc")
-        eng_tc = CodebookEngine(pol_tc, cell, max_slots=SLOTS, device=dev)
-        tc_books = eng_tc.run(alloc_d, eps_d).clone()
-        eng_tc.check()
-        pol_tc.close()
-        cpu = cpu_leg(eng.codebooks, agent, cell, allocs, eps, {"bf16_tc": tc_books})
+        # the same step with the other actor precisions: fp64 (logits within
+        # 1e-15 of the reference: settles the fp32 headline's precision) and
+        # the optional bf16 tcgen05 actor; their codebooks' agreement with the
+        # reference rides on the CPU leg
+        other_prec, books_by = {}, {}
+        for prec in ("fp64", "bf16_tc"):
+            pol_x = DevicePolicy(agent.actor, prec)
+            eng_x = CodebookEngine(pol_x, cell, max_slots=SLOTS, with_tree=not args.no_tree,
+                                   device=dev)
+            for _ in range(3):
+                eng_x.run(alloc_d, eps_d)
+            eng_x.check()
+            ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(10)]
+            for e0, e1 in ev:
+                flush.fill_(7)
+                e0.record(stream)
+                eng_x.run(alloc_d, eps_d, stream=stream)
+                e1.record(stream)
+            torch.cuda.synchronize()
+            ms = float(np.mean([e0.elapsed_time(e1) for e0, e1 in ev]))
+            books_by[prec] = eng_x.codebooks[:SLOTS].clone()
+            other_prec[prec] = {"ms_per_step": ms, "value": SLOTS / (ms * 1e-3), "unit": UNIT,
+                                "steps": 10, "what": "the headline step (K2 -> K3 -> K1, 1024 "
+                                                     "slots, L2 flushed) with this actor"}
+            pol_x.close()
+        cpu = cpu_leg(eng.codebooks, agent, cell, allocs, eps, books_by)
     line = {
         "metric": METRIC, "value": total / (mean_ms * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms,
@@ -623,6 +642,7 @@ def run_ours(args, rank, world, local_rank):
         "kernels": kernels,
         "cpu_baseline": None if cpu is None else cpu[0],
         "parity": None if cpu is None else cpu[1],
+        "other_precisions": other_prec,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks.summary(),
     }
