@@ -737,8 +737,9 @@ def mode_t_run(cell, hidden, slots, reps=3, fp32_reps=None):
 def mode_t_sharded(world, rank, dev, reps=3):
     """One BASELINE configs[4] Mode-T tree (cfg5: E=16, cap 6, 3x1024 actor,
     bf16 tcgen05) split across the ranks by subtrees of level 3 (343
-    subtrees; levels <= 3 replicated) and assembled on every rank by ONE
-    all-gather over NCCL.  Times are CUDA events, max over
+    subtrees; levels <= 3 replicated); each rank scores its leaves and ONE
+    all-gather over NCCL assembles the per-leaf summaries (SURVEY §8(e):
+    node records stay on their GPU).  Times are CUDA events, max over
     ranks.  At N > 1 rank 0 also builds the whole tree alone and checks the
     assembled one against it."""
     import torch
@@ -752,9 +753,21 @@ def mode_t_sharded(world, rank, dev, reps=3):
     al, mc, ep = (torch.from_numpy(x).to(dev) for x in (allocs, mcs, eps))
     level = 3 if world > 1 else 0
     first, count = tree.shard_extent(cap, m, level, world, rank)
+    lf, lc = tree.shard_leaf_range(cap, m, level, first, count)
+    margins = torch.from_numpy(tree.threshold_margins(mcs)).to(dev)
+    prob = torch.from_numpy(tree.admitted_count_probs(cell)).to(dev)
     pol = DevicePolicy(actor, "bf16_tc")
     out = tree.build_tree_mode_t(pol, cell, al, mc, ep, shard=(level, first, count))
-    full = tree.gather_mode_t_tree(out, cap, m, level) if world > 1 else out
+
+    def summarise():
+        # node records stay on this GPU; the per-leaf decode bitmasks and the
+        # partial expectations travel
+        ok, exp = tree.score_leaf_states(out, cell, al, margins, prob, lf, lc)
+        if world > 1:
+            return tree.gather_leaf_summary(exp, ok, cell.total_scs)
+        return exp, ok, int(exp.numel() * 8 + ok.numel() * 4)
+
+    summary = summarise()
     torch.cuda.synchronize()
     build, gather = [], []
     stream = torch.cuda.current_stream()
@@ -766,8 +779,7 @@ def mode_t_sharded(world, rank, dev, reps=3):
         e[0].record(stream)
         tree.build_tree_mode_t(pol, cell, al, mc, ep, out=out, shard=(level, first, count))
         e[1].record(stream)
-        if world > 1:
-            full = tree.gather_mode_t_tree(out, cap, m, level)
+        summary = summarise()
         e[2].record(stream)
         torch.cuda.synchronize()
         build.append(e[0].elapsed_time(e[1]))
@@ -780,10 +792,15 @@ def mode_t_sharded(world, rank, dev, reps=3):
            "precision": "bf16_tc", "shard_level": level, "subtrees": (cap + 1) ** level,
            "ranks": world, "ms_build_max": float(t[0]), "ms_gather_max": float(t[1]),
            "ms_per_tree": float(t[2]), "trees_per_s": 1e3 / float(t[2]),
-           "gathered_bytes": int(full.numel() * full.element_size())}
+           "gather": "per-leaf decode bitmasks + partial E[r]/E[goodput]/E[lost] (node "
+                     "records stay on their GPU)",
+           "gathered_bytes_per_rank": int(summary[2]),
+           "whole_tree_record_bytes": int(out.numel() * out.element_size())}
     if world > 1 and rank == 0:
         whole = tree.build_tree_mode_t(pol, cell, al, mc, ep)
-        res["matches_whole_tree"] = bool(torch.equal(whole, full))
+        ok_w, exp_w = tree.score_leaf_states(whole, cell, al, margins, prob)
+        res["summary_matches_whole_tree"] = bool(
+            torch.equal(summary[1], ok_w) and torch.allclose(summary[0], exp_w, rtol=1e-12))
     pol.close()
     return res
 

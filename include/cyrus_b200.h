@@ -298,6 +298,19 @@ int cyr_tree_mode_t_device(const cyr_policy* policy, const int32_t* alloc, const
                            const double* eps, int32_t S, int32_t N, int32_t L, int32_t M,
                            double mcs_scale, int16_t* node_state, void* workspace,
                            int32_t* status, void* stream);
+/* Leaf scoring from node records (Mode-T trees): leaves
+ * [first, first + count) of level M of every slot's BFS record array
+ * node_state [S][nodes_per_slot][Epad] — the threshold decoder per user
+ * (phy.py:73-80, 196-198), lost / goodput SCs (core.py:132-153), leaf weight
+ * prod_tau prob[tau][k_tau] (prob [M][cap+1]).  leaf_ok [S][count] uint32
+ * bitmask of decoding users (may be NULL); expect [S][3] = (E[r],
+ * E[goodput SCs], E[lost SCs]) over the given leaves (a subtree shard's
+ * partial expectation: the shards' sum is the whole tree's). */
+int cyr_tree_leaf_score_states_device(const int16_t* node_state, int64_t nodes_per_slot,
+                                      int32_t S, int32_t E, int32_t cap, int32_t M,
+                                      int64_t first, int64_t count, const int32_t* alloc,
+                                      const double* margin, const double* prob, int32_t N,
+                                      uint32_t* leaf_ok, double* expect, void* stream);
 
 /* Subtree shard of the Mode-T tree (north star "shards by
  * ... first-mini-slot branch across the 8 GPUs"): levels 1..shard_level are

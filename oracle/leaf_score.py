@@ -40,3 +40,26 @@ def score_leaves(codebook, alloc, margin, prob, minislots: int, total_scs: int):
     tot = int(np.where(n > 0, n, 0).sum())
     e_lost = float(np.sum(w * lost))
     return bits, reward, -e_lost / total_scs, float(np.sum(w * (tot - lost))), e_lost
+
+
+def score_leaf_states(leaves, alloc, margin, prob, minislots: int, total_scs: int,
+                      first: int = 0):
+    """The same scoring from explicit leaf records (Mode-T trees): leaves
+    (count, E) cumulative punctures of level-M nodes first .. first+count.
+    Returns (ok bits, E[r], E[goodput], E[lost]) over those leaves."""
+    cum = np.asarray(leaves, dtype=np.int64)
+    n = np.asarray(alloc, dtype=np.int64)
+    budget = np.asarray(margin, dtype=np.float64) * (minislots * n)
+    ok = (n[None, :] <= 0) | (cum <= budget[None, :])
+    lost = ((~ok) * np.where(n > 0, n, 0)[None, :]).sum(axis=1)
+    bits = (ok.astype(np.int64) << np.arange(n.size)[None, :]).sum(axis=1)
+    prob = np.asarray(prob)
+    r = prob.shape[1]
+    q = np.arange(first, first + cum.shape[0])
+    w = np.ones(cum.shape[0])
+    for tau in range(minislots - 1, -1, -1):
+        w = w * prob[tau][q % r]
+        q = q // r
+    tot = int(np.where(n > 0, n, 0).sum())
+    e_lost = float(np.sum(w * lost))
+    return bits, -e_lost / total_scs, float(np.sum(w * (tot - lost))), e_lost

@@ -51,6 +51,9 @@ SIGNATURES = {
     "cyr_tree_num_nodes": (_c_i64, [_c_i32, _c_i32]),
     "cyr_tree_state_stride": (_c_i32, [_c_i32]),
     "cyr_tree_expand_device": (_c_int, [_vp, _c_i32, _c_i32, _c_i32, _c_i32, _vp, _vp]),
+    "cyr_tree_leaf_score_states_device": (_c_int, [_vp, _c_i64, _c_i32, _c_i32, _c_i32, _c_i32,
+                                                   _c_i64, _c_i64, _vp, _vp, _vp, _c_i32, _vp,
+                                                   _vp, _vp]),
     "cyr_tree_mode_t_workspace_bytes": (ctypes.c_size_t, [_vp, _c_i32, _c_i32, _c_i32]),
     "cyr_tree_mode_t_device": (_c_int, [_vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i32, _c_i32,
                                         ctypes.c_double, _vp, _vp, _vp, _vp]),

@@ -1324,6 +1324,27 @@ int cyr_tree_score_device(const int32_t* codebook, const int32_t* alloc, const d
   return rc;
 }
 
+int cyr_tree_leaf_score_states_device(const int16_t* node_state, int64_t nodes_per_slot,
+                                      int32_t S, int32_t E, int32_t cap, int32_t M,
+                                      int64_t first, int64_t count, const int32_t* alloc,
+                                      const double* margin, const double* prob, int32_t N,
+                                      uint32_t* leaf_ok, double* expect, void* stream) {
+  if (S < 0 || E < 1 || E > 32 || cap < 1 || M < 1 || M > 10 || N <= 0) return CYR_BAD_ARG;
+  long long leaves = 1;
+  for (int t = 0; t < M; ++t) leaves *= cap + 1;
+  if (first < 0 || count < 0 || first + count > leaves) return CYR_BAD_ARG;
+  if (nodes_per_slot != cyr_tree_num_nodes(cap, M)) return CYR_BAD_ARG;
+  if (S == 0 || count == 0) return CYR_OK;
+  if (!node_state || !alloc || !margin || !prob || !expect) return CYR_BAD_ARG;
+  const int epad = cyr_tree_state_stride(E);
+  const long long leaf0 = nodes_per_slot - leaves;  // level M is the last run of BFS order
+  const int rc = cyr_launch_leaf_states_score(
+      node_state + (leaf0 + first) * epad, nodes_per_slot * epad, S, E, epad, first, count, cap,
+      M, alloc, margin, prob, N, leaf_ok, expect, static_cast<cudaStream_t>(stream));
+  if (rc == CYR_CUDA_ERROR) g_last_error = cudaGetErrorString(cudaGetLastError());
+  return rc;
+}
+
 int cyr_tree_mode_t_device(const cyr_policy* p, const int32_t* alloc, const int32_t* mcs,
                            const double* eps, int32_t S, int32_t N, int32_t L, int32_t M,
                            double mcs_scale, int16_t* node_state, void* workspace,

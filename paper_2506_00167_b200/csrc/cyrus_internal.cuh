@@ -265,6 +265,10 @@ int cyr_launch_actor_tc(const cyr::ActorDesc& desc, const unsigned char* tc_blob
                         int mode_t, const int32_t* mcs, const int16_t* node, int M, int tau,
                         int parents, long long nodes_per_slot, long long parent_off, int epad,
                         double mcs_scale, cudaStream_t stream, int parent_base = 0);
+int cyr_launch_leaf_states_score(const int16_t* leaves, long long slot_stride, int S, int E,
+                                 int epad, long long first, long long count, int cap, int M,
+                                 const int32_t* alloc, const double* margin, const double* prob,
+                                 int N, uint32_t* ok, double* expect, cudaStream_t stream);
 int cyr_launch_pack_policy(const cyr::ActorDesc& desc, int precision, const double* raw_d,
                            void* blob_d, unsigned char* tc_blob_d, const long long* tc_off,
                            const int* tc_npad, cudaStream_t stream);

@@ -486,3 +486,114 @@ int cyr_launch_tree_score(const int32_t* codebook, const int32_t* alloc, const d
   cudaFreeAsync(partial, stream);
   return rc;
 }
+
+// ------------------------------------------------ leaf scoring from states
+// Mode-T trees (no codebook columns: every node has its own decision) are
+// scored from the leaf records themselves: for leaves [first, first + count)
+// of level M of each slot (a subtree shard's leaves are one contiguous run),
+// the threshold decoder of every user (phy.py:73-80 via decode_user,
+// phy.py:196-198), lost / goodput SCs (core.py:132-153) and the leaf weight
+// prod_tau prob[tau][k_tau] (digits of the leaf's level-M index, first
+// mini-slot most significant).  Per 256-leaf block a fixed-order shared
+// reduction, then the blocks in order: deterministic.  This is the per-leaf
+// SUMMARY a subtree shard ships instead of its node records.
+namespace cyr {
+constexpr int kLeafThreads = 256;
+
+__global__ void __launch_bounds__(kLeafThreads) leaf_states_score_kernel(
+    const int16_t* __restrict__ leaves, long long slot_stride, int E, int epad, long long first,
+    long long count, int R, int M, const int32_t* __restrict__ alloc,
+    const double* __restrict__ margin, const double* __restrict__ prob, uint32_t* __restrict__ ok,
+    double* __restrict__ partial, int blocks_per_slot) {
+  __shared__ double s_lost[kLeafThreads], s_good[kLeafThreads];
+  const int s = blockIdx.x / blocks_per_slot, blk = blockIdx.x % blocks_per_slot;
+  const long long i = (long long)blk * kLeafThreads + threadIdx.x;
+  double lost_w = 0.0, good_w = 0.0;
+  if (i < count) {
+    const int16_t* rec = leaves + s * slot_stride + i * epad;
+    long long total = 0, lost = 0;
+    double w = 1.0;
+    unsigned q = (unsigned)(first + i);  // leaves < 2^31 (checked by the launcher)
+    for (int tau = M - 1; tau >= 0; --tau) {  // last digit = last mini-slot
+      const unsigned qd = q / (unsigned)R;
+      w *= prob[tau * R + (int)(q - qd * (unsigned)R)];
+      q = qd;
+    }
+    uint32_t bits = 0;
+    for (int e = 0; e < E; ++e) {
+      const int n = alloc[(long long)s * E + e];
+      const double budget = margin[(long long)s * E + e] * (double)(M * n);
+      const bool good = n <= 0 || (double)rec[e] <= budget;
+      bits |= good ? 1u << e : 0u;
+      if (n > 0) {
+        total += n;
+        if (!good) lost += n;
+      }
+    }
+    if (ok) ok[s * count + i] = bits;
+    lost_w = w * (double)lost;
+    good_w = w * (double)(total - lost);
+  }
+  s_lost[threadIdx.x] = lost_w;
+  s_good[threadIdx.x] = good_w;
+  __syncthreads();
+  for (int h = kLeafThreads / 2; h > 0; h >>= 1) {
+    if (threadIdx.x < h) {
+      s_lost[threadIdx.x] += s_lost[threadIdx.x + h];
+      s_good[threadIdx.x] += s_good[threadIdx.x + h];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partial[((long long)s * blocks_per_slot + blk) * 2] = s_lost[0];
+    partial[((long long)s * blocks_per_slot + blk) * 2 + 1] = s_good[0];
+  }
+}
+// per slot: the blocks' partials in a fixed order (thread t sums blocks
+// t, t + 256, ...; then a fixed shared-memory tree): deterministic
+__global__ void __launch_bounds__(kLeafThreads) leaf_partials_reduce_kernel(
+    const double* __restrict__ partial, int blocks_per_slot, int N, double* __restrict__ expect) {
+  __shared__ double s_lost[kLeafThreads], s_good[kLeafThreads];
+  const int s = blockIdx.x;
+  double l = 0.0, g = 0.0;
+  for (int b = threadIdx.x; b < blocks_per_slot; b += kLeafThreads) {
+    l += partial[((long long)s * blocks_per_slot + b) * 2];
+    g += partial[((long long)s * blocks_per_slot + b) * 2 + 1];
+  }
+  s_lost[threadIdx.x] = l;
+  s_good[threadIdx.x] = g;
+  __syncthreads();
+  for (int h = kLeafThreads / 2; h > 0; h >>= 1) {
+    if (threadIdx.x < h) {
+      s_lost[threadIdx.x] += s_lost[threadIdx.x + h];
+      s_good[threadIdx.x] += s_good[threadIdx.x + h];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    expect[s * 3] = -s_lost[0] / (double)N;  // E[r] (core.py:132-146)
+    expect[s * 3 + 1] = s_good[0];           // E[goodput SCs] (core.py:149-153)
+    expect[s * 3 + 2] = s_lost[0];           // E[lost SCs]
+  }
+}
+}  // namespace cyr
+
+int cyr_launch_leaf_states_score(const int16_t* leaves, long long slot_stride, int S, int E,
+                                 int epad, long long first, long long count, int cap, int M,
+                                 const int32_t* alloc, const double* margin, const double* prob,
+                                 int N, uint32_t* ok, double* expect, cudaStream_t stream) {
+  if (S <= 0 || count <= 0) return CYR_OK;
+  const long long bps = (count + cyr::kLeafThreads - 1) / cyr::kLeafThreads;
+  if (bps * S >= (1ll << 31) || first + count >= (1ll << 31)) return CYR_UNSUPPORTED;
+  double* partial = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&partial), (size_t)S * bps * 2 * sizeof(double),
+                      stream) != cudaSuccess)
+    return CYR_CUDA_ERROR;
+  cyr::leaf_states_score_kernel<<<(unsigned)(bps * S), cyr::kLeafThreads, 0, stream>>>(
+      leaves, slot_stride, E, epad, first, count, cap + 1, M, alloc, margin, prob, ok, partial,
+      (int)bps);
+  cyr::leaf_partials_reduce_kernel<<<S, cyr::kLeafThreads, 0, stream>>>(partial, (int)bps, N,
+                                                                         expect);
+  cudaFreeAsync(partial, stream);
+  return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
+}

@@ -297,3 +297,86 @@ def score_tree(codebooks, cell, allocs, margins, prob, out=None, leaf_ok: bool =
         out.data_ptr(), None if ok is None else ok.data_ptr(), expect.data_ptr(),
         _native.stream_handle(stream)), "score tree")
     return out, ok, expect
+
+
+# -------------------------------------------- Mode-T leaf summaries (§8(e))
+# A subtree shard of a Mode-T tree keeps its node records on its GPU; what
+# travels is a per-leaf SUMMARY: the decode bitmask of every leaf (4 B
+# instead of the Epad*2-byte record chain) and the shard's partial
+# expectations.  The expectations are additive over leaves, so the whole
+# tree's E[r] / E[goodput] / E[lost] is the (rank-ordered) sum of the
+# shards'.
+
+def score_leaf_states(states, cell, allocs, margins, prob, first: int = 0, count=None,
+                      leaf_ok: bool = True, stream=None):
+    """Threshold decode + reward of leaves [first, first+count) of level M
+    from node records (S, nodes, Epad) (cyr_tree_leaf_score_states_device).
+    Returns (leaf_ok (S, count) int32 bitmask or None, expect (S, 3) float64
+    = E[r], E[goodput SCs], E[lost SCs] over those leaves)."""
+    import torch
+    s, nodes, _ = states.shape
+    cap, m, e = cell.num_branches, cell.minislots, cell.num_embb
+    leaves = (cap + 1) ** m
+    count = leaves - first if count is None else int(count)
+    dev = states.device
+    ok = torch.empty((s, count), dtype=torch.int32, device=dev) if leaf_ok else None
+    expect = torch.zeros((s, 3), dtype=torch.float64, device=dev)
+    prob = prob.contiguous()
+    if tuple(prob.shape) != (m, cap + 1):
+        raise ValueError("prob must be (M, cap+1)")
+    _native.check(_native.lib().cyr_tree_leaf_score_states_device(
+        states.data_ptr(), nodes, s, e, cap, m, int(first), count,
+        allocs.contiguous().data_ptr(), margins.contiguous().data_ptr(), prob.data_ptr(),
+        cell.total_scs, None if ok is None else ok.data_ptr(), expect.data_ptr(),
+        _native.stream_handle(stream)), "leaf scoring")
+    return ok, expect
+
+
+def shard_leaf_range(cap: int, minislots: int, level: int, first: int, count: int) -> tuple:
+    """(first leaf, leaf count) below level-``level`` nodes [first, first+count)."""
+    span = (cap + 1) ** (minislots - level)
+    return first * span, count * span
+
+
+def gather_leaf_summary(expect, leaf_ok, total_scs: int, group=None, with_leaves: bool = True):
+    """ONE all-gather of every rank's partial expectations (S, 3) (and, with
+    ``with_leaves``, its leaves' decode bitmasks, padded to the widest shard)
+    -> (whole-tree expectations (S, 3), leaf bitmasks (S, all leaves) or
+    None, bytes this rank sent).  Rank r's leaves are the contiguous block
+    of shard r (shard_extent / shard_leaf_range), so the bitmasks assemble by
+    concatenation in rank order."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    s = expect.shape[0]
+    width = 0
+    if with_leaves:
+        n = torch.tensor([leaf_ok.shape[1]], dtype=torch.int64, device=expect.device)
+        sizes = [torch.zeros_like(n) for _ in range(world)]
+        dist.all_gather(sizes, n, group=group)
+        sizes = [int(x.item()) for x in sizes]
+        width = max(sizes)
+    # one buffer: expectations as float64 + bitmasks as int32 pairs viewed as float64
+    words = 3 + (width + 1) // 2
+    local = torch.zeros((s, words), dtype=torch.float64, device=expect.device)
+    local[:, :3] = expect
+    if with_leaves:
+        bits = torch.zeros((s, 2 * (words - 3)), dtype=torch.int32, device=expect.device)
+        bits[:, :leaf_ok.shape[1]] = leaf_ok
+        local[:, 3:] = bits.view(torch.float64)
+    out = torch.empty((world, s, words), dtype=torch.float64, device=expect.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, local, group=group)
+    else:
+        dist.all_gather(list(out.unbind(0)), local, group=group)
+    lost = out[0, :, 2].clone()
+    good = out[0, :, 1].clone()
+    for r in range(1, world):  # rank order: deterministic
+        lost += out[r, :, 2]
+        good += out[r, :, 1]
+    whole = torch.stack([-lost / total_scs, good, lost], dim=1)
+    leaves = None
+    if with_leaves:
+        blocks = [out[r, :, 3:].contiguous().view(torch.int32)[:, :sizes[r]] for r in range(world)]
+        leaves = torch.cat(blocks, dim=1)
+    return whole, leaves, int(local.numel() * local.element_size())

@@ -745,3 +745,49 @@ def test_codebook_stream_matches_engine(golden):
         st.submit(torch.from_numpy(a).pin_memory(), torch.from_numpy(e).pin_memory())
         st.submit(torch.from_numpy(a).pin_memory(), torch.from_numpy(e).pin_memory())
     st.drain()
+
+
+# -------------------------------------------- Mode-T leaf summaries (§8(e))
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+def test_leaf_scoring_from_states(golden, name):
+    """cyr_tree_leaf_score_states_device on K1's Mode-R leaf records equals
+    the fused K1 epilogue (cyr_tree_score_device) and the oracle; on a
+    Mode-T tree, shard partial expectations add up to the whole tree's."""
+    from oracle import leaf_score
+    cfg = golden.config(name)
+    cell = cfg.cell
+    cap, m, e = cell.num_branches, cell.minislots, cell.num_embb
+    slots = 3
+    books = torch.from_numpy(cfg["sto/codebook"][:slots].astype(np.int32)).cuda()
+    al = torch.from_numpy(cfg["alloc"][:slots].astype(np.int32)).cuda()
+    margins = torch.full((slots, e), 0.3, dtype=torch.float64, device="cuda")
+    prob = torch.from_numpy(tree.admitted_count_probs(cell)).cuda()
+    states, ok_k1, exp_k1 = tree.score_tree(books, cell, al, margins, prob)
+    ok, exp = tree.score_leaf_states(states, cell, al, margins, prob)
+    assert torch.equal(ok, ok_k1)
+    assert torch.allclose(exp, exp_k1, rtol=1e-12, atol=0)
+    for s in range(slots):
+        want = leaf_score.score_leaves(cfg["sto/codebook"][s], cfg["alloc"][s], np.full(e, 0.3),
+                                       prob.cpu().numpy(), m, cell.total_scs)
+        assert np.array_equal(ok[s].cpu().numpy().astype(np.int64), want[0])
+    # Mode T: the sum of shard partials is the whole tree's expectation
+    from paper_2506_00167_b200 import substream
+    actor = tree.make_mode_t_actor(cell, (64, 64), substream(5, "mode-t"))
+    pol = DevicePolicy(actor, "fp32")
+    mcs = torch.zeros_like(al)
+    ep = torch.from_numpy(cfg["eps"][:slots]).cuda()
+    mt = tree.build_tree_mode_t(pol, cell, al, mcs, ep)
+    _, whole = tree.score_leaf_states(mt, cell, al, margins, prob, leaf_ok=False)
+    lvl, world = 2, 3
+    parts = []
+    for r in range(world):
+        f, c = tree.shard_leaf_range(cap, m, lvl, *tree.shard_extent(cap, m, lvl, world, r))
+        parts.append(tree.score_leaf_states(mt, cell, al, margins, prob, f, c)[1])
+    lost = sum(p[:, 2] for p in parts)
+    assert torch.allclose(lost, whole[:, 2], rtol=1e-12, atol=1e-300)
+    leaves = mt[:, -(cap + 1) ** m:, :e].cpu().numpy()
+    for s in range(slots):
+        want = leaf_score.score_leaf_states(leaves[s], cfg["alloc"][s], np.full(e, 0.3),
+                                            prob.cpu().numpy(), m, cell.total_scs)
+        assert np.allclose(whole[s].cpu().numpy(), want[1:], rtol=1e-12, atol=0)
+    pol.close()
