@@ -576,7 +576,7 @@ int cyr_policy_actions_device(const cyr_policy* p, const int32_t* alloc, const i
   const size_t raw_b = ((size_t)R * 2 * E * p->elem + 255) / 256 * 256;
   const size_t mat_b = ((size_t)R * E * 8 + 255) / 256 * 256;
   unsigned char* ws = nullptr;
-  if (cudaMallocAsync(reinterpret_cast<void**>(&ws), raw_b + 3 * mat_b + (size_t)R * 8, st) !=
+  if (cyr::malloc_async(reinterpret_cast<void**>(&ws), raw_b + 3 * mat_b + (size_t)R * 8, st) !=
       cudaSuccess)
     return cuda_fail(cudaGetLastError(), "cudaMallocAsync(actions)");
   void* raw = ws;
@@ -647,7 +647,7 @@ int cyr_policy_sample_device(const cyr_policy* p, const int32_t* alloc, const in
   const size_t raw_b = ((size_t)R * 2 * E * p->elem + 255) / 256 * 256;
   const size_t mat_b = ((size_t)R * E * 8 + 255) / 256 * 256;
   unsigned char* ws = nullptr;
-  if (cudaMallocAsync(reinterpret_cast<void**>(&ws), raw_b + mat_b + (size_t)R * 8, st) !=
+  if (cyr::malloc_async(reinterpret_cast<void**>(&ws), raw_b + mat_b + (size_t)R * 8, st) !=
       cudaSuccess)
     return cuda_fail(cudaGetLastError(), "cudaMallocAsync(sample)");
   double* caps = reinterpret_cast<double*>(ws + raw_b);

@@ -539,7 +539,7 @@ int cyr_launch_enforce(const double* b, const double* caps, const double* demand
   if (R > kOneCtaRows) {  // multi-CTA coupled call (two passes, stream-ordered scratch)
     const size_t bytes = (size_t)R * sizeof(long long) + 16;
     void* scratch = nullptr;
-    if (cudaMallocAsync(&scratch, bytes, stream) != cudaSuccess) return CYR_CUDA_ERROR;
+    if (cyr::malloc_async(&scratch, bytes, stream) != cudaSuccess) return CYR_CUDA_ERROR;
     int* stop = reinterpret_cast<int*>(scratch);
     long long* thr = reinterpret_cast<long long*>(static_cast<unsigned char*>(scratch) + 16);
     cudaMemsetAsync(stop, 0, sizeof(int), stream);

@@ -474,7 +474,7 @@ int cyr_launch_tree_score(const int32_t* codebook, const int32_t* alloc, const d
   p.leaf_ok = leaf_ok;
   const int items = p.level_blocks[M] - p.level_blocks[M - 1];
   double* partial = nullptr;
-  if (cudaMallocAsync(reinterpret_cast<void**>(&partial), (size_t)S * items * 2 * sizeof(double),
+  if (cyr::malloc_async(reinterpret_cast<void**>(&partial), (size_t)S * items * 2 * sizeof(double),
                       stream) != cudaSuccess)
     return CYR_CUDA_ERROR;
   p.partial = partial;
@@ -586,7 +586,7 @@ int cyr_launch_leaf_states_score(const int16_t* leaves, long long slot_stride, i
   const long long bps = (count + cyr::kLeafThreads - 1) / cyr::kLeafThreads;
   if (bps * S >= (1ll << 31) || first + count >= (1ll << 31)) return CYR_UNSUPPORTED;
   double* partial = nullptr;
-  if (cudaMallocAsync(reinterpret_cast<void**>(&partial), (size_t)S * bps * 2 * sizeof(double),
+  if (cyr::malloc_async(reinterpret_cast<void**>(&partial), (size_t)S * bps * 2 * sizeof(double),
                       stream) != cudaSuccess)
     return CYR_CUDA_ERROR;
   cyr::leaf_states_score_kernel<<<(unsigned)(bps * S), cyr::kLeafThreads, 0, stream>>>(
