@@ -349,6 +349,28 @@ def measured_peak_bf16():
         return 2250.0  # nominal dense bf16 (B200_PROFILING.md)
 
 
+_FMA_PEAK: dict = {}
+
+
+def fp32_fma_peak():
+    """(TFLOP/s, source): the fp32 FMA peak MEASURED on this GPU
+    (cyr_selftest_fma_peak: FFMA2 chains on every SM, event-timed; SURVEY
+    §8(d) asks to measure it), the spec figure if the measurement fails."""
+    if "v" not in _FMA_PEAK:
+        import ctypes
+        from paper_2506_00167_b200 import _native
+        v = ctypes.c_double(0.0)
+        try:
+            _native.check(_native.lib().cyr_selftest_fma_peak(20000, ctypes.byref(v)))
+            _FMA_PEAK["v"] = (v.value, "measured: FFMA2 microbenchmark on this GPU "
+                                       "(cyr_selftest_fma_peak; spec 148 x 128 x 2 x 1965 MHz = "
+                                       "74.4)")
+        except Exception:  # reported, never fatal
+            _FMA_PEAK["v"] = (148 * 128 * 2 * 1965e6 / 1e12,
+                              "spec: 148 SMs x 128 FP32 lanes x 2 x 1965 MHz")
+    return _FMA_PEAK["v"]
+
+
 def committed_traffic():
     """dram read+write bytes per K1 launch from the committed ncu --set full
     capture (profiles/), or None."""
@@ -568,7 +590,7 @@ def run_ours(args, rank, world, local_rank):
     # every kernel of the step against its bound (live CUDA-event times)
     sizes = [cell.num_embb + 1, *HIDDEN, 2 * cell.num_embb]
     k2_flops = 2.0 * SLOTS * cell.num_branches * sum(i * o for i, o in zip(sizes[:-1], sizes[1:]))
-    fma_peak = 148 * 128 * 2 * 1965e6 / 1e12
+    fma_peak, fma_src = fp32_fma_peak()
     k3_bytes = SLOTS * (cell.num_branches * 2 * cell.num_embb * 4 + cell.num_embb * 4
                         + cell.num_branches * cell.num_embb * 8
                         + (cell.num_branches + 1) * cell.num_embb * 4)
@@ -576,7 +598,7 @@ def run_ours(args, rank, world, local_rank):
         {"kernel": "K2 actor_osplit_kernel (fp32 SIMT tiled, output-split warps, 4096 branch columns)", "bound": "fma",
          "ms": actor_ms, "achieved": k2_flops / (actor_ms * 1e-3) / 1e12, "peak": fma_peak,
          "unit": "TFLOP/s", "frac": k2_flops / (actor_ms * 1e-3) / 1e12 / fma_peak,
-         "peak_source": "spec: 148 SMs x 128 FP32 lanes x 2 x 1965 MHz",
+         "peak_source": fma_src,
          "work": f"{k2_flops / 1e6:.0f} MFLOP (2 * sum in*out per column)"},
         {"kernel": "K3 codebook_kernel (fp64 head + exact projection + Huntington-Hill)",
          "bound": "latency", "ms": k3_ms,
@@ -716,11 +738,11 @@ def mode_t_run(cell, hidden, slots, reps=3, fp32_reps=None):
         ms = a.elapsed_time(b) / n
         states[prec] = st.cpu().numpy()[:, :, :cell.num_embb]
         eff = flops / (ms * 1e-3) / 1e12
-        peak = 148 * 128 * 2 * 1965e6 / 1e12 if prec == "fp32" else measured_peak_bf16()
+        peak = fp32_fma_peak()[0] if prec == "fp32" else measured_peak_bf16()
         out[prec] = {"ms_per_tree_batch": ms, "trees_per_s": slots / (ms * 1e-3),
                      "actor_tflops_effective": eff,
                      "effective_frac_of_peak": eff / peak,
-                     "peak": peak, "peak_source": "spec fp32 FMA (148x128x2x1965 MHz)"
+                     "peak": peak, "peak_source": fp32_fma_peak()[1]
                      if prec == "fp32" else "MEASURED_PEAKS.json bf16 sustained",
                      "note": "whole tree time (actor + K3 + features) over actor FLOPs"}
         pol.close()
@@ -886,7 +908,7 @@ def mode_t_cfg3(cell, hidden, total=SLOTS, chunk=32):
         torch.cuda.synchronize()
         ms = a.elapsed_time(b)
         eff = flops / (ms * 1e-3) / 1e12
-        peak = 148 * 128 * 2 * 1965e6 / 1e12 if prec == "fp32" else measured_peak_bf16()
+        peak = fp32_fma_peak()[0] if prec == "fp32" else measured_peak_bf16()
         out[prec] = {"ms_for_1024_trees": ms, "trees_per_s": total / (ms * 1e-3),
                      "actor_tflops_effective": eff, "effective_frac_of_peak": eff / peak}
         pol.close()

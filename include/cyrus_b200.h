@@ -335,6 +335,9 @@ int cyr_tree_mode_t_shard_device(const cyr_policy* policy, const int32_t* alloc,
 int cyr_selftest_latency(int32_t which, int32_t iters, int64_t* cycles);
 /* Event-to-event time of an empty kernel launch (cluster of `cluster` CTAs
  * when > 1), averaged over reps. */
+/* Measured fp32 FMA throughput of the current device (TFLOP/s): FFMA2
+ * chains on every SM, event-timed (the SIMT actor's roofline peak). */
+int cyr_selftest_fma_peak(int32_t iters, double* tflops);
 int cyr_selftest_launch(int32_t cluster, int32_t reps, int64_t* ns_per_launch);
 /* Phase timestamps (%globaltimer, ns) of the last latency-path launch when
  * the process runs with CYR_TRACE=1; zeros otherwise.  n <= 64. */

@@ -77,6 +77,7 @@ SIGNATURES = {
     "cyr_debug_trace": (_c_int, [_pi64, _c_i32]),
     "cyr_selftest_latency": (_c_int, [_c_i32, _c_i32, _pi64]),
     "cyr_selftest_launch": (_c_int, [_c_i32, _c_i32, _pi64]),
+    "cyr_selftest_fma_peak": (_c_int, [_c_i32, ctypes.POINTER(ctypes.c_double)]),
 }
 
 

@@ -1236,6 +1236,35 @@ int cyr_selftest_latency(int32_t which, int32_t iters, int64_t* cycles) {
   return rc;
 }
 
+int cyr_selftest_fma_peak(int32_t iters, double* tflops) {
+  if (!tflops || iters < 1) return CYR_BAD_ARG;
+  const int sms = sm_count_of_current_device();
+  float* sink = nullptr;
+  CYR_CUDA(cudaMalloc(&sink, sizeof(float)));
+  cudaEvent_t a, b;
+  CYR_CUDA(cudaEventCreate(&a));
+  CYR_CUDA(cudaEventCreate(&b));
+  int rc = cyr_launch_fma_peak(iters / 4 + 1, sms, sink, nullptr);  // warm-up (clocks up)
+  float best_ms = 1e30f;
+  for (int r = 0; r < 5 && rc == CYR_OK; ++r) {
+    cudaEventRecord(a, nullptr);
+    rc = cyr_launch_fma_peak(iters, sms, sink, nullptr);
+    cudaEventRecord(b, nullptr);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    best_ms = std::min(best_ms, ms);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  if (rc != CYR_OK) return rc;
+  // threads x 8 chains x 2 lanes x 2 flops per iteration
+  const double flops = (double)sms * 4 * 256 * 8 * 2 * 2 * (double)iters;
+  *tflops = flops / (best_ms * 1e-3) / 1e12;
+  return CYR_OK;
+}
+
 int cyr_selftest_launch(int32_t cluster, int32_t reps, int64_t* ns_per_launch) {
   if (!ns_per_launch || reps < 1) return CYR_BAD_ARG;
   cudaStream_t st;

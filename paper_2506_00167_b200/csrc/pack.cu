@@ -92,3 +92,42 @@ int cyr_launch_pack_policy(const cyr::ActorDesc& desc, int precision, const doub
                                                         tc_blob_d);
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
 }
+
+// ------------------------------------------------ fp32 FMA peak (measured)
+// MEASURED_PEAKS.json carries HBM and bf16 tensor peaks only; the SIMT
+// actor's roofline needs the fp32 FMA peak of THIS part and clock.  Every
+// thread runs 8 independent packed chains (fma.rn.f32x2 = FFMA2: two FMAs
+// per instruction, the form the actor kernels use) so the FMA pipe, not
+// latency, is the limit; 4 CTAs x 256 threads per SM.
+namespace cyr {
+__global__ void __launch_bounds__(256) fma_peak_kernel(int iters, float seed, float* sink) {
+  unsigned long long acc[8];
+  const float a = seed + threadIdx.x * 1e-7f;
+  unsigned long long av;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(av) : "f"(a));
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float x = 1.0f + k * 1e-3f;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(acc[k]) : "f"(x), "f"(x + 0.5f));
+  }
+  unsigned long long bv;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(bv) : "f"(0.999999f));
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(acc[k]) : "l"(bv), "l"(av));
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc[k]));
+    s += lo + hi;
+  }
+  if (s == 1234.5f) sink[0] = s;  // keep the chains alive
+}
+}  // namespace cyr
+
+int cyr_launch_fma_peak(int iters, int sm_count, float* sink, cudaStream_t stream) {
+  cyr::fma_peak_kernel<<<sm_count * 4, 256, 0, stream>>>(iters, 0.5f, sink);
+  return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
+}
