@@ -6,6 +6,22 @@
 
 namespace cyr {
 
+// the lane kernels' seat-priority divisor table (projection_lane.cuh), built
+// once per device before the first lane launch
+inline int ensure_seat_table(cudaStream_t stream) {
+  (void)stream;  // built on a private stream: legal while the caller's stream is being captured
+  static AttrCache built;
+  const bool ok = ensure_func_attr(built, 0, [&] {
+    cudaStream_t st = nullptr;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return false;
+    seat_table_kernel<<<1, 256, 0, st>>>();
+    const bool done = cudaStreamSynchronize(st) == cudaSuccess;
+    cudaStreamDestroy(st);
+    return done;
+  });
+  return ok ? CYR_OK : CYR_CUDA_ERROR;
+}
+
 // ------------------------------------------------------------ codebook K3
 // A CTA holds `spc` whole slots (<= 32 rows); 8 warps stride over the rows
 // in the per-row phases and warp 0 runs every slot's coupled loop at once.
@@ -493,6 +509,7 @@ int cyr_launch_codebook(int precision, const void* raw, const int32_t* alloc, co
   if (S <= 0) return CYR_OK;
   if (E < 1 || E > cyr::kMaxUsers || cap < 1 || cap > 16) return CYR_UNSUPPORTED;
   if (S >= 1184) {  // throughput: one lane per row, 32 / cap slots per warp
+    if (cyr::ensure_seat_table(stream) != CYR_OK) return CYR_CUDA_ERROR;
     const int per_cta = cyr::kLaneWarps * (32 / cap);
     const dim3 grid((S + per_cta - 1) / per_cta), block(32 * cyr::kLaneWarps);
     const size_t smem = cyr::kLaneWarps * cyr::lane_scratch_bytes(E);
@@ -600,6 +617,7 @@ int cyr_launch_tree_level(int precision, const void* raw, const int32_t* alloc, 
           static_cast<const float*>(raw), io, groups, L, status);
     return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
   }
+  if (cyr::ensure_seat_table(stream) != CYR_OK) return CYR_CUDA_ERROR;
   const long long per_cta = (long long)cyr::kLaneWarps * (32 / cap);
   const long long blocks = (groups + per_cta - 1) / per_cta;
   if (blocks >= (1ll << 31)) return CYR_UNSUPPORTED;

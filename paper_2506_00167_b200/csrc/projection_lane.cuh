@@ -165,13 +165,42 @@ __device__ __forceinline__ double kl_finish_lane(LaneRow& r) {
   return 0.0;
 }
 
+// sqrt(max(a(a+1), 1)) of seat a = 0 .. kSeatTab-1, the divisor of the
+// reference's seat priority (enforcer.py:150-154): built once per device by
+// seat_table_kernel with the same __dsqrt_rn expression as seat_prio, so a
+// table lookup is bit-identical to computing it (one division per priority
+// instead of a division and a square root).
+constexpr int kSeatTab = 1024;
+static __device__ double g_seat_sqrt[kSeatTab];
+
+static __global__ void seat_table_kernel() {
+  for (int a = threadIdx.x; a < kSeatTab; a += blockDim.x) {
+    const double x = (double)a;
+    g_seat_sqrt[a] = __dsqrt_rn(fmax(__dmul_rn(x, __dadd_rn(x, 1.0)), 1.0));
+  }
+}
+
+__device__ __forceinline__ double seat_prio_tab(double m, int seat) {
+  if (seat < kSeatTab) return div_or_zero(m, g_seat_sqrt[seat]);
+  return seat_prio(m, seat);
+}
+
 // Huntington-Hill seats for m = mT[e * 32], caps cT; seats into hT[e * 32]
-// (hh_row of projection.cuh, one lane).  Returns the near-tie margin.
+// (hh_row of projection.cuh, one lane).  Returns the near-tie margin.  nT
+// caches each user's seat count once per row: cnt = ceil(cap) when the user
+// has positive mass and cnt >= 1, else -cnt - 1.
 __device__ __forceinline__ double hh_lane(const double* mT, const double* cT, int E, long long want,
-                                          int* hT) {
+                                          int* hT, int* nT) {
   auto m = [&](int e) { return mT[e * 32]; };
-  auto cnt = [&](int e) { return (int)ceil(cT[e * 32]); };
-  auto posu = [&](int e) { return m(e) > 0.0 && cnt(e) >= 1; };
+  for (int e = 0; e < E; ++e) {
+    const int c = (int)ceil(cT[e * 32]);
+    nT[e * 32] = (m(e) > 0.0 && c >= 1) ? c : -c - 1;
+  }
+  auto cnt = [&](int e) {
+    const int v = nT[e * 32];
+    return v >= 1 ? v : -v - 1;
+  };
+  auto posu = [&](int e) { return nT[e * 32] >= 1; };
   double margin = CUDART_INF;
   for (int e = 0; e < E; ++e) hT[e * 32] = 0;
   if (want <= 0) return margin;
@@ -221,7 +250,7 @@ __device__ __forceinline__ double hh_lane(const double* mT, const double* cT, in
         const int h = hT[e * 32];
         const double me = m(e);
         if (h + 1 <= cnt(e) - 1) {
-          const double p = seat_prio(me, h + 1);
+          const double p = seat_prio_tab(me, h + 1);
           if (!oka || precedes(p, e, pa, la)) {
             pa = p;
             la = e;
@@ -229,7 +258,7 @@ __device__ __forceinline__ double hh_lane(const double* mT, const double* cT, in
           }
         }
         if (h >= 1) {
-          const double p = seat_prio(me, h);
+          const double p = seat_prio_tab(me, h);
           if (!okd || precedes(pd, ld, p, e)) {
             pd = p;
             ld = e;
@@ -279,10 +308,10 @@ __device__ __forceinline__ double hh_lane(const double* mT, const double* cT, in
   return margin;
 }
 
-// Per-warp scratch for up to 32 rows of E users: bT, cT (double) and hT
-// (int), each [E][32].
+// Per-warp scratch for up to 32 rows of E users: bT, cT (double), hT and
+// nT (int), each [E][32].
 __host__ __device__ constexpr size_t lane_scratch_bytes(int E) {
-  return (size_t)E * 32 * (2 * sizeof(double) + sizeof(int));
+  return (size_t)E * 32 * (2 * sizeof(double) + 2 * sizeof(int));
 }
 
 // Rows row0 .. row0 + nrows of this warp (whole calls of `cap` rows, lane
@@ -310,6 +339,7 @@ __device__ void codebook_rows_lane(const RawT* raw, long long row0, int nrows, i
   double* bT = reinterpret_cast<double*>(scratch) + lane;
   double* cT = bT + plane;
   int* hT = reinterpret_cast<int*>(scratch + 2 * plane * sizeof(double)) + lane;
+  int* nT = hT + plane;
   const bool live = lane < nrows;
   const long long grow = row0 + (live ? lane : 0);
   const long long group = grow / cap;
@@ -360,7 +390,7 @@ __device__ void codebook_rows_lane(const RawT* raw, long long row0, int nrows, i
   double nu = 0.0, margin = 0.0;
   if (live) nu = kl_finish_lane(r);
   mark(5);
-  if (live) margin = hh_lane(bT, cT, E, (long long)j * L, hT);
+  if (live) margin = hh_lane(bT, cT, E, (long long)j * L, hT, nT);
   mark(6);
   if (live) io.emit_lane(grow, group, j, hT, E, bT, nu, margin, iters);
   mark(7);
