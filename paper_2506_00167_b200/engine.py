@@ -273,10 +273,12 @@ class CodebookEngine:
                 self.node_state.data_ptr(), st), "tree")
         return self.codebooks[:s]
 
-    def check(self) -> None:
-        stream = getattr(self, "_stream", None)
-        if stream is None:
-            return
+    def check(self, stream=None) -> None:
+        """Synchronise ``stream`` (default: the stream of the last ``run``,
+        else the device's current stream) and raise the reference's
+        exception for a failing slot."""
+        stream = stream or getattr(self, "_stream", None) or \
+            self.torch.cuda.current_stream(self.device)
         stream.synchronize()
         code = int(self.status[0].item())
         if code:
