@@ -344,9 +344,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) actor_tc_kernel(const TcLaunch 
 // TMEM (512 columns) holds D + A2 + A3 of one block and no more.
 // Measured (scripts/fused_probe.py, 2M Mode-R columns, event timing): 852 us
 // vs 937 us for the layer-by-layer kernels; per block the tensor pipe is busy
-// ~4.7k of ~15k cycles (printf profile, CYR_FUSED_PROF): MMA2 2.9k, the
-// N = 32 head 1.3k (16 K steps, instruction-overhead bound), MMA1 0.5k; the
-// rest is the epilogue hand-offs.  A/B knobs (compile-time): CYR_FUSED_EPI
+// ~4.7k of ~15k cycles.  Per-block phase sums (CYR_FUSED_PROF, every block
+// of CTAs 0 and 77): MMA thread 15.2k cycles per block, of which waiting for
+// epi1 + MMA2 8.6k and for epi2 + MMA3 5.9k; epilogue warps 1.0-2.0k (epi1)
+// and 1.6k (epi2) of work, the rest waiting.  Splitting the head's K chain
+// over 2 or 4 accumulators changed nothing (not chain-latency-bound).  A/B knobs (compile-time): CYR_FUSED_EPI
 // (8 / 16 epilogue warps: 16), CYR_FUSED_NSPLIT (MMA2 in N halves: slower),
 // CYR_FUSED_PERPART (MMA2 K steps per landed part: slower), CYR_FUSED_FADD2.
 #ifndef CYR_FUSED_GROUPS
@@ -546,6 +548,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const 
                      w3 = smem_u32(base + f.w_off[2]);
       const uint32_t t2 = (uint32_t)n2 * 128u, t3 = (uint32_t)n3 * 128u;  // bytes per k tile
       int i = 0;
+#ifdef CYR_FUSED_PROF
+      long long pacc[6] = {0, 0, 0, 0, 0, 0};
+      const long long pstart = clock64();
+#endif
       for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
         const int fb = i % NB;
         const uint32_t ph = (uint32_t)(i & 1);
@@ -615,11 +621,16 @@ __global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const 
         tc_commit(d3full);
 #ifdef CYR_FUSED_PROF
         const long long pt6 = clock64();
-        if (blockIdx.x == 0 && i >= 20 && i < 24)
-          printf("MMA blk %d: wait feat %lld, mma1 %lld, wait a2 %lld, mma2 %lld, wait a3 %lld, mma3 %lld\n",
-                 i, pt1 - pt0, pt2 - pt1, pt3 - pt2, pt4 - pt3, pt5 - pt4, pt6 - pt5);
+        pacc[0] += pt1 - pt0; pacc[1] += pt2 - pt1; pacc[2] += pt3 - pt2;
+        pacc[3] += pt4 - pt3; pacc[4] += pt5 - pt4; pacc[5] += pt6 - pt5;
 #endif
       }
+#ifdef CYR_FUSED_PROF
+      if (blockIdx.x == 0 || blockIdx.x == 77)
+        printf("MMA cta %d blocks %d per block: wait feat %lld, mma1 %lld, wait a2 %lld, mma2 %lld, "
+               "wait a3 %lld, mma3 %lld, total %lld\n", blockIdx.x, i, pacc[0] / i, pacc[1] / i,
+               pacc[2] / i, pacc[3] / i, pacc[4] / i, pacc[5] / i, (clock64() - pstart) / i);
+#endif
     }
     __syncwarp();
   } else if (warp >= kFusedEpi) {
@@ -641,6 +652,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const 
     const int row = quarter * 32 + lane;  // TMEM lane = column within the block
     const int out3 = p.desc.layer[2].out;
     int i = 0;
+#ifdef CYR_FUSED_PROF
+    long long eacc[5] = {0, 0, 0, 0, 0};
+#endif
     for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
       const uint32_t ph = (uint32_t)(i & 1);
 #ifdef CYR_FUSED_PROF
@@ -674,9 +688,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const 
       tc_fence_after();
 #ifdef CYR_FUSED_PROF
       const long long q5 = clock64();
-      if (blockIdx.x == 0 && i >= 20 && i < 24 && lane == 0 && (warp == 0 || warp == kFusedEpi - 1))
-        printf("EPI w%d blk %d: wait d1 %lld, epi1 %lld, wait d2 %lld, epi2 %lld, wait d3 %lld\n",
-               warp, i, q1 - q0, q2 - q1, q3 - q2, q4 - q3, q5 - q4);
+      eacc[0] += q1 - q0; eacc[1] += q2 - q1; eacc[2] += q3 - q2; eacc[3] += q4 - q3;
+      eacc[4] += q5 - q4;
 #endif
       if (part == 0) {
         const int col = b * kTcM + row;
@@ -694,6 +707,13 @@ __global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const 
       }
       tc_fence_before();
     }
+#ifdef CYR_FUSED_PROF
+    if ((blockIdx.x == 0 || blockIdx.x == 77) && lane == 0 &&
+        (warp == 0 || warp == kFusedEpi - 1 || warp == 5))
+      printf("EPI cta %d w%d per block: wait d1 %lld, epi1 %lld, wait d2 %lld, epi2 %lld, "
+             "wait d3 %lld\n", blockIdx.x, warp, eacc[0] / i, eacc[1] / i, eacc[2] / i,
+             eacc[3] / i, eacc[4] / i);
+#endif
   }
   tc_fence_before();
   __syncthreads();
