@@ -49,13 +49,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = _nvcc()
     headers = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "cyrus_b200.h")]
     objs, jobs = [], []
+    # CYR_NVCC_EXTRA: extra nvcc flags for A/B builds (e.g. -DNAME=VALUE); a
+    # change of flags since the last build rebuilds every object
+    extra = os.environ.get("CYR_NVCC_EXTRA", "").split()
+    stamp = os.path.join(BUILD, "flags.txt")
+    flags_now = " ".join(extra)
+    if not os.path.exists(stamp) or open(stamp).read() != flags_now:
+        force = True
     for src in SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            # CYR_NVCC_EXTRA: extra nvcc flags for A/B builds (e.g. -DNAME=VALUE)
-            extra = os.environ.get("CYR_NVCC_EXTRA", "").split()
             jobs.append([nvcc, *ARCH, *FLAGS, *extra, "-c", s, "-o", o])
 
     def run(cmd):
@@ -70,6 +75,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         list(pool.map(run, jobs))
     if force or jobs or _stale(LIB, objs):
         run([nvcc, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static"])
+    with open(stamp, "w") as fh:
+        fh.write(flags_now)
     build_fastpath(force=force, verbose=verbose)
     return LIB
 

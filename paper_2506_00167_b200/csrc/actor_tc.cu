@@ -88,6 +88,30 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
                    smem_u32(bar))
                : "memory");
 }
+// Warp-wide forms: the WHOLE (converged) warp executes these and elect.sync
+// picks the one lane that issues.  Issued from inside `if (lane == 0)`,
+// ptxas cannot prove the operands uniform and wraps every tcgen05.mma /
+// commit in an ELECT + R2UR.BROADCAST + BRA.U.ANY waterfall: ~150 cycles per
+// instruction measured in-kernel (64 MMAs: 9.7k cycles for N=256 and 10.9k
+// for N=32 alike), which bounded the narrow MLP's K-step rate.
+__device__ __forceinline__ void tc_mma_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, int accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -342,15 +366,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) actor_tc_kernel(const TcLaunch 
 // overlaps the head epilogue, and the features are never on the critical path.
 // A second block in flight would need a second 256-column fp32 accumulator:
 // TMEM (512 columns) holds D + A2 + A3 of one block and no more.
-// Measured (scripts/fused_probe.py, 2M Mode-R columns, event timing): 852 us
-// vs 937 us for the layer-by-layer kernels; per block the tensor pipe is busy
-// ~4.7k of ~15k cycles.  Per-block phase sums (CYR_FUSED_PROF, every block
-// of CTAs 0 and 77): MMA thread 15.2k cycles per block, of which waiting for
-// epi1 + MMA2 8.6k and for epi2 + MMA3 5.9k; epilogue warps 1.0-2.0k (epi1)
-// and 1.6k (epi2) of work, the rest waiting.  Splitting the head's K chain
-// over 2 or 4 accumulators changed nothing (not chain-latency-bound).  A/B knobs (compile-time): CYR_FUSED_EPI
-// (8 / 16 epilogue warps: 16), CYR_FUSED_NSPLIT (MMA2 in N halves: slower),
-// CYR_FUSED_PERPART (MMA2 K steps per landed part: slower), CYR_FUSED_FADD2.
+// Measured (scripts/fused_probe.py, 2M Mode-R columns, event timing): 474 us
+// = 46 % of the bf16 peak (852 us / 27 % before these changes):
+//  * MMA issue: every tcgen05.mma used to be its own asm inside `lane == 0`;
+//    ptxas wrapped each in an ELECT / R2UR.BROADCAST / BRA.U.ANY waterfall,
+//    ~146 cycles per instruction whatever N (scripts/micro/mma_rate.cu).  Now
+//    the whole warp runs the loop and one asm issues a K tile (4 MMAs) with
+//    the per-step operands added inside the asm: 17.5 cycles for N = 32,
+//    129 for N = 256 (the pipe floor is 128 * N / 256);
+//  * the head output (128 x out fp32 per block) used to be 20 scattered
+//    4-byte stores per thread by epilogue part 0, ~3.6k cycles on the
+//    critical path (epi1 of the next block waited for it); now the builder
+//    warps read D3, release it (d3free), stage the block's logits row-major
+//    in shared memory and write them with one bulk copy;
+//  * no integer division left in the issue loop (the per-part K-step
+//    bookkeeping of the PERPART / NSPLIT experiments is gone).
+// Per block (CYR_FUSED_PROF trace, CTA 0): MMA1 0.3k issue + 0.6k, epi1 1.4k,
+// MMA2 2.1k + ~0.3k wake-up, epi2 1.7k, MMA3 0.6k + ~0.5k wake-up: ~8.1k
+// cycles, the tensor pipe busy ~2.9k of them.  A/B knobs (compile-time):
+// CYR_FUSED_EPI (8 / 16 epilogue warps: 16), CYR_FUSED_FADD2.
 #ifndef CYR_FUSED_GROUPS
 #define CYR_FUSED_GROUPS 1
 #endif
@@ -373,6 +407,56 @@ __device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+__device__ __forceinline__ void tc_mma_ts_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                            uint32_t idesc, int accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Four consecutive K steps (K = 64, one SW128 K tile) in ONE asm statement,
+// the per-step operands derived INSIDE the asm from one base each.  Measured
+// (scripts/micro/mma_rate.cu, M = 128, TS): one asm per MMA 146 cycles per
+// instruction whatever N; four per asm with the operands precomputed in C
+// (each a separate R2UR) 52-59; four per asm with in-asm adds 17.5 for
+// N = 32, 33 for N = 64, 129 for N = 256 -- the tensor-pipe floor
+// 128 * N / 256.  B descriptors of consecutive K steps inside one SW128 atom
+// are 32 bytes (+2 in the start-address field) apart; A columns in TMEM 8.
+__device__ __forceinline__ void tc_mma_ts_x4(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                             uint32_t idesc, int accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 ta;\n\t.reg .b64 bd;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "add.u32 ta, %1, 8;\n\tadd.u64 bd, %2, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, 1;\n\t"
+      "add.u32 ta, %1, 16;\n\tadd.u64 bd, %2, 4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, 1;\n\t"
+      "add.u32 ta, %1, 24;\n\tadd.u64 bd, %2, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, 1;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_ss_x4(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t idesc, int accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 ad, bd;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "add.u64 ad, %1, 2;\n\tadd.u64 bd, %2, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ad, bd, %3, 1;\n\t"
+      "add.u64 ad, %1, 4;\n\tadd.u64 bd, %2, 4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ad, bd, %3, 1;\n\t"
+      "add.u64 ad, %1, 6;\n\tadd.u64 bd, %2, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ad, bd, %3, 1;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
@@ -393,9 +477,13 @@ __device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&r)[16])
       : "memory");
 }
 
+#ifdef CYR_FUSED_PROF
+__device__ int g_fused_trace_launch = 0;
+#endif
 struct FusedLayout {  // shared-memory carve-up (bytes from the 1024-aligned base)
-  uint32_t w_off[3], w_bytes[3], feat, bias, bars, total;
+  uint32_t w_off[3], w_bytes[3], feat, bias, bars, stage, stage_bytes, total;
 };
+constexpr uint32_t kSmemOptinSm100 = 232448;  // 227 KB opt-in per CTA on sm_100
 
 __host__ __device__ inline FusedLayout fused_layout(const ActorDesc& d, const int* npad) {
   FusedLayout f{};
@@ -412,6 +500,18 @@ __host__ __device__ inline FusedLayout fused_layout(const ActorDesc& d, const in
   off = (off + 7u) & ~7u;
   f.bars = off;
   off += 32 * 8 + 16;
+  // head output stage: the block's [128 x out] fp32 logits, row-major, i.e.
+  // exactly its contiguous slice of `raw`, written by one bulk copy instead
+  // of 128 threads x out scattered 4-byte stores (80-byte stride: every warp
+  // store touched 32 sectors; ~3.6k cycles per block on the critical path).
+  // Left out (stage_bytes = 0, direct stores) when it would not fit.
+  off = (off + 127u) & ~127u;
+  const uint32_t sb = (uint32_t)kTcM * (uint32_t)d.layer[2].out * 4u;
+  if (off + sb + 1024 <= kSmemOptinSm100) {
+    f.stage = off;
+    f.stage_bytes = sb;
+    off += sb;
+  }
   f.total = off + 1024;  // alignment slack
   return f;
 }
@@ -471,9 +571,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const 
   uint64_t* d1full = bars + 9;    // MMA1 complete
   uint64_t* a2p = bars + 10;      // [kFusedParts] epi1 part p complete (its 4 warps): the
                                   // A2 K columns of part p are in TMEM, its D1 columns drained
-  uint64_t* d2full = bars + 14;   // [2] MMA2 complete, N half 0 / 1
+  uint64_t* d2full = bars + 14;   // MMA2 complete
   uint64_t* a3p = bars + 16;      // [kFusedParts] epi2 part p complete
   uint64_t* d3full = bars + 20;   // MMA3 complete
+  uint64_t* d3free = bars + 21;   // head (builder warps) has read D3 out of TMEM
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n1 = p.tc_npad[0], n2 = p.tc_npad[1], n3 = p.tc_npad[2];
@@ -496,9 +597,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const 
       mbar_init(&a2p[q], 4);
       mbar_init(&a3p[q], 4);
     }
-    mbar_init(&d2full[0], 1);
-    mbar_init(&d2full[1], 1);
+    mbar_init(d2full, 1);
     mbar_init(d3full, 1);
+    mbar_init(d3free, 4);
     fence_mbar_init();
   }
   {  // biases (fp32) -> shared, zero past each layer's width
@@ -515,6 +616,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+#ifdef CYR_FUSED_PROF
+  __shared__ long long trace[64];  // one steady-state block's event clocks (CTA 0)
+  constexpr int kTraceBlock = 100;
+#define CYR_TRACE(slot, it) \
+  if ((it) == kTraceBlock && lane == 0) trace[slot] = clock64();
+#endif
   const float* bias1 = sbias;
   const float* bias2 = sbias + n1;
   const float* bias3 = sbias + n1 + n2;
@@ -530,18 +637,22 @@ __global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const 
           const uint32_t nbytes = min(16384u, f.w_bytes[l] - c);
           bulk_g2s(base + f.w_off[l] + c, p.tc_blob + p.tc_off[l] + c, nbytes, wbar);
         }
+    }
+    __syncwarp();
+    {  // the whole warp runs the issue loop; the tc_mma_* asm elect the issuing lane
+      // The only CTA on the SM allocates all 512 columns, so the allocation
+      // starts at lane 0, column 0.  With the base a compile-time 0 the MMA
+      // operands are immediates and uniform-datapath adds; from the base read
+      // out of shared memory ptxas re-broadcast every operand of every MMA
+      // (R2UR.BROADCAST), ~100 cycles per N = 32 MMA instead of ~17.
+      if (tmem != 0u) __trap();
+      constexpr uint32_t tm = 0u;
       mbar_wait(wbar, 0);
       tc_fence_after();
       const uint32_t id1 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n1 >> 3) << 17) |
                            ((uint32_t)(kTcM >> 4) << 24);
-#ifndef CYR_FUSED_NSPLIT
-#define CYR_FUSED_NSPLIT 0
-#endif
-      // CYR_FUSED_NSPLIT=1: MMA2 in two N halves, so the epilogue of half 0
-      // overlaps the MMAs of half 1 (A/B: slower, the halves read A2 twice)
-      constexpr int NH = CYR_FUSED_NSPLIT ? 2 : 1;
-      const uint32_t id2 = (1u << 4) | (1u << 7) | (1u << 10) |
-                           ((uint32_t)(n2 / NH >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
+      const uint32_t id2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n2 >> 3) << 17) |
+                           ((uint32_t)(kTcM >> 4) << 24);
       const uint32_t id3 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n3 >> 3) << 17) |
                            ((uint32_t)(kTcM >> 4) << 24);
       const uint32_t w1 = smem_u32(base + f.w_off[0]), w2 = smem_u32(base + f.w_off[1]),
@@ -562,138 +673,152 @@ __global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const 
         tc_fence_after();
 #ifdef CYR_FUSED_PROF
         const long long pt1 = clock64();
+        CYR_TRACE(0, i)
 #endif
         const uint32_t a1 = smem_u32(feat + fb * kTcM * 128);
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks)
-          tc_mma(tmem, umma_desc_sw128(a1 + ks * 32), umma_desc_sw128(w1 + ks * 32), id1,
-                 ks > 0 ? 1 : 0);
-        tc_commit(&ffree[fb]);
-        tc_commit(d1full);
+        tc_mma_ss_x4(tm, umma_desc_sw128(a1), umma_desc_sw128(w1), id1, 0);
+        tc_commit_w(&ffree[fb]);
+        tc_commit_w(d1full);
 #ifdef CYR_FUSED_PROF
         const long long pt2 = clock64();
+        CYR_TRACE(1, i)
+#ifdef CYR_FUSED_PROF_SERIAL  // exec time of MMA1 alone (serialises the issue)
+        mbar_wait(d1full, ph);
+        pacc[1] += clock64() - pt2;
+#endif
 #endif
 #ifdef CYR_FUSED_PROF
         const long long pt3 = clock64();
 #endif
-        // MMA2's K steps of part q start as soon as epi1 part q has written
-        // them (the first parts finish well before the last)
-#ifndef CYR_FUSED_PERPART
-#define CYR_FUSED_PERPART 0
-#endif
-        // per part (A/B): CYR_FUSED_PERPART=1 starts K steps as parts land;
-        // 0 waits for every part before the first MMA
-        const int k2 = CYR_FUSED_PERPART ? n1 / 16 / kFusedParts : n1 / 16;
-        const int k3 = CYR_FUSED_PERPART ? n2 / 16 / kFusedParts : n2 / 16;
-        for (int h = 0; h < NH; ++h) {  // rows [h * n2/2, ...) of W2 start (n2/2/8) * 1 KB in
-          const uint32_t wb = w2 + (uint32_t)h * (uint32_t)(n2 / 16) * 1024u;
-          for (int ks = 0; ks < n1 / 16; ++ks) {
-            if (h == 0 && ks % k2 == 0) {
-              for (int q = ks / k2 * (kFusedParts * k2 * 16 / n1);
-                   q < (ks / k2 + 1) * (kFusedParts * k2 * 16 / n1); ++q)
-                mbar_wait(&a2p[q], ph);
-              tc_fence_after();
-            }
-            tc_mma_ts(tmem + (uint32_t)(h * (n2 / NH)), tmem + (uint32_t)(kFusedA2Col + ks * 8),
-                      umma_desc_sw128(wb + (uint32_t)(ks >> 2) * t2 + (uint32_t)(ks & 3) * 32),
-                      id2, ks > 0 ? 1 : 0);
-          }
-          tc_commit(&d2full[h]);
-        }
-        if (NH == 1) tc_commit(&d2full[1]);
+        // MMA2 once every epi1 part has written its A2 K columns (and drained
+        // its D1 columns).  Starting the K steps of each part as it lands, or
+        // MMA2 in two N halves, measured slower (A/B in round 2).
+        for (int q = 0; q < kFusedParts; ++q) mbar_wait(&a2p[q], ph);
+        tc_fence_after();
+        for (int ks = 0; ks < n1 / 16; ks += 4)
+          tc_mma_ts_x4(tm, tm + (uint32_t)(kFusedA2Col + ks * 8),
+                       umma_desc_sw128(w2 + (uint32_t)(ks >> 2) * t2), id2, ks > 0 ? 1 : 0);
+        tc_commit_w(d2full);
 #ifdef CYR_FUSED_PROF
         const long long pt4 = clock64();
+        CYR_TRACE(2, i)
 #endif
 #ifdef CYR_FUSED_PROF
         const long long pt5 = clock64();
 #endif
-        for (int ks = 0; ks < n2 / 16; ++ks) {
-          if (ks % k3 == 0) {  // epi2 part q: its A3 K columns written, its D2 columns drained
-            for (int q = ks / k3 * (kFusedParts * k3 * 16 / n2);
-                 q < (ks / k3 + 1) * (kFusedParts * k3 * 16 / n2); ++q)
-              mbar_wait(&a3p[q], ph);
-            tc_fence_after();
-          }
-          tc_mma_ts(tmem + kFusedD3Col, tmem + (uint32_t)(kFusedA3Col + ks * 8),
-                    umma_desc_sw128(w3 + (uint32_t)(ks >> 2) * t3 + (uint32_t)(ks & 3) * 32), id3,
-                    ks > 0 ? 1 : 0);
-        }
-        tc_commit(d3full);
+        // MMA3 (the head) once every epi2 part has written A3 / drained D2
+        for (int q = 0; q < kFusedParts; ++q) mbar_wait(&a3p[q], ph);
+        tc_fence_after();
 #ifdef CYR_FUSED_PROF
+        CYR_TRACE(22, i)
+#endif
+        for (int ks = 0; ks < n2 / 16; ks += 4) {
+          tc_mma_ts_x4(tm + kFusedD3Col, tm + (uint32_t)(kFusedA3Col + ks * 8),
+                       umma_desc_sw128(w3 + (uint32_t)(ks >> 2) * t3), id3, ks > 0 ? 1 : 0);
+#ifdef CYR_FUSED_PROF
+          if (ks / 4 < 4) { CYR_TRACE(56 + ks / 4, i) }
+#endif
+        }
+#ifdef CYR_FUSED_PROF
+        CYR_TRACE(23, i)
+#endif
+        tc_commit_w(d3full);
+#ifdef CYR_FUSED_PROF
+#ifdef CYR_FUSED_PROF_SERIAL  // exec time of MMA3 alone
+        {
+          const long long t = clock64();
+          mbar_wait(d3full, ph);
+          pacc[2] += clock64() - t;
+        }
+#endif
         const long long pt6 = clock64();
-        pacc[0] += pt1 - pt0; pacc[1] += pt2 - pt1; pacc[2] += pt3 - pt2;
+        CYR_TRACE(3, i)
+        pacc[0] += pt1 - pt0; pacc[1] += pt2 - pt1;
         pacc[3] += pt4 - pt3; pacc[4] += pt5 - pt4; pacc[5] += pt6 - pt5;
 #endif
       }
 #ifdef CYR_FUSED_PROF
-      if (blockIdx.x == 0 || blockIdx.x == 77)
+      if ((blockIdx.x == 0 || blockIdx.x == 77) && lane == 0)
         printf("MMA cta %d blocks %d per block: wait feat %lld, mma1 %lld, wait a2 %lld, mma2 %lld, "
-               "wait a3 %lld, mma3 %lld, total %lld\n", blockIdx.x, i, pacc[0] / i, pacc[1] / i,
+               "wait a3 %lld, mma3 %lld, total %lld (SERIAL: wait a2 = MMA3 exec, mma1 = issue + exec)\n", blockIdx.x, i, pacc[0] / i, pacc[1] / i,
                pacc[2] / i, pacc[3] / i, pacc[4] / i, pacc[5] / i, (clock64() - pstart) / i);
 #endif
     }
     __syncwarp();
   } else if (warp >= kFusedEpi) {
-    // ---------------------------------------------------- feature builders
-    const int grp = (warp - kFusedEpi) >> 2, row = (tid - 32 * kFusedEpi) & 127;
-    int i = 0;
-    for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
-      const int fb = i % NB;
-      if (kFusedGroups > 1 && fb != grp) continue;
-      if (i >= NB) mbar_wait(&ffree[fb], (uint32_t)(((i / NB) - 1) & 1));
-      tc_feature_tile(p, b * kTcM + row, 0, feat + fb * kTcM * 128, row);
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ffull[fb]);
-    }
-  } else {
-    // ------------------------------------------------------------ epilogues
-    const int quarter = warp & 3, part = warp >> 2;
-    const int row = quarter * 32 + lane;  // TMEM lane = column within the block
+    // ------------------------------------------- feature builders + head
+    // Block i's feature tile, then the head output of block i - 1: its D3
+    // is read out of TMEM (then `d3free` lets the epilogues overwrite those
+    // columns with A2 of block i + 1), staged row-major in shared memory and
+    // written by one bulk copy.  Off the epilogue warps, the head no longer
+    // delays epi1 of the next block (the MMA2 input): 10.1k -> see DESIGN.
+    static_assert(kFusedGroups == 1, "the head runs on the single builder group");
+    const int quarter = warp & 3, row = (tid - 32 * kFusedEpi) & 127;
+    const bool leader = warp == kFusedEpi && lane == 0;
     const int out3 = p.desc.layer[2].out;
-    int i = 0;
 #ifdef CYR_FUSED_PROF
-    long long eacc[5] = {0, 0, 0, 0, 0};
+    long long bacc[3] = {0, 0, 0};
 #endif
-    for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
-      const uint32_t ph = (uint32_t)(i & 1);
+    auto head = [&](int hb, int hi) {
 #ifdef CYR_FUSED_PROF
-      const long long q0 = clock64();
+      const long long h0 = clock64();
 #endif
-      mbar_wait(d1full, ph);
+      mbar_wait(d3full, (uint32_t)(hi & 1));
       tc_fence_after();
 #ifdef CYR_FUSED_PROF
-      const long long q1 = clock64();
+      const long long h1 = clock64();
+      if (warp == kFusedEpi) { CYR_TRACE(20, hi) }
 #endif
-      fused_hidden_epi(tmem, quarter, part, n1, 0, kFusedA2Col, bias1);
-#ifdef CYR_FUSED_PROF
-      const long long q2 = clock64();
-#endif
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&a2p[part]);
-      mbar_wait(&d2full[part >= kFusedParts / 2 ? 1 : 0], ph);
-      tc_fence_after();
-#ifdef CYR_FUSED_PROF
-      const long long q3 = clock64();
-#endif
-      fused_hidden_epi(tmem, quarter, part, n2, 0, kFusedA3Col, bias2);
-#ifdef CYR_FUSED_PROF
-      const long long q4 = clock64();
-#endif
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&a3p[part]);
-      mbar_wait(d3full, ph);
-      tc_fence_after();
-#ifdef CYR_FUSED_PROF
-      const long long q5 = clock64();
-      eacc[0] += q1 - q0; eacc[1] += q2 - q1; eacc[2] += q3 - q2; eacc[3] += q4 - q3;
-      eacc[4] += q5 - q4;
-#endif
-      if (part == 0) {
-        const int col = b * kTcM + row;
-        const uint32_t lanes = (uint32_t)(quarter * 32) << 16;
+      const uint32_t lanes = (uint32_t)(quarter * 32) << 16;
+      if (f.stage_bytes) {
+        // explicit st.shared: through a generic pointer every store was
+        // ordered against the next bias load (possible alias)
+        const uint32_t st = smem_u32(base + f.stage) + (uint32_t)(row * out3) * 4u;
+        auto stage16 = [&](const uint32_t (&r)[16], int n0) {
+          float v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]) + bias3[n0 + j];
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (n0 + j < out3)
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(st + (uint32_t)(n0 + j) * 4u), "f"(v[j])
+                           : "memory");
+        };
+        if (n3 <= 32) {  // both chunks in registers: D3 is released before the stores
+          uint32_t r0[16], r1[16];
+          tc_ld16(tmem + lanes + (uint32_t)kFusedD3Col, r0);
+          if (n3 > 16) tc_ld16(tmem + lanes + (uint32_t)(kFusedD3Col + 16), r1);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(d3free);
+          stage16(r0, 0);
+          if (n3 > 16) stage16(r1, 16);
+        } else {
+          for (int n0 = 0; n0 < n3; n0 += 16) {
+            uint32_t r[16];
+            tc_ld16(tmem + lanes + (uint32_t)(kFusedD3Col + n0), r);
+            stage16(r, n0);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(d3free);
+        }
+        fence_proxy_async_smem();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int valid = min(kTcM, p.ncols - hb * kTcM);
+        const uint32_t bytes = (uint32_t)valid * (uint32_t)out3 * 4u;
+        float* dst = p.raw + (long long)hb * kTcM * out3;
+        if (bytes % 16u == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+          if (leader) {
+            bulk_s2g(dst, base + f.stage, bytes);
+            bulk_commit();
+          }
+        } else {  // ragged last block / unaligned output: coalesced word copy
+          const float* s0 = reinterpret_cast<const float*>(base + f.stage);
+          for (int e = row; e < valid * out3; e += kTcM) dst[e] = s0[e];
+        }
+      } else {  // no room for the stage: direct stores
+        const int col = hb * kTcM + row;
         for (int n0 = 0; n0 < n3; n0 += 16) {
           uint32_t r[16];
           tc_ld16(tmem + lanes + (uint32_t)(kFusedD3Col + n0), r);
@@ -704,19 +829,137 @@ __global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const 
               if (n0 + j < out3) dst[n0 + j] = __uint_as_float(r[j]) + bias3[n0 + j];
           }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(d3free);
       }
+#ifdef CYR_FUSED_PROF
+      if (warp == kFusedEpi) { CYR_TRACE(21, hi) }
+      bacc[1] += h1 - h0;
+      bacc[2] += clock64() - h1;
+#endif
+    };
+    int i = 0, prev = -1;
+    for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
+      const int fb = i % NB;
+#ifdef CYR_FUSED_PROF
+      const long long f0 = clock64();
+      if (warp == kFusedEpi) { CYR_TRACE(60, i - 1) }
+#endif
+      if (i >= NB) mbar_wait(&ffree[fb], (uint32_t)(((i / NB) - 1) & 1));
+      tc_feature_tile(p, b * kTcM + row, 0, feat + fb * kTcM * 128, row);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ffull[fb]);
+#ifdef CYR_FUSED_PROF
+      bacc[0] += clock64() - f0;
+      if (warp == kFusedEpi) { CYR_TRACE(61, i - 1) }
+#endif
+      if (prev >= 0) {
+        // the stage is free once the previous bulk store has read it
+        if (f.stage_bytes) {
+          if (leader) bulk_wait_read<0>();
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
+        head(prev, i - 1);
+      }
+      prev = b;
+    }
+    if (prev >= 0) {
+      if (f.stage_bytes) {
+        if (leader) bulk_wait_read<0>();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+      head(prev, i - 1);
+    }
+    if (leader) bulk_wait_all();
+#ifdef CYR_FUSED_PROF
+    if ((blockIdx.x == 0 || blockIdx.x == 77) && lane == 0 && warp == kFusedEpi)
+      printf("BUILD cta %d w%d per block: feature %lld, head wait d3 %lld, head %lld\n",
+             blockIdx.x, warp, bacc[0] / i, bacc[1] / i, bacc[2] / i);
+#endif
+  } else {
+    // ------------------------------------------------------------ epilogues
+    const int quarter = warp & 3, part = warp >> 2;
+    int i = 0;
+#ifdef CYR_FUSED_PROF
+    long long eacc[5] = {0, 0, 0, 0, 0};
+#endif
+    for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
+      const uint32_t ph = (uint32_t)(i & 1);
+#ifdef CYR_FUSED_PROF
+      const long long q0 = clock64();
+#endif
+      mbar_wait(d1full, ph);
+#ifdef CYR_FUSED_PROF
+      const long long q0b = clock64();
+#endif
+      // A2 shares TMEM columns with the previous block's D3 (head output)
+      if (i > 0) mbar_wait(d3free, ph ^ 1u);
+      tc_fence_after();
+#ifdef CYR_FUSED_PROF
+      const long long q1 = clock64();
+      if ((warp % 5) == 0) { CYR_TRACE(4 + (warp / 5) * 4 + 0, i) }
+      eacc[4] += q1 - q0b;
+#endif
+      fused_hidden_epi(tmem, quarter, part, n1, 0, kFusedA2Col, bias1);
+#ifdef CYR_FUSED_PROF
+      const long long q2 = clock64();
+      if ((warp % 5) == 0) { CYR_TRACE(4 + (warp / 5) * 4 + 1, i) }
+      CYR_TRACE(24 + warp, i)
+#endif
       tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a2p[part]);
+      mbar_wait(d2full, ph);
+      tc_fence_after();
+#ifdef CYR_FUSED_PROF
+      const long long q3 = clock64();
+      if ((warp % 5) == 0) { CYR_TRACE(4 + (warp / 5) * 4 + 2, i) }
+#endif
+      fused_hidden_epi(tmem, quarter, part, n2, 0, kFusedA3Col, bias2);
+#ifdef CYR_FUSED_PROF
+      const long long q4 = clock64();
+      if ((warp % 5) == 0) { CYR_TRACE(4 + (warp / 5) * 4 + 3, i) }
+      CYR_TRACE(40 + warp, i)
+      eacc[0] += q1 - q0; eacc[1] += q2 - q1; eacc[2] += q3 - q2; eacc[3] += q4 - q3;
+#endif
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a3p[part]);
     }
 #ifdef CYR_FUSED_PROF
     if ((blockIdx.x == 0 || blockIdx.x == 77) && lane == 0 &&
         (warp == 0 || warp == kFusedEpi - 1 || warp == 5))
-      printf("EPI cta %d w%d per block: wait d1 %lld, epi1 %lld, wait d2 %lld, epi2 %lld, "
-             "wait d3 %lld\n", blockIdx.x, warp, eacc[0] / i, eacc[1] / i, eacc[2] / i,
-             eacc[3] / i, eacc[4] / i);
+      printf("EPI cta %d w%d per block: wait d1 %lld (of it d3free %lld), epi1 %lld, wait d2 %lld, "
+             "epi2 %lld\n", blockIdx.x, warp, eacc[0] / i, eacc[4] / i, eacc[1] / i, eacc[2] / i,
+             eacc[3] / i);
 #endif
   }
   tc_fence_before();
   __syncthreads();
+#ifdef CYR_FUSED_PROF
+  if (tid == 0 && blockIdx.x == 0 && nblocks > kTraceBlock * (int)gridDim.x &&
+      atomicAdd(&g_fused_trace_launch, 1) == 4) {  // one launch (the 5th large one) prints
+    const long long t0 = trace[0];
+    printf("TRACE cta 0 block %d (clock - MMA1 issue start): MMA feat-ok 0, mma1-issued %lld, "
+           "mma2-issued %lld, mma3-issued %lld | head d3-seen %lld, head-done %lld\n", kTraceBlock,
+           trace[1] - t0, trace[2] - t0, trace[3] - t0, trace[20] - t0, trace[21] - t0);
+    printf("TRACE cta 0 builder feat(next) start %lld end %lld\n", trace[60] - t0, trace[61] - t0);
+    printf("TRACE cta 0 MMA a3-all-seen %lld, mma3 groups %lld %lld %lld %lld, before-commit %lld\n",
+           trace[22] - t0, trace[56] - t0, trace[57] - t0, trace[58] - t0, trace[59] - t0,
+           trace[23] - t0);
+    for (int w = 0; w < 4; ++w)
+      printf("TRACE cta 0 epi w%d: d1-seen %lld, epi1-done %lld, d2-seen %lld, epi2-done %lld\n",
+             w * 5, trace[4 + w * 4] - t0, trace[5 + w * 4] - t0, trace[6 + w * 4] - t0,
+             trace[7 + w * 4] - t0);
+    printf("TRACE cta 0 all epi1-done:");
+    for (int w = 0; w < kFusedEpi; ++w) printf(" w%d %lld", w, trace[24 + w] - t0);
+    printf("\nTRACE cta 0 all epi2-done:");
+    for (int w = 0; w < kFusedEpi; ++w) printf(" w%d %lld", w, trace[40 + w] - t0);
+    printf("\n");
+  }
+#endif
   if (warp == 0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
