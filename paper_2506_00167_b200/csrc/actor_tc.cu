@@ -74,42 +74,57 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
-__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                       uint32_t idesc, int accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
-}
-// Warp-wide forms: the WHOLE (converged) warp executes these and elect.sync
-// picks the one lane that issues.  Issued from inside `if (lane == 0)`,
-// ptxas cannot prove the operands uniform and wraps every tcgen05.mma /
-// commit in an ELECT + R2UR.BROADCAST + BRA.U.ANY waterfall: ~150 cycles per
-// instruction measured in-kernel (64 MMAs: 9.7k cycles for N=256 and 10.9k
-// for N=32 alike), which bounded the narrow MLP's K-step rate.
-__device__ __forceinline__ void tc_mma_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                         uint32_t idesc, int accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
+// MMA issue is warp-wide: the WHOLE (converged) warp runs the issue loop and
+// elect.sync inside each asm picks the one lane that issues.  Issued from
+// inside `if (lane == 0)`, ptxas cannot prove the operands uniform and wraps
+// every tcgen05.mma / commit in an ELECT + R2UR.BROADCAST + BRA.U.ANY
+// waterfall (~146 cycles per instruction whatever N).
 __device__ __forceinline__ void tc_commit_w(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
           smem_u32(bar))
+      : "memory");
+}
+// Four consecutive K steps (K = 64, one SW128 K tile) in ONE asm statement,
+// the per-step operands derived INSIDE the asm from one base each.  Measured
+// (scripts/micro/mma_rate.cu, M = 128, TS): one asm per MMA 146 cycles per
+// instruction whatever N; four per asm with the operands precomputed in C
+// (each a separate R2UR) 52-59; four per asm with in-asm adds 17.5 for
+// N = 32, 33 for N = 64, 129 for N = 256 -- the tensor-pipe floor
+// 128 * N / 256.  B descriptors of consecutive K steps inside one SW128 atom
+// are 32 bytes (+2 in the start-address field) apart; A columns in TMEM 8.
+__device__ __forceinline__ void tc_mma_ts_x4(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                             uint32_t idesc, int accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 ta;\n\t.reg .b64 bd;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "add.u32 ta, %1, 8;\n\tadd.u64 bd, %2, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, 1;\n\t"
+      "add.u32 ta, %1, 16;\n\tadd.u64 bd, %2, 4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, 1;\n\t"
+      "add.u32 ta, %1, 24;\n\tadd.u64 bd, %2, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, 1;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_ss_x4(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t idesc, int accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 ad, bd;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "add.u64 ad, %1, 2;\n\tadd.u64 bd, %2, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ad, bd, %3, 1;\n\t"
+      "add.u64 ad, %1, 4;\n\tadd.u64 bd, %2, 4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ad, bd, %3, 1;\n\t"
+      "add.u64 ad, %1, 6;\n\tadd.u64 bd, %2, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ad, bd, %3, 1;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 __device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
@@ -207,7 +222,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) actor_tc_kernel(const TcLaunch 
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_mma + 1);
 
   const int tid = threadIdx.x;
-  const int warp = tid >> 5;
+  const int warp = tid >> 5, lane = tid & 31;
   const int c0 = blockIdx.x * kTcM;
   const int nl = p.desc.n_layers;
 
@@ -273,7 +288,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) actor_tc_kernel(const TcLaunch 
     const int npad = p.tc_npad[l];
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(npad >> 3) << 17) |
                            ((uint32_t)(kTcM >> 4) << 24);
-    if (tid == 0) {
+    if (warp == 0) {  // whole warp: the K-tile asm elects the issuing lane
       tc_fence_after();
       for (int t = 0; t < kt; ++t, ++g) {
         const int slot = g % kTcSlots;
@@ -281,14 +296,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) actor_tc_kernel(const TcLaunch 
         tc_fence_after();
         const uint32_t a_addr = smem_u32(a_tiles + t * kTcM * 128);
         const uint32_t b_addr = smem_u32(ring + (size_t)slot * kTcSlotBytes);
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks)
-          tc_mma(tmem, umma_desc_sw128(a_addr + ks * 32), umma_desc_sw128(b_addr + ks * 32),
-                 idesc, (t > 0 || ks > 0) ? 1 : 0);
-        tc_commit(&bar_free[slot]);  // slot reusable once these MMAs retire
-        issue(g + kTcSlots - 1);     // refill the slot freed by the previous tile
+        tc_mma_ss_x4(tmem, umma_desc_sw128(a_addr), umma_desc_sw128(b_addr), idesc, t > 0 ? 1 : 0);
+        tc_commit_w(&bar_free[slot]);  // slot reusable once these MMAs retire
+        if (lane == 0) issue(g + kTcSlots - 1);  // refill the slot freed by the previous tile
+        __syncwarp();
       }
-      tc_commit(bar_mma);  // accumulator complete
+      tc_commit_w(bar_mma);  // accumulator complete
     }
     // epilogue: TMEM lane (32*warp + lane) = batch column c0 + tid
     mbar_wait(bar_mma, (uint32_t)(mma_phase & 1));
@@ -398,65 +411,6 @@ constexpr int kFusedMmaWarp = kFusedEpi + 4 * kFusedGroups;
 constexpr int kFusedThreads = 32 * (kFusedMmaWarp + 1);
 constexpr int kFusedA2Col = 256, kFusedA3Col = 384, kFusedD3Col = 256;
 
-__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
-                                          uint32_t idesc, int accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void tc_mma_ts_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
-                                            uint32_t idesc, int accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// Four consecutive K steps (K = 64, one SW128 K tile) in ONE asm statement,
-// the per-step operands derived INSIDE the asm from one base each.  Measured
-// (scripts/micro/mma_rate.cu, M = 128, TS): one asm per MMA 146 cycles per
-// instruction whatever N; four per asm with the operands precomputed in C
-// (each a separate R2UR) 52-59; four per asm with in-asm adds 17.5 for
-// N = 32, 33 for N = 64, 129 for N = 256 -- the tensor-pipe floor
-// 128 * N / 256.  B descriptors of consecutive K steps inside one SW128 atom
-// are 32 bytes (+2 in the start-address field) apart; A columns in TMEM 8.
-__device__ __forceinline__ void tc_mma_ts_x4(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
-                                             uint32_t idesc, int accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t.reg .b32 ta;\n\t.reg .b64 bd;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
-      "add.u32 ta, %1, 8;\n\tadd.u64 bd, %2, 2;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, 1;\n\t"
-      "add.u32 ta, %1, 16;\n\tadd.u64 bd, %2, 4;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, 1;\n\t"
-      "add.u32 ta, %1, 24;\n\tadd.u64 bd, %2, 6;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, 1;\n\t}" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void tc_mma_ss_x4(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                             uint32_t idesc, int accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t.reg .b64 ad, bd;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
-      "add.u64 ad, %1, 2;\n\tadd.u64 bd, %2, 2;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ad, bd, %3, 1;\n\t"
-      "add.u64 ad, %1, 4;\n\tadd.u64 bd, %2, 4;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ad, bd, %3, 1;\n\t"
-      "add.u64 ad, %1, 6;\n\tadd.u64 bd, %2, 6;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ad, bd, %3, 1;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
 __device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
@@ -1104,7 +1058,7 @@ __global__ void __launch_bounds__(kWideFirstThreads, 1) actor_tc_wide_kernel(con
     }
   } else if (warp == 9) {
     // ---------------------------------------------------------- MMA issuer
-    if (lane == 0) {
+    {  // whole warp: one asm per K tile elects the issuing lane (tc_mma_ss_x4)
       long long st = 0;
       int a = 0, i = 0;
       for (int cb = cb0; cb < q.ncb; cb += cbs, ++i) {
@@ -1130,15 +1084,12 @@ __global__ void __launch_bounds__(kWideFirstThreads, 1) actor_tc_wide_kernel(con
             const uint32_t s_addr = smem_u32(ring + (size_t)slot * q.slot_bytes);
             const uint32_t a_addr = FIRST ? smem_u32(feat + fb * kWideImage) : s_addr;
             const uint32_t b_addr = s_addr + q.a_bytes;
-#pragma unroll
-            for (int ks = 0; ks < 4; ++ks)
-              tc_mma(d, umma_desc_sw128(a_addr + ks * 32), umma_desc_sw128(b_addr + ks * 32),
-                     idesc, (t > 0 || ks > 0) ? 1 : 0);
-            tc_commit(&freeb[slot]);
+            tc_mma_ss_x4(d, umma_desc_sw128(a_addr), umma_desc_sw128(b_addr), idesc, t > 0 ? 1 : 0);
+            tc_commit_w(&freeb[slot]);
           }
-          tc_commit(&tfull[acc]);
+          tc_commit_w(&tfull[acc]);
         }
-        if (FIRST) tc_commit(&ffree[fb]);
+        if (FIRST) tc_commit_w(&ffree[fb]);
       }
     }
     __syncwarp();
