@@ -338,6 +338,10 @@ int cyr_selftest_latency(int32_t which, int32_t iters, int64_t* cycles);
 /* Measured fp32 FMA throughput of the current device (TFLOP/s): FFMA2
  * chains on every SM, event-timed (the SIMT actor's roofline peak). */
 int cyr_selftest_fma_peak(int32_t iters, double* tflops);
+/* The lane K3's shared-divisor quotient (one reciprocal, FMA corrections,
+ * projection.cuh) against IEEE division on pairs_total pseudo-random operand
+ * pairs (seeded): *mismatches = pairs whose bits differ (0 expected). */
+int cyr_selftest_shared_divisor(int64_t pairs_total, uint64_t seed, int64_t* mismatches);
 int cyr_selftest_launch(int32_t cluster, int32_t reps, int64_t* ns_per_launch);
 /* Phase timestamps (%globaltimer, ns) of the last latency-path launch when
  * the process runs with CYR_TRACE=1; zeros otherwise.  n <= 64. */

@@ -78,6 +78,7 @@ SIGNATURES = {
     "cyr_selftest_latency": (_c_int, [_c_i32, _c_i32, _pi64]),
     "cyr_selftest_launch": (_c_int, [_c_i32, _c_i32, _pi64]),
     "cyr_selftest_fma_peak": (_c_int, [_c_i32, ctypes.POINTER(ctypes.c_double)]),
+    "cyr_selftest_shared_divisor": (_c_int, [ctypes.c_int64, ctypes.c_uint64, _pi64]),
 }
 
 

@@ -1211,9 +1211,9 @@ int cyr_debug_trace(int64_t* out, int32_t n) {
   for (int i = 0; i < n && i < 64; ++i)
     out[i] = g_trace_host ? (int64_t)g_trace_host[i] : 0;
   if (g_prof_dev != nullptr) {
-    unsigned long long h[9] = {};
+    unsigned long long h[16] = {};
     cudaMemcpy(h, g_prof_dev, sizeof(h), cudaMemcpyDeviceToHost);
-    for (int i = 0; i < 9 && 36 + i < n; ++i) out[36 + i] = (int64_t)h[i];
+    for (int i = 0; i < 16 && 36 + i < n; ++i) out[36 + i] = (int64_t)h[i];
   }
   return CYR_OK;
 }
@@ -1233,6 +1233,24 @@ int cyr_selftest_latency(int32_t which, int32_t iters, int64_t* cycles) {
   cudaFree(d);
   cudaFree(sink);
   *cycles = (int64_t)h;
+  return rc;
+}
+
+int cyr_selftest_shared_divisor(int64_t pairs_total, uint64_t seed, int64_t* mismatches) {
+  if (!mismatches || pairs_total < 1) return CYR_BAD_ARG;
+  const int sms = sm_count_of_current_device();
+  const long long threads = (long long)sms * 8 * 256;
+  unsigned long long* bad = nullptr;
+  CYR_CUDA(cudaMalloc(&bad, sizeof(unsigned long long)));
+  int rc = cudaMemset(bad, 0, sizeof(unsigned long long)) == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
+  if (rc == CYR_OK)
+    rc = cyr_launch_shared_divisor_check((pairs_total + threads - 1) / threads, seed, sms, bad,
+                                         nullptr);
+  unsigned long long h = 0;
+  if (rc == CYR_OK && cudaMemcpy(&h, bad, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess)
+    rc = CYR_CUDA_ERROR;
+  cudaFree(bad);
+  *mismatches = (int64_t)h;
   return rc;
 }
 

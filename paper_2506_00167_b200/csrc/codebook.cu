@@ -43,7 +43,10 @@ __global__ void __launch_bounds__(256, 4) codebook_kernel(
 // Batch K3, one lane per row (projection_lane.cuh): each warp holds
 // 32 / cap whole slots; 4 warps per CTA, no CTA barrier.
 constexpr int kLaneWarps = 4;
-constexpr int kLaneMinBlocks = 5;  // <= 102 registers: 20 warps per SM (no spills; 4/6/8 measured flat)
+#ifndef CYR_LANE_MINB
+#define CYR_LANE_MINB 5
+#endif
+constexpr int kLaneMinBlocks = CYR_LANE_MINB;  // <= 102 registers: 20 warps per SM (no spills; 4/6/8 measured flat)
 
 template <typename RawT>
 __global__ void __launch_bounds__(32 * kLaneWarps) codebook_lane_kernel(
@@ -635,5 +638,62 @@ int cyr_launch_tree_level(int precision, const void* raw, const int32_t* alloc, 
     cyr::tree_level_kernel<float><<<(unsigned)blocks, 32 * cyr::kLaneWarps, smem, stream>>>(
         static_cast<const float*>(raw), io, groups, L, status);
   }
+  return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
+}
+
+// ------------------------------------------- shared-divisor division check
+// div_rn_shared (projection.cuh) against __ddiv_rn, bit for bit, on operand
+// pairs drawn from five families: random normals over a wide exponent range,
+// cap-like dividends over water-level-like divisors, random bit patterns
+// across the whole fast range, quotients planted next to representable
+// values (a = RN(q * b)), and the Huntington-Hill divisors of seats 0..1023.
+namespace cyr {
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long& s) {
+  unsigned long long z = (s += 0x9e3779b97f4a7c15ull);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double bits_in(unsigned long long r, int emin, int emax) {
+  const int e = emin + (int)((r >> 52) % (unsigned long long)(emax - emin + 1));
+  return __longlong_as_double((long long)(((unsigned long long)(e + 1023) << 52) |
+                                          (r & 0xfffffffffffffull)));
+}
+__global__ void shared_divisor_check_kernel(long long per_thread, unsigned long long seed,
+                                            unsigned long long* bad) {
+  unsigned long long st = seed ^ ((unsigned long long)(blockIdx.x * blockDim.x + threadIdx.x) << 20);
+  unsigned long long mism = 0;
+  for (long long i = 0; i < per_thread; ++i) {
+    const unsigned long long r1 = splitmix64(st), r2 = splitmix64(st);
+    double a, b;
+    switch ((int)(i % 5)) {
+      case 0: a = bits_in(r1, -60, 60); b = bits_in(r2, -60, 60); break;
+      case 1: a = (double)(r1 % 800) + (double)(r1 >> 40) * 0x1p-24;
+              b = bits_in(r2, -20, 10); break;
+      case 2: a = bits_in(r1, -500, 499); b = bits_in(r2, -500, 499); break;
+      case 3: {
+        b = bits_in(r2, -30, 30);
+        const double q = bits_in(r1, -30, 30);
+        a = __dmul_rn(q, b);
+        a = __longlong_as_double(__double_as_longlong(a) + (long long)(r1 % 5) - 2);
+        break;
+      }
+      default: {
+        const double x = (double)(r2 % kSeatTab);
+        b = __dsqrt_rn(fmax(__dmul_rn(x, __dadd_rn(x, 1.0)), 1.0));
+        a = bits_in(r1, -40, 12);
+      }
+    }
+    const double want = __ddiv_rn(a, b);
+    const double got = div_rn_shared(a, shared_divisor(b));
+    mism += __double_as_longlong(want) != __double_as_longlong(got);
+  }
+  if (mism) atomicAdd(bad, mism);
+}
+}  // namespace cyr
+
+int cyr_launch_shared_divisor_check(long long per_thread, unsigned long long seed, int sm_count,
+                                    unsigned long long* bad, cudaStream_t stream) {
+  cyr::shared_divisor_check_kernel<<<sm_count * 8, 256, 0, stream>>>(per_thread, seed, bad);
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
 }

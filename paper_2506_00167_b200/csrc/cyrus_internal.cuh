@@ -270,6 +270,8 @@ int cyr_launch_leaf_states_score(const int16_t* leaves, long long slot_stride, i
                                  const int32_t* alloc, const double* margin, const double* prob,
                                  int N, uint32_t* ok, double* expect, cudaStream_t stream);
 int cyr_launch_fma_peak(int iters, int sm_count, float* sink, cudaStream_t stream);
+int cyr_launch_shared_divisor_check(long long per_thread, unsigned long long seed, int sm_count,
+                                    unsigned long long* bad, cudaStream_t stream);
 int cyr_launch_pack_policy(const cyr::ActorDesc& desc, int precision, const double* raw_d,
                            void* blob_d, unsigned char* tc_blob_d, const long long* tc_off,
                            const int* tc_npad, cudaStream_t stream);

@@ -36,6 +36,52 @@ __device__ __forceinline__ double div_or_zero(double a, double b) {
   return a != 0.0 ? q : 0.0;
 }
 
+// Division by a divisor shared by many dividends (one fill evaluation divides
+// a row's E masses by one water level; the Huntington-Hill priorities divide
+// by per-seat constants): y = RN(1/b) once (__drcp_rn), then per dividend
+// q0 = RN(a*y), one Newton correction q1 = RN(q0 + (a - b*q0)*y), and
+// Markstein's final step q = RN(q1 + (a - b*q1)*y) -- the remainders exact by
+// FMA.  With y within half an ulp of 1/b and q1 within one ulp of a/b, that
+// step returns RN(a/b) (Markstein 1990; Muller et al., Handbook of
+// Floating-Point Arithmetic, "Markstein's theorem"), i.e. the bits of
+// __ddiv_rn.  The operands are held to [2^-500, 2^500] so no quotient,
+// product or remainder leaves the normal range; anything else (zero,
+// subnormal, huge, inf, NaN) takes __ddiv_rn.  cyr_selftest_shared_divisor
+// compares the two on 2^30+ operand pairs (tests/test_gpu_guards.py).
+struct SharedDivisor {
+  double b, y;
+  bool fast;
+};
+__device__ __forceinline__ bool markstein_range(double v) {
+  return v >= 0x1p-500 && v <= 0x1p500;
+}
+__device__ __forceinline__ SharedDivisor shared_divisor(double b) {
+  SharedDivisor s;
+  s.b = b;
+  s.fast = markstein_range(b);
+  s.y = s.fast ? __drcp_rn(b) : 0.0;
+  return s;
+}
+__device__ __forceinline__ SharedDivisor shared_divisor(double b, double y) {  // y = __drcp_rn(b)
+  SharedDivisor s;
+  s.b = b;
+  s.y = y;
+  s.fast = markstein_range(b);
+  return s;
+}
+__device__ __forceinline__ double div_rn_shared(double a, const SharedDivisor& s) {
+  if (s.fast && markstein_range(a)) {
+    double q = __dmul_rn(a, s.y);
+    q = __fma_rn(__fma_rn(-q, s.b, a), s.y, q);
+    return __fma_rn(__fma_rn(-q, s.b, a), s.y, q);
+  }
+  return __ddiv_rn(a, s.b);
+}
+// div_or_zero(a, s.b), bit for bit
+__device__ __forceinline__ double div_or_zero(double a, const SharedDivisor& s) {
+  return a != 0.0 ? div_rn_shared(a, s) : 0.0;
+}
+
 struct Row {
   double b, c, d;  // this lane's raw action and cap; the row demand
   bool valid;      // row exists (warp-uniform)

@@ -53,13 +53,16 @@ struct LaneRow {
   double d;
   bool bis, degen, full;
   double lo, hi;
+  mutable int evals;  // fill evaluations (CYR_TRACE profile only)
   __device__ __forceinline__ double b(int e) const { return bT[e * 32]; }
   __device__ __forceinline__ double c(int e) const { return cT[e * 32]; }
   __device__ __forceinline__ bool pos(int e) const { return b(e) > kMassFloor && c(e) > 0.0; }
 };
 
 __device__ __forceinline__ bool fill_reaches_lane(const LaneRow& r, double x) {
-  return np_sum_lane(r.E, [&](int e) { return fmin(r.c(e), div_or_zero(r.b(e), x)); }) >= r.d;
+  ++r.evals;
+  const SharedDivisor sx = shared_divisor(x);  // one reciprocal for the row's E divisions
+  return np_sum_lane(r.E, [&](int e) { return fmin(r.c(e), div_or_zero(r.b(e), sx)); }) >= r.d;
 }
 
 // enforcer.py:57-89 (kl_setup of projection.cuh, one lane)
@@ -146,7 +149,8 @@ __device__ __forceinline__ long long fill_threshold_lane(const LaneRow& r, doubl
 __device__ __forceinline__ double kl_finish_lane(LaneRow& r) {
   if (r.bis) {
     const double nu = __dmul_rn(__dsqrt_rn(r.lo), __dsqrt_rn(r.hi));
-    for (int e = 0; e < r.E; ++e) r.bT[e * 32] = fmin(r.c(e), div_or_zero(r.b(e), nu));
+    const SharedDivisor snu = shared_divisor(nu);
+    for (int e = 0; e < r.E; ++e) r.bT[e * 32] = fmin(r.c(e), div_or_zero(r.b(e), snu));
     return nu;
   }
   if (r.degen) {
@@ -170,18 +174,24 @@ __device__ __forceinline__ double kl_finish_lane(LaneRow& r) {
 // seat_table_kernel with the same __dsqrt_rn expression as seat_prio, so a
 // table lookup is bit-identical to computing it (one division per priority
 // instead of a division and a square root).
+// The table also holds each divisor's correctly rounded reciprocal, so a
+// priority is a Markstein quotient (SharedDivisor) instead of a division.
 constexpr int kSeatTab = 1024;
-static __device__ double g_seat_sqrt[kSeatTab];
+static __device__ double2 g_seat_div[kSeatTab];  // {sqrt(max(a(a+1), 1)), RN(1 / that)}
 
 static __global__ void seat_table_kernel() {
   for (int a = threadIdx.x; a < kSeatTab; a += blockDim.x) {
     const double x = (double)a;
-    g_seat_sqrt[a] = __dsqrt_rn(fmax(__dmul_rn(x, __dadd_rn(x, 1.0)), 1.0));
+    const double d = __dsqrt_rn(fmax(__dmul_rn(x, __dadd_rn(x, 1.0)), 1.0));
+    g_seat_div[a] = make_double2(d, __drcp_rn(d));
   }
 }
 
 __device__ __forceinline__ double seat_prio_tab(double m, int seat) {
-  if (seat < kSeatTab) return div_or_zero(m, g_seat_sqrt[seat]);
+  if (seat < kSeatTab) {
+    const double2 t = g_seat_div[seat];
+    return div_or_zero(m, shared_divisor(t.x, t.y));
+  }
   return seat_prio(m, seat);
 }
 
@@ -190,7 +200,7 @@ __device__ __forceinline__ double seat_prio_tab(double m, int seat) {
 // caches each user's seat count once per row: cnt = ceil(cap) when the user
 // has positive mass and cnt >= 1, else -cnt - 1.
 __device__ __forceinline__ double hh_lane(const double* mT, const double* cT, int E, long long want,
-                                          int* hT, int* nT) {
+                                          int* hT, int* nT, int* steps_out = nullptr) {
   auto m = [&](int e) { return mT[e * 32]; };
   for (int e = 0; e < E; ++e) {
     const int c = (int)ceil(cT[e * 32]);
@@ -277,6 +287,7 @@ __device__ __forceinline__ double hh_lane(const double* mT, const double* cT, in
         hT[ld * 32] -= 1;
       } else {
         if (oka && okd) margin = div_or_zero(__dsub_rn(pd, pa), pd);
+        if (steps_out) *steps_out = (int)step + 1;
         break;
       }
     }
@@ -355,6 +366,7 @@ __device__ void codebook_rows_lane(const RawT* raw, long long row0, int nrows, i
   r.d = (double)((long long)j * L);
   r.bis = r.degen = r.full = false;
   r.lo = r.hi = 0.0;
+  r.evals = 0;
   long long thr = 0;
   if (live) {
     // head (neural.py:144-165, sac.py:348-355) and action_to_scs (neural.py:181-183)
@@ -390,11 +402,27 @@ __device__ void codebook_rows_lane(const RawT* raw, long long row0, int nrows, i
   double nu = 0.0, margin = 0.0;
   if (live) nu = kl_finish_lane(r);
   mark(5);
-  if (live) margin = hh_lane(bT, cT, E, (long long)j * L, hT, nT);
+  int hh_steps = 0;
+  if (live) margin = hh_lane(bT, cT, E, (long long)j * L, hT, nT, prof ? &hh_steps : nullptr);
   mark(6);
   if (live) io.emit_lane(grow, group, j, hT, E, bT, nu, margin, iters);
   mark(7);
-  if (prof && lane == 0) atomicAdd(prof + 8, 1ull);
+  if (prof) {  // event counts summed over the warp's live rows
+    unsigned long long ev = live ? (unsigned long long)r.evals : 0ull;
+    unsigned long long hs = live ? (unsigned long long)hh_steps : 0ull;
+    for (int o = 16; o > 0; o >>= 1) {
+      ev += __shfl_xor_sync(0xffffffffu, ev, o);
+      hs += __shfl_xor_sync(0xffffffffu, hs, o);
+    }
+    const unsigned nlive = (unsigned)__popc(__ballot_sync(0xffffffffu, live));
+    if (lane == 0) {
+      atomicAdd(prof + 8, 1ull);
+      atomicAdd(prof + 9, ev);
+      atomicAdd(prof + 10, hs);
+      atomicAdd(prof + 11, (unsigned long long)nlive);
+      atomicAdd(prof + 12, (unsigned long long)iters);
+    }
+  }
 }
 
 }  // namespace cyr

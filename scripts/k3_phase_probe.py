@@ -25,10 +25,13 @@ tree.build_tree_mode_t(pol, cell, al, mc, ep)
 torch.cuda.synchronize()
 buf = (ctypes.c_int64 * 64)()
 _native.lib().cyr_debug_trace(buf, 64)
-vals = [buf[i] for i in range(36, 45)]
+vals = [buf[i] for i in range(36, 52)]
 warps = max(vals[8], 1)
 names = ["head", "setup", "water level", "threshold", "coupled loop", "finish", "HH", "emit"]
 tot = sum(vals[:8])
 print(f"{name}: {warps} warps, {tot / warps:.0f} cycles per warp")
 for k, nm in enumerate(names):
     print(f"  {nm:13s} {vals[k] / warps:9.0f} cycles/warp  {100 * vals[k] / max(tot, 1):5.1f} %")
+rows = max(vals[11], 1)
+print(f"  per row: {vals[9] / rows:.2f} fill evaluations, {vals[10] / rows:.2f} Huntington-Hill "
+      f"exchange steps (phase-1 rows); coupled-bisection iterations per warp {vals[12] / warps:.1f}")
