@@ -398,6 +398,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) actor_tc_kernel(const TcLaunch 
 // MMA2 2.1k + ~0.3k wake-up, epi2 1.7k, MMA3 0.6k + ~0.5k wake-up: ~8.1k
 // cycles, the tensor pipe busy ~2.9k of them.  A/B knobs (compile-time):
 // CYR_FUSED_EPI (8 / 16 epilogue warps: 16), CYR_FUSED_FADD2.
+#ifndef CYR_FUSED_SPIN
+#define CYR_FUSED_SPIN 0
+#endif
+#if CYR_FUSED_SPIN
+#define CYR_FUSED_WAIT mbar_wait_spin
+#else
+#define CYR_FUSED_WAIT mbar_wait
+#endif
 #ifndef CYR_FUSED_GROUPS
 #define CYR_FUSED_GROUPS 1
 #endif
@@ -647,7 +655,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const 
         // MMA2 once every epi1 part has written its A2 K columns (and drained
         // its D1 columns).  Starting the K steps of each part as it lands, or
         // MMA2 in two N halves, measured slower (A/B in round 2).
-        for (int q = 0; q < kFusedParts; ++q) mbar_wait(&a2p[q], ph);
+        for (int q = 0; q < kFusedParts; ++q) CYR_FUSED_WAIT(&a2p[q], ph);
         tc_fence_after();
         for (int ks = 0; ks < n1 / 16; ks += 4)
           tc_mma_ts_x4(tm, tm + (uint32_t)(kFusedA2Col + ks * 8),
@@ -661,7 +669,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const 
         const long long pt5 = clock64();
 #endif
         // MMA3 (the head) once every epi2 part has written A3 / drained D2
-        for (int q = 0; q < kFusedParts; ++q) mbar_wait(&a3p[q], ph);
+        for (int q = 0; q < kFusedParts; ++q) CYR_FUSED_WAIT(&a3p[q], ph);
         tc_fence_after();
 #ifdef CYR_FUSED_PROF
         CYR_TRACE(22, i)
@@ -844,7 +852,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const 
 #ifdef CYR_FUSED_PROF
       const long long q0 = clock64();
 #endif
-      mbar_wait(d1full, ph);
+      CYR_FUSED_WAIT(d1full, ph);
 #ifdef CYR_FUSED_PROF
       const long long q0b = clock64();
 #endif
@@ -865,7 +873,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const 
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&a2p[part]);
-      mbar_wait(d2full, ph);
+      CYR_FUSED_WAIT(d2full, ph);
       tc_fence_after();
 #ifdef CYR_FUSED_PROF
       const long long q3 = clock64();
