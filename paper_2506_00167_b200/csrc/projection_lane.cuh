@@ -48,6 +48,7 @@ __device__ __forceinline__ double np_sum_lane(int n, F term) {
 // from the allocation row (int32, shared by the call's rows), demand d.
 struct LaneRow {
   double* bT;        // this lane's column of the warp's [E][32] array
+  double* tT;        // scratch column (fill-evaluation terms; the HH seat arrays' space)
   const double* cT;  // caps (allocation row as doubles), same layout
   int E;
   double d;
@@ -59,10 +60,16 @@ struct LaneRow {
   __device__ __forceinline__ bool pos(int e) const { return b(e) > kMassFloor && c(e) > 0.0; }
 };
 
+// The terms go through the lane's scratch column so the quotient code exists
+// once (a rolled loop) instead of once per unrolled slot of the pairwise sum
+// at every call site: the lane kernel's hot loops had outgrown the
+// instruction cache (stall_no_instruction 2.4 of 9.1 cycles per issue).
 __device__ __forceinline__ bool fill_reaches_lane(const LaneRow& r, double x) {
   ++r.evals;
   const SharedDivisor sx = shared_divisor(x);  // one reciprocal for the row's E divisions
-  return np_sum_lane(r.E, [&](int e) { return fmin(r.c(e), div_or_zero(r.b(e), sx)); }) >= r.d;
+#pragma unroll 1
+  for (int e = 0; e < r.E; ++e) r.tT[e * 32] = fmin(r.c(e), div_or_zero(r.b(e), sx));
+  return np_sum_lane(r.E, [&](int e) { return r.tT[e * 32]; }) >= r.d;
 }
 
 // enforcer.py:57-89 (kl_setup of projection.cuh, one lane)
@@ -115,32 +122,37 @@ __device__ __forceinline__ double water_level_lane(const LaneRow& r) {
   return nu;
 }
 
-// Exact fill threshold (fill_threshold of projection.cuh, one lane).
+// Exact fill threshold (fill_threshold of projection.cuh, one lane): gallop
+// from the water level, then halve.  One evaluation site (a state machine)
+// keeps the loop's code small.
 __device__ __forceinline__ long long fill_threshold_lane(const LaneRow& r, double x0) {
   constexpr long long kInf = 0x7ff0000000000000ll;
-  long long lo, hi;
   const long long a = __double_as_longlong(x0);
-  if (fill_reaches_lane(r, x0)) {
-    lo = a;
-    for (long long step = 1;; step <<= 1) {
-      const long long cand = lo + step;
-      if (cand >= kInf) { hi = kInf; break; }
-      if (!fill_reaches_lane(r, __longlong_as_double(cand))) { hi = cand; break; }
-      lo = cand;
+  long long lo = 0, hi = 0, step = 1, cand = a;
+  int ph = 0;  // 0 first probe, 1 gallop up, 2 gallop down, 3 halve
+#pragma unroll 1
+  for (;;) {
+    const bool ok = fill_reaches_lane(r, __longlong_as_double(cand));
+    if (ph == 0) {
+      if (ok) { lo = a; ph = 1; } else { hi = a; ph = 2; }
+    } else if (ph == 1) {
+      if (ok) { lo = cand; step <<= 1; } else { hi = cand; ph = 3; }
+    } else if (ph == 2) {
+      if (ok) { lo = cand; ph = 3; } else { hi = cand; step <<= 1; }
+    } else {
+      if (ok) lo = cand; else hi = cand;
     }
-  } else {
-    hi = a;
-    for (long long step = 1;; step <<= 1) {
-      const long long cand = hi - step;
-      if (cand <= 0) { lo = 0; break; }
-      if (fill_reaches_lane(r, __longlong_as_double(cand))) { lo = cand; break; }
-      hi = cand;
+    if (ph == 1) {
+      cand = lo + step;
+      if (cand >= kInf) { hi = kInf; ph = 3; }
+    } else if (ph == 2) {
+      cand = hi - step;
+      if (cand <= 0) { lo = 0; ph = 3; }
     }
-  }
-  while (hi - lo > 1) {
-    const long long mid = lo + ((hi - lo) >> 1);
-    if (fill_reaches_lane(r, __longlong_as_double(mid))) lo = mid;
-    else hi = mid;
+    if (ph == 3) {
+      if (hi - lo <= 1) break;
+      cand = lo + ((hi - lo) >> 1);
+    }
   }
   return lo;
 }
@@ -358,6 +370,7 @@ __device__ void codebook_rows_lane(const RawT* raw, long long row0, int nrows, i
   LaneRow r;
   r.bT = bT;
   r.cT = cT;
+  r.tT = reinterpret_cast<double*>(scratch + 2 * plane * sizeof(double)) + lane;  // = hT/nT space
   if (live) {
     const int32_t* n = io.alloc_row(group);
     for (int e = 0; e < E; ++e) cT[e * 32] = (double)__ldg(n + e);
@@ -415,12 +428,19 @@ __device__ void codebook_rows_lane(const RawT* raw, long long row0, int nrows, i
       hs += __shfl_xor_sync(0xffffffffu, hs, o);
     }
     const unsigned nlive = (unsigned)__popc(__ballot_sync(0xffffffffu, live));
+    int emax = live ? r.evals : 0, hmax = live ? hh_steps : 0;
+    for (int o = 16; o > 0; o >>= 1) {
+      emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+      hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+    }
     if (lane == 0) {
       atomicAdd(prof + 8, 1ull);
       atomicAdd(prof + 9, ev);
       atomicAdd(prof + 10, hs);
       atomicAdd(prof + 11, (unsigned long long)nlive);
       atomicAdd(prof + 12, (unsigned long long)iters);
+      atomicAdd(prof + 13, (unsigned long long)emax);  // warp's slowest lane: what the warp runs
+      atomicAdd(prof + 14, (unsigned long long)hmax);
     }
   }
 }

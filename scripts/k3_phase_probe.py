@@ -35,3 +35,5 @@ for k, nm in enumerate(names):
 rows = max(vals[11], 1)
 print(f"  per row: {vals[9] / rows:.2f} fill evaluations, {vals[10] / rows:.2f} Huntington-Hill "
       f"exchange steps (phase-1 rows); coupled-bisection iterations per warp {vals[12] / warps:.1f}")
+print(f"  per warp (its slowest lane): {vals[13] / warps:.2f} fill evaluations, "
+      f"{vals[14] / warps:.2f} exchange steps")
