@@ -44,9 +44,9 @@ __global__ void __launch_bounds__(256, 4) codebook_kernel(
 // 32 / cap whole slots; 4 warps per CTA, no CTA barrier.
 constexpr int kLaneWarps = 4;
 #ifndef CYR_LANE_MINB
-#define CYR_LANE_MINB 5
+#define CYR_LANE_MINB 7
 #endif
-constexpr int kLaneMinBlocks = CYR_LANE_MINB;  // <= 102 registers: 20 warps per SM (no spills; 4/6/8 measured flat)
+constexpr int kLaneMinBlocks = CYR_LANE_MINB;  // <= 72 registers: 28 warps per SM at E = 10 (5 / 6 / 7 / 8: 1,004 / 983 / 972 / 988 us, deepest cfg2 level)
 
 template <typename RawT>
 __global__ void __launch_bounds__(32 * kLaneWarps) codebook_lane_kernel(
