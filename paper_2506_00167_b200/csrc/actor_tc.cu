@@ -153,16 +153,114 @@ __device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 //            (tau-1)/M]
 // The column's indices are decoded once and the per-user loads are issued in
 // independent batches of four, so their latencies overlap.
-__device__ __forceinline__ void tc_put(unsigned char* a, int row, int t, int i, float x) {
-  if (i >= t * 64 && i < t * 64 + 64)
-    *reinterpret_cast<__nv_bfloat16*>(a + sw128_offset(row, i - t * 64)) = __float2bfloat16_rn(x);
+// Shared-memory stores by address, without a "memory" clobber: through the
+// generic tile pointer every bf16 store was ordered before the next user's
+// global loads (possible alias), so each batch of loads paid its full
+// latency after the previous batch's stores (~4k cycles per 128-column tile
+// in the fused MLP, whose builders are on its critical path).
+__device__ __forceinline__ void tc_put(uint32_t a, int row, int t, int i, float x) {
+  if (i >= t * 64 && i < t * 64 + 64) {
+    const __nv_bfloat16 h = __float2bfloat16_rn(x);
+    asm volatile("st.shared.b16 [%0], %1;" ::"r"(a + sw128_offset(row, i - t * 64)),
+                 "h"(*reinterpret_cast<const unsigned short*>(&h)));
+  }
+}
+
+// x / d for 0 <= x < 2^22 from a float reciprocal and one correction step
+// (the quotient is off by at most one there); larger x: integer division.
+__device__ __forceinline__ int div_small(int x, int d, float inv) {
+  if (x >= (1 << 22)) return x / d;
+  const int q = (int)((float)x * inv);
+  const int r = x - q * d;
+  return r < 0 ? q - 1 : (r >= d ? q + 1 : q);
+}
+
+// The feature row of one column for a compile-time user count (cfg1 / cfg2 /
+// cfg5: E = 4 / 10 / 16; K tile 0, in <= 64): every load issued up front,
+// the 64 bf16 values packed in registers (cvt.rn.bf16x2.f32, the same RN
+// rounding as the per-element path) and written as 8 16-byte chunks.  The
+// per-element path cost ~6.5k cycles per 128-column Mode-T tile (runtime
+// integer divisions, 33 scalar stores with their swizzle arithmetic), more
+// than the fused MLP's whole block chain.
+template <int kE>
+__device__ __forceinline__ void tc_feature_row(const TcLaunch& p, int col, uint32_t a, int row) {
+  uint32_t w[32];
+  if (col >= p.ncols) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) w[j] = 0u;
+  } else {
+    const int cap = p.cap;
+    const int g = div_small(col, cap, 1.0f / (float)cap);
+    const int k = col - g * cap + 1;
+    const int s = p.mode_t ? div_small(g, p.parents, 1.0f / (float)p.parents) : g;
+    const int q = p.mode_t ? g - s * p.parents : 0;
+    const int32_t* al = p.alloc + (long long)s * kE;
+    int av[kE], mv[kE], nv[kE];
+#pragma unroll
+    for (int e = 0; e < kE; ++e) av[e] = __ldg(al + e);
+    float arr = 0.f, tauf = 0.f;
+    if (p.mode_t) {
+      const int32_t* mc = p.mcs + (long long)s * kE;
+      const int16_t* nd =
+          p.parent_off >= 0
+              ? p.node + ((long long)s * p.nodes_per_slot + p.parent_off + q) * p.epad
+              : nullptr;
+#pragma unroll
+      for (int e = 0; e < kE; ++e) {
+        mv[e] = __ldg(mc + e);
+        nv[e] = nd ? __ldg(nd + e) : 0;
+      }
+      int arrivals = 0, x = p.parent_base + q;
+      const int base = cap + 1;
+      const float inv_base = 1.0f / (float)base;
+      for (int d = 1; d < p.tau; ++d) {
+        const int xq = div_small(x, base, inv_base);
+        arrivals += x - xq * base;
+        x = xq;
+      }
+      arr = (float)arrivals / (float)(p.M * p.cap);
+      tauf = (float)(p.tau - 1) / (float)p.M;
+    } else {
+#pragma unroll
+      for (int e = 0; e < kE; ++e) mv[e] = nv[e] = 0;
+    }
+    const float inv_n = 1.0f / (float)p.N, inv_mcs = (float)(1.0 / p.mcs_scale);
+    const float kf = (float)k / (float)p.cap;
+    auto feat = [&](int i) -> float {  // i is a compile-time constant after unrolling
+      if (i < kE) return (float)av[i] * inv_n;
+      if (i == kE) return kf;
+      if (!p.mode_t) return 0.f;
+      if (i < 2 * kE + 1) return (float)nv[i - kE - 1] * inv_n;
+      if (i < 3 * kE + 1) return (float)mv[i - 2 * kE - 1] * inv_mcs;
+      if (i == 3 * kE + 1) return arr;
+      if (i == 3 * kE + 2) return tauf;
+      return 0.f;
+    };
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w[j]) : "f"(feat(2 * j + 1)), "f"(feat(2 * j)));
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a + sw128_offset(row, c * 8)),
+                 "r"(w[4 * c]), "r"(w[4 * c + 1]), "r"(w[4 * c + 2]), "r"(w[4 * c + 3]));
 }
 
 __device__ __forceinline__ void tc_feature_tile(const TcLaunch& p, int col, int t,
-                                                unsigned char* a, int row) {
+                                                unsigned char* tile, int row) {
+  const uint32_t a = smem_u32(tile);
+  if (t == 0 && p.desc.layer[0].in <= 64) {
+    switch (p.E) {
+      case 4: tc_feature_row<4>(p, col, a, row); return;
+      case 10: tc_feature_row<10>(p, col, a, row); return;
+      case 16: tc_feature_row<16>(p, col, a, row); return;
+      default: break;
+    }
+  }
 #pragma unroll
   for (int c = 0; c < 8; ++c)
-    *reinterpret_cast<uint4*>(a + sw128_offset(row, c * 8)) = make_uint4(0, 0, 0, 0);
+    asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(a + sw128_offset(row, c * 8)),
+                 "r"(0u));
   if (col >= p.ncols) return;
   const int E = p.E;
   const int k = col % p.cap + 1;
@@ -176,25 +274,21 @@ __device__ __forceinline__ void tc_feature_tile(const TcLaunch& p, int col, int 
           ? p.node + ((long long)s * p.nodes_per_slot + p.parent_off + q) * p.epad
           : nullptr;
   const float inv_n = 1.0f / (float)p.N, inv_mcs = (float)(1.0 / p.mcs_scale);
-  for (int e0 = 0; e0 < E; e0 += 4) {
-    int av[4], mv[4], nv[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int e = e0 + j < E ? e0 + j : E - 1;
-      av[j] = al[e];
-      mv[j] = mc ? mc[e] : 0;
-      nv[j] = nd ? nd[e] : 0;
+  // every global load first (one latency for the column, not one per batch
+  // of users), the values parked in local memory (L1), then the stores
+  int v[3 * kMaxUsers];
+  for (int e = 0; e < E; ++e) {
+    v[e] = __ldg(al + e);
+    if (p.mode_t) {
+      v[kMaxUsers + e] = nd ? __ldg(nd + e) : 0;
+      v[2 * kMaxUsers + e] = __ldg(mc + e);
     }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int e = e0 + j;
-      if (e < E) {
-        tc_put(a, row, t, e, (float)av[j] * inv_n);
-        if (p.mode_t) {
-          tc_put(a, row, t, E + 1 + e, (float)nv[j] * inv_n);
-          tc_put(a, row, t, 2 * E + 1 + e, (float)mv[j] * inv_mcs);
-        }
-      }
+  }
+  for (int e = 0; e < E; ++e) {
+    tc_put(a, row, t, e, (float)v[e] * inv_n);
+    if (p.mode_t) {
+      tc_put(a, row, t, E + 1 + e, (float)v[kMaxUsers + e] * inv_n);
+      tc_put(a, row, t, 2 * E + 1 + e, (float)v[2 * kMaxUsers + e] * inv_mcs);
     }
   }
   tc_put(a, row, t, E, (float)k / (float)p.cap);
@@ -415,6 +509,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) actor_tc_kernel(const TcLaunch 
 constexpr int kFusedGroups = CYR_FUSED_GROUPS;     // feature-builder groups of 4 warps
 constexpr int kFusedEpi = CYR_FUSED_EPI;           // epilogue warps (8 or 16)
 constexpr int kFusedParts = kFusedEpi / 4;         // column parts per TMEM lane quarter
+static_assert(kFusedEpi == 16, "epilogue chunks are n/8 columns: 4 parts per lane quarter");
 constexpr int kFusedMmaWarp = kFusedEpi + 4 * kFusedGroups;
 constexpr int kFusedThreads = 32 * (kFusedMmaWarp + 1);
 constexpr int kFusedA2Col = 256, kFusedA3Col = 384, kFusedD3Col = 256;
@@ -442,6 +537,13 @@ __device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&r)[16])
 #ifdef CYR_FUSED_PROF
 __device__ int g_fused_trace_launch = 0;
 #endif
+__device__ __forceinline__ void tc_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+      : "memory");
+}
+
 struct FusedLayout {  // shared-memory carve-up (bytes from the 1024-aligned base)
   uint32_t w_off[3], w_bytes[3], feat, bias, bars, stage, stage_bytes, total;
 };
@@ -478,44 +580,40 @@ __host__ __device__ inline FusedLayout fused_layout(const ActorDesc& d, const in
   return f;
 }
 
-// hidden-layer epilogue: D (fp32, TMEM cols [d_col, d_col + n)) -> bias, ReLU
-// -> bf16 pairs into A (TMEM cols [a_col, a_col + n / 2)); this warp's lane
-// quarter, column part `part` (of kFusedParts) of n
-__device__ __forceinline__ void fused_hidden_epi(uint32_t tmem, int quarter, int part, int n,
-                                                 int d_col, int a_col, const float* bias) {
+// One column chunk of a hidden-layer epilogue: this warp's TMEM lane
+// quarter, D columns [c0, c0 + W) (fp32) -> bias, ReLU -> bf16 pairs into A
+// columns [a_col + c0 / 2, + W / 2).  Per column pair one packed fp32 add of
+// the bias pair (add.rn.f32x2, bit-identical to two FADDs) and one convert
+// with the ReLU folded in (cvt.rn.relu.bf16x2.f32: max(x, 0) then round, low
+// half = even K).  Waits for its TMEM stores.
+template <int W>
+__device__ __forceinline__ void fused_epi_chunk(uint32_t tmem, int quarter, int c0, int a_col,
+                                                const float* bias) {
   const uint32_t lanes = (uint32_t)(quarter * 32) << 16;
-  const int c0 = part * (n / kFusedParts), c1 = c0 + n / kFusedParts;
-  for (int n0 = c0; n0 < c1; n0 += 32) {
-    uint32_t r[32];
-    tc_ld32(tmem + lanes + (uint32_t)(d_col + n0), r);
-    // per column pair: one packed fp32 add of the bias pair (add.rn.f32x2,
-    // bit-identical to two FADDs) and one convert with the ReLU folded in
-    // (cvt.rn.relu.bf16x2.f32: max(x, 0) then round, low half = even K)
-    const unsigned long long* b2 = reinterpret_cast<const unsigned long long*>(bias + n0);
-    uint32_t w[16];
-#ifndef CYR_FUSED_FADD2
-#define CYR_FUSED_FADD2 1
-#endif
+  uint32_t r[W];
+  if constexpr (W == 32) tc_ld32(tmem + lanes + (uint32_t)c0, r);
+  else tc_ld16(tmem + lanes + (uint32_t)c0, r);
+  // bias pairs by ld.shared.v2.b64 (explicit shared state space: through the
+  // generic pointer these loads were 19 % of the kernel's instructions' cost)
+  const uint32_t bs = smem_u32(bias + c0);
+  uint32_t w[W / 2];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      if (!CYR_FUSED_FADD2) {
-        float v0 = __uint_as_float(r[2 * j]) + bias[n0 + 2 * j];
-        float v1 = __uint_as_float(r[2 * j + 1]) + bias[n0 + 2 * j + 1];
-        v0 = v0 > 0.f ? v0 : 0.f;
-        v1 = v1 > 0.f ? v1 : 0.f;
-        const __nv_bfloat162 pr = __floats2bfloat162_rn(v0, v1);
-        w[j] = *reinterpret_cast<const uint32_t*>(&pr);
-        continue;
-      }
-      unsigned long long v;
-      asm("add.rn.f32x2 %0, %1, %2;" : "=l"(v) : "l"(f32x2_pack(__uint_as_float(r[2 * j]),
-                                                               __uint_as_float(r[2 * j + 1]))),
-          "l"(b2[j]));
-      const float2 f = f32x2_unpack(v);
-      asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(w[j]) : "f"(f.y), "f"(f.x));
-    }
-    tc_st16(tmem + lanes + (uint32_t)(a_col + n0 / 2), w);
+  for (int j = 0; j < W / 2; j += 2) {
+    unsigned long long b01, b23;
+    asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(b01), "=l"(b23) : "r"(bs + 8u * j));
+    unsigned long long v0, v1;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(v0) : "l"(f32x2_pack(__uint_as_float(r[2 * j]),
+                                                              __uint_as_float(r[2 * j + 1]))),
+        "l"(b01));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(v1) : "l"(f32x2_pack(__uint_as_float(r[2 * j + 2]),
+                                                              __uint_as_float(r[2 * j + 3]))),
+        "l"(b23));
+    const float2 f0 = f32x2_unpack(v0), f1 = f32x2_unpack(v1);
+    asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(w[j]) : "f"(f0.y), "f"(f0.x));
+    asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(w[j + 1]) : "f"(f1.y), "f"(f1.x));
   }
+  if constexpr (W == 32) tc_st16(tmem + lanes + (uint32_t)(a_col + c0 / 2), w);
+  else tc_st8(tmem + lanes + (uint32_t)(a_col + c0 / 2), w);
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
@@ -530,13 +628,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const 
   uint64_t* wbar = bars;          // weights resident
   uint64_t* ffull = bars + 1;     // [NB <= 4] feature tile ready (4 builder warps)
   uint64_t* ffree = bars + 5;     // [NB] feature tile consumed (MMA1 commit)
-  uint64_t* d1full = bars + 9;    // MMA1 complete
-  uint64_t* a2p = bars + 10;      // [kFusedParts] epi1 part p complete (its 4 warps): the
-                                  // A2 K columns of part p are in TMEM, its D1 columns drained
-  uint64_t* d2full = bars + 14;   // MMA2 complete
-  uint64_t* a3p = bars + 16;      // [kFusedParts] epi2 part p complete
-  uint64_t* d3full = bars + 20;   // MMA3 complete
-  uint64_t* d3free = bars + 21;   // head (builder warps) has read D3 out of TMEM
+  // The block's chain runs in N halves (h = 0: D columns [0, n/2), 1: the
+  // rest) so each epilogue's first half overlaps the MMAs of the second:
+  uint64_t* d1h = bars + 9;       // [2] MMA1 N half h complete
+  uint64_t* a2h = bars + 11;      // [2] epi1 chunk h done by every epilogue warp: A2 K
+                                  //     columns of half h written, D1 half h drained
+  uint64_t* d2h = bars + 13;      // [2] MMA2 N half h complete
+  uint64_t* a3h = bars + 15;      // [2] epi2 chunk h done (A3 K half h, D2 half h drained)
+  uint64_t* d3full = bars + 17;   // MMA3 complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n1 = p.tc_npad[0], n2 = p.tc_npad[1], n3 = p.tc_npad[2];
@@ -554,14 +653,13 @@ __global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const 
       mbar_init(&ffull[i], 4);
       mbar_init(&ffree[i], 1);
     }
-    mbar_init(d1full, 1);
-    for (int q = 0; q < kFusedParts; ++q) {
-      mbar_init(&a2p[q], 4);
-      mbar_init(&a3p[q], 4);
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&d1h[h], 1);
+      mbar_init(&d2h[h], 1);
+      mbar_init(&a2h[h], kFusedEpi);
+      mbar_init(&a3h[h], kFusedEpi);
     }
-    mbar_init(d2full, 1);
     mbar_init(d3full, 1);
-    mbar_init(d3free, 4);
     fence_mbar_init();
   }
   {  // biases (fp32) -> shared, zero past each layer's width
@@ -611,162 +709,169 @@ __global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const 
       constexpr uint32_t tm = 0u;
       mbar_wait(wbar, 0);
       tc_fence_after();
-      const uint32_t id1 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n1 >> 3) << 17) |
-                           ((uint32_t)(kTcM >> 4) << 24);
-      const uint32_t id2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n2 >> 3) << 17) |
-                           ((uint32_t)(kTcM >> 4) << 24);
-      const uint32_t id3 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n3 >> 3) << 17) |
-                           ((uint32_t)(kTcM >> 4) << 24);
+      auto idesc = [](int n) {
+        return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) |
+               ((uint32_t)(kTcM >> 4) << 24);
+      };
+      const uint32_t id1 = idesc(n1 / 2), id2 = idesc(n2 / 2), id3 = idesc(n3);
       const uint32_t w1 = smem_u32(base + f.w_off[0]), w2 = smem_u32(base + f.w_off[1]),
                      w3 = smem_u32(base + f.w_off[2]);
-      const uint32_t t2 = (uint32_t)n2 * 128u, t3 = (uint32_t)n3 * 128u;  // bytes per k tile
+      const uint32_t t2 = (uint32_t)n2 * 128u, t3 = (uint32_t)n3 * 128u;  // bytes per K tile
+      // rows [n/2, n) of a SW128 weight image start (n/2/8) 1-KB row groups in
+      const uint32_t w1b = w1 + (uint32_t)(n1 / 16) * 1024u, w2b = (uint32_t)(n2 / 16) * 1024u;
+      const int k2 = n1 / 16, k3 = n2 / 16;  // K steps of MMA2 / MMA3
       int i = 0;
 #ifdef CYR_FUSED_PROF
-      long long pacc[6] = {0, 0, 0, 0, 0, 0};
       const long long pstart = clock64();
 #endif
       for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
         const int fb = i % NB;
         const uint32_t ph = (uint32_t)(i & 1);
-#ifdef CYR_FUSED_PROF
-        const long long pt0 = clock64();
-#endif
         mbar_wait(&ffull[fb], (uint32_t)((i / NB) & 1));
         tc_fence_after();
 #ifdef CYR_FUSED_PROF
-        const long long pt1 = clock64();
         CYR_TRACE(0, i)
+        CYR_TRACE(12, i - 1)
 #endif
+        // MMA1 (K = 64, one tile) in N halves
         const uint32_t a1 = smem_u32(feat + fb * kTcM * 128);
         tc_mma_ss_x4(tm, umma_desc_sw128(a1), umma_desc_sw128(w1), id1, 0);
+        tc_commit_w(&d1h[0]);
+        tc_mma_ss_x4(tm + (uint32_t)(n1 / 2), umma_desc_sw128(a1), umma_desc_sw128(w1b), id1, 0);
         tc_commit_w(&ffree[fb]);
-        tc_commit_w(d1full);
-#ifdef CYR_FUSED_PROF
-        const long long pt2 = clock64();
-        CYR_TRACE(1, i)
-#ifdef CYR_FUSED_PROF_SERIAL  // exec time of MMA1 alone (serialises the issue)
-        mbar_wait(d1full, ph);
-        pacc[1] += clock64() - pt2;
-#endif
-#endif
-#ifdef CYR_FUSED_PROF
-        const long long pt3 = clock64();
-#endif
-        // MMA2 once every epi1 part has written its A2 K columns (and drained
-        // its D1 columns).  Starting the K steps of each part as it lands, or
-        // MMA2 in two N halves, measured slower (A/B in round 2).
-        for (int q = 0; q < kFusedParts; ++q) CYR_FUSED_WAIT(&a2p[q], ph);
+        tc_commit_w(&d1h[1]);
+        // MMA2 half 0 over K half 0 (A2 from epi1 chunk 0; it drained D1 half
+        // 0, which D2 half 0 overwrites), then over K half 1 once epi1 chunk 1
+        // is in, then half 1 over all of K: epi2 chunk 0 overlaps the last.
+        CYR_FUSED_WAIT(&a2h[0], ph);
         tc_fence_after();
-        for (int ks = 0; ks < n1 / 16; ks += 4)
+        for (int ks = 0; ks < k2 / 2; ks += 4)
           tc_mma_ts_x4(tm, tm + (uint32_t)(kFusedA2Col + ks * 8),
                        umma_desc_sw128(w2 + (uint32_t)(ks >> 2) * t2), id2, ks > 0 ? 1 : 0);
-        tc_commit_w(d2full);
+        CYR_FUSED_WAIT(&a2h[1], ph);
+        tc_fence_after();
 #ifdef CYR_FUSED_PROF
-        const long long pt4 = clock64();
+        CYR_TRACE(1, i)
+#endif
+        for (int ks = k2 / 2; ks < k2; ks += 4)
+          tc_mma_ts_x4(tm, tm + (uint32_t)(kFusedA2Col + ks * 8),
+                       umma_desc_sw128(w2 + (uint32_t)(ks >> 2) * t2), id2, 1);
+        tc_commit_w(&d2h[0]);
+        for (int ks = 0; ks < k2; ks += 4)
+          tc_mma_ts_x4(tm + (uint32_t)(n2 / 2), tm + (uint32_t)(kFusedA2Col + ks * 8),
+                       umma_desc_sw128(w2 + w2b + (uint32_t)(ks >> 2) * t2), id2, ks > 0 ? 1 : 0);
+        tc_commit_w(&d2h[1]);
+#ifdef CYR_FUSED_PROF
         CYR_TRACE(2, i)
 #endif
-#ifdef CYR_FUSED_PROF
-        const long long pt5 = clock64();
-#endif
-        // MMA3 (the head) once every epi2 part has written A3 / drained D2
-        for (int q = 0; q < kFusedParts; ++q) CYR_FUSED_WAIT(&a3p[q], ph);
+        // MMA3 (the head) over K half 0 as soon as epi2 chunk 0 is in, then half 1
+        CYR_FUSED_WAIT(&a3h[0], ph);
         tc_fence_after();
 #ifdef CYR_FUSED_PROF
         CYR_TRACE(22, i)
 #endif
-        for (int ks = 0; ks < n2 / 16; ks += 4) {
+        for (int ks = 0; ks < k3 / 2; ks += 4)
           tc_mma_ts_x4(tm + kFusedD3Col, tm + (uint32_t)(kFusedA3Col + ks * 8),
                        umma_desc_sw128(w3 + (uint32_t)(ks >> 2) * t3), id3, ks > 0 ? 1 : 0);
-#ifdef CYR_FUSED_PROF
-          if (ks / 4 < 4) { CYR_TRACE(56 + ks / 4, i) }
-#endif
-        }
+        CYR_FUSED_WAIT(&a3h[1], ph);
+        tc_fence_after();
+        for (int ks = k3 / 2; ks < k3; ks += 4)
+          tc_mma_ts_x4(tm + kFusedD3Col, tm + (uint32_t)(kFusedA3Col + ks * 8),
+                       umma_desc_sw128(w3 + (uint32_t)(ks >> 2) * t3), id3, 1);
 #ifdef CYR_FUSED_PROF
         CYR_TRACE(23, i)
 #endif
         tc_commit_w(d3full);
 #ifdef CYR_FUSED_PROF
-#ifdef CYR_FUSED_PROF_SERIAL  // exec time of MMA3 alone
-        {
-          const long long t = clock64();
-          mbar_wait(d3full, ph);
-          pacc[2] += clock64() - t;
-        }
-#endif
-        const long long pt6 = clock64();
         CYR_TRACE(3, i)
-        pacc[0] += pt1 - pt0; pacc[1] += pt2 - pt1;
-        pacc[3] += pt4 - pt3; pacc[4] += pt5 - pt4; pacc[5] += pt6 - pt5;
 #endif
       }
 #ifdef CYR_FUSED_PROF
       if ((blockIdx.x == 0 || blockIdx.x == 77) && lane == 0)
-        printf("MMA cta %d blocks %d per block: wait feat %lld, mma1 %lld, wait a2 %lld, mma2 %lld, "
-               "wait a3 %lld, mma3 %lld, total %lld (SERIAL: wait a2 = MMA3 exec, mma1 = issue + exec)\n", blockIdx.x, i, pacc[0] / i, pacc[1] / i,
-               pacc[2] / i, pacc[3] / i, pacc[4] / i, pacc[5] / i, (clock64() - pstart) / i);
+        printf("MMA cta %d blocks %d: %lld cycles per block\n", blockIdx.x, i,
+               (clock64() - pstart) / max(i, 1));
 #endif
     }
     __syncwarp();
   } else if (warp >= kFusedEpi) {
-    // ------------------------------------------- feature builders + head
-    // Block i's feature tile, then the head output of block i - 1: its D3
-    // is read out of TMEM (then `d3free` lets the epilogues overwrite those
-    // columns with A2 of block i + 1), staged row-major in shared memory and
-    // written by one bulk copy.  Off the epilogue warps, the head no longer
-    // delays epi1 of the next block (the MMA2 input): 10.1k -> see DESIGN.
-    static_assert(kFusedGroups == 1, "the head runs on the single builder group");
-    const int quarter = warp & 3, row = (tid - 32 * kFusedEpi) & 127;
-    const bool leader = warp == kFusedEpi && lane == 0;
+    // ---------------------------------------------------- feature builders
+    const int grp = (warp - kFusedEpi) >> 2, row = (tid - 32 * kFusedEpi) & 127;
+    int i = 0;
+    for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
+      const int fb = i % NB;
+      if (kFusedGroups > 1 && fb != grp) continue;
+      if (i >= NB) mbar_wait(&ffree[fb], (uint32_t)(((i / NB) - 1) & 1));
+#ifdef CYR_FUSED_PROF
+      if (warp == kFusedEpi) { CYR_TRACE(60, i - 1) }
+#endif
+      tc_feature_tile(p, b * kTcM + row, 0, feat + fb * kTcM * 128, row);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ffull[fb]);
+#ifdef CYR_FUSED_PROF
+      if (warp == kFusedEpi) { CYR_TRACE(61, i - 1) }
+#endif
+    }
+  } else {
+    // ------------------------------------------------------------ epilogues
+    // Every warp does its column chunk of N half 0, arrives, then half 1:
+    // half 0 of each layer is complete (and its MMAs can start) while half 1
+    // is still being converted.  Warp = (lane quarter, part): chunk columns
+    // [h * n/2 + part * n/8, + n/8) of its 32 TMEM lanes.
+    const int quarter = warp & 3, part = warp >> 2;
+    const int cw1 = n1 / (2 * kFusedParts), cw2 = n2 / (2 * kFusedParts);  // 32 or 16
+    auto chunk = [&](int cw, int c0, int a_col, const float* bias) {
+      if (cw == 32) fused_epi_chunk<32>(tmem, quarter, c0, a_col, bias);
+      else fused_epi_chunk<16>(tmem, quarter, c0, a_col, bias);
+      tc_fence_before();
+      __syncwarp();
+    };
     const int out3 = p.desc.layer[2].out;
-#ifdef CYR_FUSED_PROF
-    long long bacc[3] = {0, 0, 0};
-#endif
-    auto head = [&](int hb, int hi) {
-#ifdef CYR_FUSED_PROF
-      const long long h0 = clock64();
-#endif
-      mbar_wait(d3full, (uint32_t)(hi & 1));
-      tc_fence_after();
-#ifdef CYR_FUSED_PROF
-      const long long h1 = clock64();
-      if (warp == kFusedEpi) { CYR_TRACE(20, hi) }
-#endif
-      const uint32_t lanes = (uint32_t)(quarter * 32) << 16;
+    const int row = quarter * 32 + lane;  // TMEM lane = column within the block
+    const bool leader = warp == 0 && lane == 0;
+    // Head output.  Right after MMA3 each warp reads 8 of D3's columns for
+    // its 32 TMEM lanes (part p: logits [8p, 8p + 8)) into registers, then a
+    // barrier: the next block's epi1 may overwrite those columns with A2.  The
+    // logits are staged row-major in shared memory (the block's 128 x out3
+    // fp32 = its contiguous slice of `raw`) and written by one bulk copy
+    // while the next block's MMA2 runs.
+    const int hc0 = part * 8;
+    float hbias[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) hbias[j] = hc0 + j < n3 ? bias3[hc0 + j] : 0.f;
+    float hv[8];
+    auto head_read = [&]() {
+      uint32_t r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (hc0 < n3) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+              "=r"(r[6]), "=r"(r[7])
+            : "r"(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(kFusedD3Col + hc0)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) hv[j] = __uint_as_float(r[j]) + hbias[j];
+      tc_fence_before();
+      asm volatile("bar.sync 2, %0;" ::"n"(32 * kFusedEpi) : "memory");  // every D3 read done
+    };
+    auto head_write = [&](int hb, int hi) {
       if (f.stage_bytes) {
-        // explicit st.shared: through a generic pointer every store was
-        // ordered against the next bias load (possible alias)
-        const uint32_t st = smem_u32(base + f.stage) + (uint32_t)(row * out3) * 4u;
-        auto stage16 = [&](const uint32_t (&r)[16], int n0) {
-          float v[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]) + bias3[n0 + j];
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (n0 + j < out3)
-              asm volatile("st.shared.f32 [%0], %1;" ::"r"(st + (uint32_t)(n0 + j) * 4u), "f"(v[j])
-                           : "memory");
-        };
-        if (n3 <= 32) {  // both chunks in registers: D3 is released before the stores
-          uint32_t r0[16], r1[16];
-          tc_ld16(tmem + lanes + (uint32_t)kFusedD3Col, r0);
-          if (n3 > 16) tc_ld16(tmem + lanes + (uint32_t)(kFusedD3Col + 16), r1);
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(d3free);
-          stage16(r0, 0);
-          if (n3 > 16) stage16(r1, 16);
+        if (leader && hi > 0) bulk_wait_read<0>();  // the previous block's store has read the stage
+        asm volatile("bar.sync 2, %0;" ::"n"(32 * kFusedEpi) : "memory");
+        const uint32_t st = smem_u32(base + f.stage) + (uint32_t)(row * out3 + hc0) * 4u;
+        if ((out3 & 3) == 0 && hc0 + 8 <= out3) {
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(st), "f"(hv[0]),
+                       "f"(hv[1]), "f"(hv[2]), "f"(hv[3]));
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(st + 16u), "f"(hv[4]),
+                       "f"(hv[5]), "f"(hv[6]), "f"(hv[7]));
         } else {
-          for (int n0 = 0; n0 < n3; n0 += 16) {
-            uint32_t r[16];
-            tc_ld16(tmem + lanes + (uint32_t)(kFusedD3Col + n0), r);
-            stage16(r, n0);
-          }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(d3free);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (hc0 + j < out3) asm volatile("st.shared.f32 [%0], %1;" ::"r"(st + 4u * j), "f"(hv[j]));
         }
         fence_proxy_async_smem();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 2, %0;" ::"n"(32 * kFusedEpi) : "memory");
         const int valid = min(kTcM, p.ncols - hb * kTcM);
         const uint32_t bytes = (uint32_t)valid * (uint32_t)out3 * 4u;
         float* dst = p.raw + (long long)hb * kTcM * out3;
@@ -777,149 +882,73 @@ __global__ void __launch_bounds__(kFusedThreads, 1) actor_tc_fused_kernel(const 
           }
         } else {  // ragged last block / unaligned output: coalesced word copy
           const float* s0 = reinterpret_cast<const float*>(base + f.stage);
-          for (int e = row; e < valid * out3; e += kTcM) dst[e] = s0[e];
+          for (int e = tid; e < valid * out3; e += 32 * kFusedEpi) dst[e] = s0[e];
+          asm volatile("bar.sync 2, %0;" ::"n"(32 * kFusedEpi) : "memory");
         }
       } else {  // no room for the stage: direct stores
         const int col = hb * kTcM + row;
-        for (int n0 = 0; n0 < n3; n0 += 16) {
-          uint32_t r[16];
-          tc_ld16(tmem + lanes + (uint32_t)(kFusedD3Col + n0), r);
-          if (col < p.ncols) {
-            float* dst = p.raw + (long long)col * out3;
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (n0 + j < out3) dst[n0 + j] = __uint_as_float(r[j]) + bias3[n0 + j];
-          }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(d3free);
+        if (col < p.ncols)
+          for (int j = 0; j < 8; ++j)
+            if (hc0 + j < out3) p.raw[(long long)col * out3 + hc0 + j] = hv[j];
       }
-#ifdef CYR_FUSED_PROF
-      if (warp == kFusedEpi) { CYR_TRACE(21, hi) }
-      bacc[1] += h1 - h0;
-      bacc[2] += clock64() - h1;
-#endif
     };
     int i = 0, prev = -1;
     for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
-      const int fb = i % NB;
+      const uint32_t ph = (uint32_t)(i & 1);
+      for (int h = 0; h < 2; ++h) {  // epi1: D1 -> A2
+        CYR_FUSED_WAIT(&d1h[h], ph);
+        tc_fence_after();
 #ifdef CYR_FUSED_PROF
-      const long long f0 = clock64();
-      if (warp == kFusedEpi) { CYR_TRACE(60, i - 1) }
+        if (warp == 0) { CYR_TRACE(4 + h, i) }
 #endif
-      if (i >= NB) mbar_wait(&ffree[fb], (uint32_t)(((i / NB) - 1) & 1));
-      tc_feature_tile(p, b * kTcM + row, 0, feat + fb * kTcM * 128, row);
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ffull[fb]);
+        chunk(cw1, h * (n1 / 2) + part * cw1, kFusedA2Col, bias1);
+        if (lane == 0) mbar_arrive(&a2h[h]);
 #ifdef CYR_FUSED_PROF
-      bacc[0] += clock64() - f0;
-      if (warp == kFusedEpi) { CYR_TRACE(61, i - 1) }
+        if (warp == 0) { CYR_TRACE(6 + h, i) }
 #endif
-      if (prev >= 0) {
-        // the stage is free once the previous bulk store has read it
-        if (f.stage_bytes) {
-          if (leader) bulk_wait_read<0>();
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-        }
-        head(prev, i - 1);
       }
+      if (prev >= 0) head_write(prev, i - 1);  // the previous block's logits, during MMA2
+      for (int h = 0; h < 2; ++h) {  // epi2: D2 -> A3
+        CYR_FUSED_WAIT(&d2h[h], ph);
+        tc_fence_after();
+#ifdef CYR_FUSED_PROF
+        if (warp == 0) { CYR_TRACE(8 + h, i) }
+#endif
+        chunk(cw2, h * (n2 / 2) + part * cw2, kFusedA3Col, bias2);
+        if (lane == 0) mbar_arrive(&a3h[h]);
+#ifdef CYR_FUSED_PROF
+        if (warp == 0) { CYR_TRACE(10 + h, i) }
+#endif
+      }
+      CYR_FUSED_WAIT(d3full, ph);
+      tc_fence_after();
+#ifdef CYR_FUSED_PROF
+      if (warp == 0) { CYR_TRACE(20, i) }
+#endif
+      head_read();
+#ifdef CYR_FUSED_PROF
+      if (warp == 0) { CYR_TRACE(21, i) }
+#endif
       prev = b;
     }
-    if (prev >= 0) {
-      if (f.stage_bytes) {
-        if (leader) bulk_wait_read<0>();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-      }
-      head(prev, i - 1);
-    }
-    if (leader) bulk_wait_all();
-#ifdef CYR_FUSED_PROF
-    if ((blockIdx.x == 0 || blockIdx.x == 77) && lane == 0 && warp == kFusedEpi)
-      printf("BUILD cta %d w%d per block: feature %lld, head wait d3 %lld, head %lld\n",
-             blockIdx.x, warp, bacc[0] / i, bacc[1] / i, bacc[2] / i);
-#endif
-  } else {
-    // ------------------------------------------------------------ epilogues
-    const int quarter = warp & 3, part = warp >> 2;
-    int i = 0;
-#ifdef CYR_FUSED_PROF
-    long long eacc[5] = {0, 0, 0, 0, 0};
-#endif
-    for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
-      const uint32_t ph = (uint32_t)(i & 1);
-#ifdef CYR_FUSED_PROF
-      const long long q0 = clock64();
-#endif
-      CYR_FUSED_WAIT(d1full, ph);
-#ifdef CYR_FUSED_PROF
-      const long long q0b = clock64();
-#endif
-      // A2 shares TMEM columns with the previous block's D3 (head output)
-      if (i > 0) mbar_wait(d3free, ph ^ 1u);
-      tc_fence_after();
-#ifdef CYR_FUSED_PROF
-      const long long q1 = clock64();
-      if ((warp % 5) == 0) { CYR_TRACE(4 + (warp / 5) * 4 + 0, i) }
-      eacc[4] += q1 - q0b;
-#endif
-      fused_hidden_epi(tmem, quarter, part, n1, 0, kFusedA2Col, bias1);
-#ifdef CYR_FUSED_PROF
-      const long long q2 = clock64();
-      if ((warp % 5) == 0) { CYR_TRACE(4 + (warp / 5) * 4 + 1, i) }
-      CYR_TRACE(24 + warp, i)
-#endif
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&a2p[part]);
-      CYR_FUSED_WAIT(d2full, ph);
-      tc_fence_after();
-#ifdef CYR_FUSED_PROF
-      const long long q3 = clock64();
-      if ((warp % 5) == 0) { CYR_TRACE(4 + (warp / 5) * 4 + 2, i) }
-#endif
-      fused_hidden_epi(tmem, quarter, part, n2, 0, kFusedA3Col, bias2);
-#ifdef CYR_FUSED_PROF
-      const long long q4 = clock64();
-      if ((warp % 5) == 0) { CYR_TRACE(4 + (warp / 5) * 4 + 3, i) }
-      CYR_TRACE(40 + warp, i)
-      eacc[0] += q1 - q0; eacc[1] += q2 - q1; eacc[2] += q3 - q2; eacc[3] += q4 - q3;
-#endif
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&a3p[part]);
-    }
-#ifdef CYR_FUSED_PROF
-    if ((blockIdx.x == 0 || blockIdx.x == 77) && lane == 0 &&
-        (warp == 0 || warp == kFusedEpi - 1 || warp == 5))
-      printf("EPI cta %d w%d per block: wait d1 %lld (of it d3free %lld), epi1 %lld, wait d2 %lld, "
-             "epi2 %lld\n", blockIdx.x, warp, eacc[0] / i, eacc[4] / i, eacc[1] / i, eacc[2] / i,
-             eacc[3] / i);
-#endif
+    if (prev >= 0) head_write(prev, i - 1);
+    if (leader && f.stage_bytes) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
 #ifdef CYR_FUSED_PROF
   if (tid == 0 && blockIdx.x == 0 && nblocks > kTraceBlock * (int)gridDim.x &&
-      atomicAdd(&g_fused_trace_launch, 1) == 4) {  // one launch (the 5th large one) prints
+      atomicAdd(&g_fused_trace_launch, 1) == 1) {  // one launch (the 2nd large one) prints
     const long long t0 = trace[0];
-    printf("TRACE cta 0 block %d (clock - MMA1 issue start): MMA feat-ok 0, mma1-issued %lld, "
-           "mma2-issued %lld, mma3-issued %lld | head d3-seen %lld, head-done %lld\n", kTraceBlock,
-           trace[1] - t0, trace[2] - t0, trace[3] - t0, trace[20] - t0, trace[21] - t0);
-    printf("TRACE cta 0 builder feat(next) start %lld end %lld\n", trace[60] - t0, trace[61] - t0);
-    printf("TRACE cta 0 MMA a3-all-seen %lld, mma3 groups %lld %lld %lld %lld, before-commit %lld\n",
-           trace[22] - t0, trace[56] - t0, trace[57] - t0, trace[58] - t0, trace[59] - t0,
-           trace[23] - t0);
-    for (int w = 0; w < 4; ++w)
-      printf("TRACE cta 0 epi w%d: d1-seen %lld, epi1-done %lld, d2-seen %lld, epi2-done %lld\n",
-             w * 5, trace[4 + w * 4] - t0, trace[5 + w * 4] - t0, trace[6 + w * 4] - t0,
-             trace[7 + w * 4] - t0);
-    printf("TRACE cta 0 all epi1-done:");
-    for (int w = 0; w < kFusedEpi; ++w) printf(" w%d %lld", w, trace[24 + w] - t0);
-    printf("\nTRACE cta 0 all epi2-done:");
-    for (int w = 0; w < kFusedEpi; ++w) printf(" w%d %lld", w, trace[40 + w] - t0);
-    printf("\n");
+    printf("TRACE cta 0 block %d (clocks after its features are in): MMA2 K-half 1 start %lld, "
+           "MMA2 issued %lld, MMA3 K-half 0 start %lld, MMA3 issued %lld, next block %lld | "
+           "epi1 d1h %lld/%lld done %lld/%lld | epi2 d2h %lld/%lld done %lld/%lld | head d3 seen "
+           "%lld done %lld\n", kTraceBlock, trace[1] - t0, trace[2] - t0, trace[22] - t0,
+           trace[23] - t0, trace[12] - t0, trace[4] - t0, trace[5] - t0, trace[6] - t0,
+           trace[7] - t0, trace[8] - t0, trace[9] - t0, trace[10] - t0, trace[11] - t0,
+           trace[20] - t0, trace[21] - t0);
+    printf("TRACE cta 0 builder: next block's features %lld .. %lld\n", trace[60] - t0,
+           trace[61] - t0);
   }
 #endif
   if (warp == 0) {
