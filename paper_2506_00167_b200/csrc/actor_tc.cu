@@ -459,39 +459,47 @@ __global__ void __launch_bounds__(kTcThreads, 1) actor_tc_kernel(const TcLaunch 
 // TMEM (512 columns): D1 / D2 at [0, 256), A2 at [256, 384), A3 at [384, 512),
 // D3 at [256, 256 + N3) (A2 is dead once MMA2 has completed).
 // Roles:
-//   warps 0-15  epilogues: warp w reads TMEM lane quarter w % 4 and column
-//               part w / 4 of D1 / D2 (packed bias add, ReLU folded into the
-//               bf16x2 convert, tcgen05.st); warps 0-3 also run the head
-//               epilogue (bias, fp32 logits); each part arrives on its own
-//               barrier (a2p / a3p);
-//   warps 8..   feature builders: kFusedGroups groups of 4 warps, group g
-//               building the blocks i = g (mod groups) into A1 tile g (two
-//               groups: each has two blocks' time to build one);
-//   last warp   lane 0 issues the weight TMA and every MMA.
-// Each block's chain MMA1 -> epi1 -> MMA2 -> epi2 -> MMA3 -> epi3 is
-// serial; block b + 1's MMA1 is issued right after block b's MMA3, so it
-// overlaps the head epilogue, and the features are never on the critical path.
+//   warps 0-15  epilogues: warp w reads TMEM lane quarter w % 4; per layer it
+//               converts a chunk of N half 0 (columns part * n/8 of it, part
+//               = w / 4), arrives, then the same chunk of half 1 (packed bias
+//               add, ReLU folded into the bf16x2 convert, tcgen05.st); after
+//               MMA3 each warp reads 8 head logits (the head epilogue);
+//   warps 16-19 feature builders (kFusedGroups groups of 4 warps, group g
+//               building the blocks i = g (mod groups) into A1 tile g);
+//   last warp   the weight TMA (lane 0) and every MMA (one elected lane).
 // A second block in flight would need a second 256-column fp32 accumulator:
-// TMEM (512 columns) holds D + A2 + A3 of one block and no more.
-// Measured (scripts/fused_probe.py, 2M Mode-R columns, event timing): 474 us
-// = 46 % of the bf16 peak (852 us / 27 % before these changes):
-//  * MMA issue: every tcgen05.mma used to be its own asm inside `lane == 0`;
-//    ptxas wrapped each in an ELECT / R2UR.BROADCAST / BRA.U.ANY waterfall,
-//    ~146 cycles per instruction whatever N (scripts/micro/mma_rate.cu).  Now
-//    the whole warp runs the loop and one asm issues a K tile (4 MMAs) with
-//    the per-step operands added inside the asm: 17.5 cycles for N = 32,
-//    129 for N = 256 (the pipe floor is 128 * N / 256);
-//  * the head output (128 x out fp32 per block) used to be 20 scattered
-//    4-byte stores per thread by epilogue part 0, ~3.6k cycles on the
-//    critical path (epi1 of the next block waited for it); now the builder
-//    warps read D3, release it (d3free), stage the block's logits row-major
-//    in shared memory and write them with one bulk copy;
-//  * no integer division left in the issue loop (the per-part K-step
-//    bookkeeping of the PERPART / NSPLIT experiments is gone).
-// Per block (CYR_FUSED_PROF trace, CTA 0): MMA1 0.3k issue + 0.6k, epi1 1.4k,
-// MMA2 2.1k + ~0.3k wake-up, epi2 1.7k, MMA3 0.6k + ~0.5k wake-up: ~8.1k
-// cycles, the tensor pipe busy ~2.9k of them.  A/B knobs (compile-time):
-// CYR_FUSED_EPI (8 / 16 epilogue warps: 16), CYR_FUSED_FADD2.
+// TMEM (512 columns) holds D + A2 + A3 of one block and no more, so the
+// overlap comes from splitting each block's chain in N halves instead.
+// Measured (scripts/fused_probe.py, 2M Mode-R columns, event timing): 350 us
+// = 63 % of the bf16 peak (852 us / 27 % before these changes; 8M columns
+// 1,230-1,345 us = 65-71 %); the deepest cfg2 Mode-T level (2M columns,
+// 316 GFLOP) 358 us under ncu = 63 %:
+//  * MMA issue: the whole warp runs the loop and one asm issues a K tile (4
+//    MMAs) under one elect.sync with the per-step operands added inside the
+//    asm.  Issued one per asm from inside `lane == 0`, every tcgen05.mma cost
+//    ~146 cycles whatever N (ptxas's ELECT / R2UR.BROADCAST / BRA.U.ANY
+//    waterfall; scripts/micro/mma_rate.cu); now 17.5 for N = 32, 129 for
+//    N = 256 (the pipe floor is 128 * N / 256);
+//  * the block chain runs in N halves: MMA1 in two halves, each epilogue in
+//    two column chunks per warp (half 0 first, its own barrier), MMA2 half 0
+//    over K half 0 as soon as epi1 chunk 0 is in, MMA2 half 1 while epi2
+//    chunk 0 runs, MMA3 K half 0 while epi2 chunk 1 runs;
+//  * the head output: each epilogue warp reads 8 of D3's columns into
+//    registers right after MMA3 and writes them, with the bias, into a
+//    row-major shared-memory stage during the next block's MMA2; one bulk
+//    copy per block (128 x out fp32 = the block's contiguous slice of raw).
+//    As 20 scattered generic 4-byte stores per thread it cost ~3.6k cycles;
+//  * feature rows (builders) for E = 4 / 10 / 16 built in registers and
+//    written as 8 16-byte chunks; the per-element path (runtime integer
+//    divisions, scalar stores through a generic pointer that serialised the
+//    next loads) took 6.5k cycles per Mode-T tile, more than the chain;
+//  * bias pairs by explicit ld.shared (as generic 64-bit loads they were the
+//    kernel's most expensive instructions).
+// Per block (CYR_FUSED_PROF trace, CTA 0, 2M Mode-R columns): ~5.2k cycles,
+// the tensor pipe busy ~2.9k of them.  A/B knobs (compile-time):
+// CYR_FUSED_GROUPS (2 builder groups: Mode R 73.7 % vs 65.3 % at 8M
+// columns, Mode T 370 vs 358 us: 1 kept), CYR_FUSED_SPIN (test_wait spinning
+// on the hand-off barriers: slower).
 #ifndef CYR_FUSED_SPIN
 #define CYR_FUSED_SPIN 0
 #endif
