@@ -1170,21 +1170,44 @@ __global__ void __launch_bounds__(kWideFirstThreads, 1) actor_tc_wide_kernel(con
             if (leader) bulk_wait_read<1>();  // the store that last used this image has read it
             epi_sync(grp);
             unsigned char* sp = stg + (grp * 2 + sb) * kWideImage;
+            const uint32_t spa = smem_u32(sp);
+            // whole 8-output groups inside the layer with a 16-byte aligned
+            // bias: two float4 loads (uniform broadcast) per group instead of
+            // eight scalar ones, packed add + ReLU-folded convert (the fused
+            // MLP's epilogue), explicit st.shared
+            const bool vec = o0 + 64 <= q.out && ((reinterpret_cast<uintptr_t>(bias + o0) & 15u) == 0);
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
               uint32_t w[4];
+              if (vec) {
+                const float4 ba = __ldg(reinterpret_cast<const float4*>(bias + o0 + c * 8));
+                const float4 bb = __ldg(reinterpret_cast<const float4*>(bias + o0 + c * 8 + 4));
+                const float bv[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
 #pragma unroll
-              for (int h = 0; h < 4; ++h) {
-                const int j = c * 8 + 2 * h, o = o0 + j;
-                float v0 = o < q.out ? __uint_as_float(r[j]) + bias[o] : 0.f;
-                float v1 = o + 1 < q.out ? __uint_as_float(r[j + 1]) + bias[o + 1] : 0.f;
-                v0 = v0 > 0.f ? v0 : 0.f;
-                v1 = v1 > 0.f ? v1 : 0.f;
-                const __nv_bfloat162 pr = __floats2bfloat162_rn(v0, v1);
-                w[h] = *reinterpret_cast<const uint32_t*>(&pr);
+                for (int h = 0; h < 4; ++h) {
+                  unsigned long long v;
+                  asm("add.rn.f32x2 %0, %1, %2;"
+                      : "=l"(v)
+                      : "l"(f32x2_pack(__uint_as_float(r[c * 8 + 2 * h]),
+                                       __uint_as_float(r[c * 8 + 2 * h + 1]))),
+                        "l"(f32x2_pack(bv[2 * h], bv[2 * h + 1])));
+                  const float2 f = f32x2_unpack(v);
+                  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(w[h]) : "f"(f.y), "f"(f.x));
+                }
+              } else {
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                  const int j = c * 8 + 2 * h, o = o0 + j;
+                  float v0 = o < q.out ? __uint_as_float(r[j]) + bias[o] : 0.f;
+                  float v1 = o + 1 < q.out ? __uint_as_float(r[j + 1]) + bias[o + 1] : 0.f;
+                  v0 = v0 > 0.f ? v0 : 0.f;
+                  v1 = v1 > 0.f ? v1 : 0.f;
+                  const __nv_bfloat162 pr = __floats2bfloat162_rn(v0, v1);
+                  w[h] = *reinterpret_cast<const uint32_t*>(&pr);
+                }
               }
-              *reinterpret_cast<uint4*>(sp + sw128_offset(row, c * 8)) =
-                  make_uint4(w[0], w[1], w[2], w[3]);
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(spa + sw128_offset(row, c * 8)),
+                           "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]));
             }
             fence_proxy_async_smem();
             epi_sync(grp);
