@@ -72,10 +72,10 @@ static unsigned long long* g_prof_dev = nullptr;
 unsigned long long* cyr_prof_buffer() {
   if (cyr_trace_buffer() == nullptr) return nullptr;
   if (g_prof_dev == nullptr) {
-    if (cudaMalloc(reinterpret_cast<void**>(&g_prof_dev), 16 * sizeof(unsigned long long)) !=
+    if (cudaMalloc(reinterpret_cast<void**>(&g_prof_dev), 32 * sizeof(unsigned long long)) !=
         cudaSuccess)
       return nullptr;
-    cudaMemset(g_prof_dev, 0, 16 * sizeof(unsigned long long));
+    cudaMemset(g_prof_dev, 0, 32 * sizeof(unsigned long long));
   }
   return g_prof_dev;
 }
@@ -1211,9 +1211,9 @@ int cyr_debug_trace(int64_t* out, int32_t n) {
   for (int i = 0; i < n && i < 64; ++i)
     out[i] = g_trace_host ? (int64_t)g_trace_host[i] : 0;
   if (g_prof_dev != nullptr) {
-    unsigned long long h[16] = {};
+    unsigned long long h[28] = {};
     cudaMemcpy(h, g_prof_dev, sizeof(h), cudaMemcpyDeviceToHost);
-    for (int i = 0; i < 16 && 36 + i < n; ++i) out[36 + i] = (int64_t)h[i];
+    for (int i = 0; i < 28 && 36 + i < n; ++i) out[36 + i] = (int64_t)h[i];
   }
   return CYR_OK;
 }

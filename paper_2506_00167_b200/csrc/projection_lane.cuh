@@ -433,6 +433,10 @@ __device__ void codebook_rows_lane(const RawT* raw, long long row0, int nrows, i
       emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
       hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
     }
+    if (live) {  // histogram of fill evaluations per row: bins 1 .. 11, 12+ (prof[16..27])
+      const int bin = min(max(r.evals, 1), 12) - 1;
+      atomicAdd(prof + 16 + bin, 1ull);
+    }
     if (lane == 0) {
       atomicAdd(prof + 8, 1ull);
       atomicAdd(prof + 9, ev);

@@ -25,7 +25,7 @@ tree.build_tree_mode_t(pol, cell, al, mc, ep)
 torch.cuda.synchronize()
 buf = (ctypes.c_int64 * 64)()
 _native.lib().cyr_debug_trace(buf, 64)
-vals = [buf[i] for i in range(36, 52)]
+vals = [buf[i] for i in range(36, 64)]
 warps = max(vals[8], 1)
 names = ["head", "setup", "water level", "threshold", "coupled loop", "finish", "HH", "emit"]
 tot = sum(vals[:8])
@@ -37,3 +37,5 @@ print(f"  per row: {vals[9] / rows:.2f} fill evaluations, {vals[10] / rows:.2f} 
       f"exchange steps (phase-1 rows); coupled-bisection iterations per warp {vals[12] / warps:.1f}")
 print(f"  per warp (its slowest lane): {vals[13] / warps:.2f} fill evaluations, "
       f"{vals[14] / warps:.2f} exchange steps")
+hist = vals[16:28]
+print("  fill evaluations per row (1 .. 11, 12+):", hist)
