@@ -216,3 +216,37 @@ def test_fused_tc_mlp_equals_layer_path(golden):
     worst = float((np.abs(outs["1"] - outs["0"]) / scale).max())
     print(f"[bf16_tc] fused vs layer path: worst |dlogit|/max|col| = {worst:.2e}")
     assert worst < 1e-6
+
+
+@pytest.mark.parametrize("users,slots", [(3, 1601), (7, 1111)])
+def test_fused_tc_ragged_odd_users_equals_layer_path(users, slots):
+    """The fused MLP's generic paths: a user count without a specialised
+    feature row (E not in 4 / 10 / 16), an odd logit count (2E = 6 or 14) and
+    a ragged last block whose logits are not a 16-byte multiple (the word-copy
+    fallback of the head output instead of the bulk copy).  Against the
+    layer path (CYR_TC_FUSED=0) in a subprocess, as above."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r);"
+        "from tests.test_gpu_tc import _logits; from bench import synthetic_inputs;"
+        "from paper_2506_00167_b200 import AgentHyper, CellConfig, DevicePolicy, make_agent, substream;"
+        "cell = CellConfig(780, %d, 260);"
+        "agent = make_agent(cell, AgentHyper(actor_hidden=(256, 256)), substream(3, 'ragged'));"
+        "a, _ = synthetic_inputs(cell, %d);"
+        "x = _logits(DevicePolicy(agent.actor, 'bf16_tc'), cell, a);"
+        "np.save(sys.argv[1], x)" % (ROOT, users, slots))
+    outs = {}
+    for flag in ("1", "0"):
+        path = os.path.join(ROOT, "gpurun_out", f"ragged_{users}_{flag}.npy")
+        os.makedirs(os.path.dirname(path), exist_ok=True)
+        env = dict(os.environ, CYR_TC_FUSED=flag)
+        subprocess.run([sys.executable, "-c", code, path], env=env, check=True, cwd=ROOT)
+        outs[flag] = np.load(path)
+    cap = 780 // 260
+    last = (slots * cap) % 128  # columns in the ragged last block
+    assert (last * 2 * users * 4) % 16 != 0  # its logits miss the bulk-copy granularity
+    assert outs["1"].shape == (slots * cap, 2 * users)
+    scale = np.abs(outs["0"]).max(axis=1, keepdims=True)
+    worst = float((np.abs(outs["1"] - outs["0"]) / scale).max())
+    assert worst < 1e-6, worst
