@@ -250,3 +250,31 @@ def test_fused_tc_ragged_odd_users_equals_layer_path(users, slots):
     scale = np.abs(outs["0"]).max(axis=1, keepdims=True)
     worst = float((np.abs(outs["1"] - outs["0"]) / scale).max())
     assert worst < 1e-6, worst
+
+
+def test_fused_tc_mode_t_generic_users_equals_layer_path():
+    """Mode-T features through the fused MLP's generic (per-element) feature
+    path: E = 7 (no specialised row), cap 3; the node records of the whole
+    tree equal the layer path's (CYR_TC_FUSED=0), both bf16 tcgen05."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, %r);"
+        "from bench import synthetic_inputs;"
+        "from paper_2506_00167_b200 import CellConfig, DevicePolicy, substream, tree;"
+        "cell = CellConfig(780, 7, 260);"
+        "actor = tree.make_mode_t_actor(cell, (256, 256), substream(5, 'mode-t'));"
+        "a, e = synthetic_inputs(cell, 2, seed=4);"
+        "m = np.random.default_rng(2).integers(0, 6, size=a.shape).astype(np.int32);"
+        "al, mc, ep = (torch.from_numpy(x).cuda() for x in (a, m, e));"
+        "s = tree.build_tree_mode_t(DevicePolicy(actor, 'bf16_tc'), cell, al, mc, ep);"
+        "np.save(sys.argv[1], s.cpu().numpy())" % ROOT)
+    outs = {}
+    for flag in ("1", "0"):
+        path = os.path.join(ROOT, "gpurun_out", f"modet_generic_{flag}.npy")
+        os.makedirs(os.path.dirname(path), exist_ok=True)
+        env = dict(os.environ, CYR_TC_FUSED=flag)
+        subprocess.run([sys.executable, "-c", code, path], env=env, check=True, cwd=ROOT)
+        outs[flag] = np.load(path)
+    assert outs["1"].shape == outs["0"].shape
+    assert np.array_equal(outs["1"], outs["0"])
