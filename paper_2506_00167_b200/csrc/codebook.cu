@@ -121,7 +121,7 @@ struct TreeIO {
 
 // K3 of one Mode-T level, one lane per row: each warp holds 32 / cap
 // parents (one coupled call of cap rows each).
-template <typename RawT>
+template <typename RawT, int KE = 0>
 __global__ void __launch_bounds__(32 * kLaneWarps, kLaneMinBlocks) tree_level_kernel(const RawT* __restrict__ raw,
                                                                   TreeIO io, long long groups,
                                                                   int L,
@@ -133,9 +133,9 @@ __global__ void __launch_bounds__(32 * kLaneWarps, kLaneMinBlocks) tree_level_ke
   if (g0 >= groups) return;
   const int n = (int)min((long long)gpw, groups - g0);
   const long long row0 = g0 * io.cap;
-  codebook_rows_lane<RawT, TreeIO>(raw + row0 * 2 * io.E, row0, n * io.cap, io.cap, io.E, L, io,
-                                   status, lane_smem + (size_t)w * lane_scratch_bytes(io.E),
-                                   io.prof);
+  codebook_rows_lane<RawT, TreeIO, KE>(raw + row0 * 2 * io.E, row0, n * io.cap, io.cap, io.E, L,
+                                       io, status, lane_smem + (size_t)w * lane_scratch_bytes(io.E),
+                                       io.prof);
 }
 
 // K3 of a SMALL Mode-T level (few rows: the lane mapping would leave the
@@ -632,11 +632,21 @@ int cyr_launch_tree_level(int precision, const void* raw, const int32_t* alloc, 
     cyr::tree_level_kernel<double><<<(unsigned)blocks, 32 * cyr::kLaneWarps, smem, stream>>>(
         static_cast<const double*>(raw), io, groups, L, status);
   } else {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(cyr::tree_level_kernel<float>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cyr::tree_level_kernel<float><<<(unsigned)blocks, 32 * cyr::kLaneWarps, smem, stream>>>(
-        static_cast<const float*>(raw), io, groups, L, status);
+    auto launch = [&](auto kern) {
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kern<<<(unsigned)blocks, 32 * cyr::kLaneWarps, smem, stream>>>(
+          static_cast<const float*>(raw), io, groups, L, status);
+    };
+#ifndef CYR_LANE_SPECIALISE
+#define CYR_LANE_SPECIALISE 1
+#endif
+    // cfg2's E = 10 with the user count compiled in (known trip counts):
+    // deepest cfg2 level 990 -> 895 us.  E = 16 (cfg5) measured no gain (its
+    // unrolled code is 8.2k instructions against 7.6k generic: the kernel is
+    // instruction-cache sensitive), so it stays generic.
+    if (CYR_LANE_SPECIALISE && E == 10) launch(cyr::tree_level_kernel<float, 10>);
+    else launch(cyr::tree_level_kernel<float, 0>);
   }
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
 }

@@ -344,10 +344,13 @@ __host__ __device__ constexpr size_t lane_scratch_bytes(int E) {
 // clock64 cycles of each phase summed into prof[0..7] (head, setup, water
 // level, threshold, coupled loop, finish, Huntington-Hill, emit), warps in
 // prof[8].  Diagnostics only (system-scope atomics on mapped memory).
-template <typename RawT, typename IO>
-__device__ void codebook_rows_lane(const RawT* raw, long long row0, int nrows, int cap, int E, int L,
-                                   const IO& io, int32_t* status, unsigned char* scratch,
+// KE > 0: the user count as a compile-time constant (every per-user loop
+// has a known trip count); 0: runtime E.
+template <typename RawT, typename IO, int KE = 0>
+__device__ void codebook_rows_lane(const RawT* raw, long long row0, int nrows, int cap, int E_rt,
+                                   int L, const IO& io, int32_t* status, unsigned char* scratch,
                                    unsigned long long* prof = nullptr) {
+  const int E = KE > 0 ? KE : E_rt;
   const int lane = threadIdx.x & 31;
   long long tp = prof ? clock64() : 0;
   auto mark = [&](int k) {
