@@ -25,7 +25,7 @@ inline int ensure_seat_table(cudaStream_t stream) {
 // ------------------------------------------------------------ codebook K3
 // A CTA holds `spc` whole slots (<= 32 rows); 8 warps stride over the rows
 // in the per-row phases and warp 0 runs every slot's coupled loop at once.
-template <typename RawT>
+template <typename RawT, int KE = 0>
 __global__ void __launch_bounds__(256, 4) codebook_kernel(
     const RawT* __restrict__ raw, const int32_t* __restrict__ alloc,
     const double* __restrict__ eps, int S, int spc, int E, int L, int cap,
@@ -36,8 +36,8 @@ __global__ void __launch_bounds__(256, 4) codebook_kernel(
   const long long s0 = (long long)blockIdx.x * spc;
   const int slots = (int)min((long long)spc, S - s0);
   const long long row0 = s0 * cap;
-  codebook_rows<RawT>(raw + row0 * 2 * E, alloc, eps, row0, slots * cap, cap, E, L, cb, m_out,
-                      nu_out, margin_out, iters_out, status, sc);
+  codebook_rows<RawT, KE>(raw + row0 * 2 * E, alloc, eps, row0, slots * cap, cap, E, L, cb, m_out,
+                          nu_out, margin_out, iters_out, status, sc);
 }
 
 // Batch K3, one lane per row (projection_lane.cuh): each warp holds
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(32 * kLaneWarps, kLaneMinBlocks) tree_level_ke
 // machine empty and serialise E divisions per lane): one warp per row, lane
 // = eMBB user, 32 / cap parents per CTA (codebook_rows_io, the latency
 // path's mapping).
-template <typename RawT>
+template <typename RawT, int KE = 0>
 __global__ void __launch_bounds__(1024) tree_level_warp_kernel(const RawT* __restrict__ raw,
                                                              TreeIO io, long long groups, int L,
                                                              int32_t* __restrict__ status) {
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(1024) tree_level_warp_kernel(const RawT* __res
   const long long g0 = (long long)blockIdx.x * gpc;
   const int n = (int)min((long long)gpc, groups - g0);
   const long long row0 = g0 * io.cap;
-  codebook_rows_io<RawT, TreeIO>(raw + row0 * 2 * io.E, row0, n * io.cap, io.cap, io.E, L, io,
+  codebook_rows_io<RawT, TreeIO, KE>(raw + row0 * 2 * io.E, row0, n * io.cap, io.cap, io.E, L, io,
                                  status, sc);
 }
 
@@ -536,14 +536,19 @@ int cyr_launch_codebook(int precision, const void* raw, const int32_t* alloc, co
   // small batches: one slot per CTA (latency)
   const int spc = 1;
   const dim3 grid((S + spc - 1) / spc), block(S < 1184 ? 32 * cap : 256);
-  if (precision == CYR_FP64)
-    cyr::codebook_kernel<double><<<grid, block, 0, stream>>>(
-        static_cast<const double*>(raw), alloc, eps, S, spc, E, L, cap, codebook, m_hat, nu,
-        margin, iters, status);
-  else
-    cyr::codebook_kernel<float><<<grid, block, 0, stream>>>(
-        static_cast<const float*>(raw), alloc, eps, S, spc, E, L, cap, codebook, m_hat, nu,
-        margin, iters, status);
+#ifndef CYR_WARP_SPECIALISE
+#define CYR_WARP_SPECIALISE 1
+#endif
+  const bool e10 = CYR_WARP_SPECIALISE && E == 10;  // cfg2 / the bench geometry
+  if (precision == CYR_FP64) {
+    auto kern = e10 ? cyr::codebook_kernel<double, 10> : cyr::codebook_kernel<double, 0>;
+    kern<<<grid, block, 0, stream>>>(static_cast<const double*>(raw), alloc, eps, S, spc, E, L,
+                                     cap, codebook, m_hat, nu, margin, iters, status);
+  } else {
+    auto kern = e10 ? cyr::codebook_kernel<float, 10> : cyr::codebook_kernel<float, 0>;
+    kern<<<grid, block, 0, stream>>>(static_cast<const float*>(raw), alloc, eps, S, spc, E, L,
+                                     cap, codebook, m_hat, nu, margin, iters, status);
+  }
   return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
 }
 
@@ -612,12 +617,16 @@ int cyr_launch_tree_level(int precision, const void* raw, const int32_t* alloc, 
     const int gpc = 32 / cap;
     const long long blocks = (groups + gpc - 1) / gpc;
     const int threads = 32 * gpc * cap;
-    if (precision == CYR_FP64)
-      cyr::tree_level_warp_kernel<double><<<(unsigned)blocks, threads, 0, stream>>>(
-          static_cast<const double*>(raw), io, groups, L, status);
-    else
-      cyr::tree_level_warp_kernel<float><<<(unsigned)blocks, threads, 0, stream>>>(
-          static_cast<const float*>(raw), io, groups, L, status);
+    const bool e10w = CYR_WARP_SPECIALISE && E == 10;
+    if (precision == CYR_FP64) {
+      auto kern = e10w ? cyr::tree_level_warp_kernel<double, 10> : cyr::tree_level_warp_kernel<double, 0>;
+      kern<<<(unsigned)blocks, threads, 0, stream>>>(static_cast<const double*>(raw), io, groups,
+                                                    L, status);
+    } else {
+      auto kern = e10w ? cyr::tree_level_warp_kernel<float, 10> : cyr::tree_level_warp_kernel<float, 0>;
+      kern<<<(unsigned)blocks, threads, 0, stream>>>(static_cast<const float*>(raw), io, groups,
+                                                    L, status);
+    }
     return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
   }
   if (cyr::ensure_seat_table(stream) != CYR_OK) return CYR_CUDA_ERROR;
