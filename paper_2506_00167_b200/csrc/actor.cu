@@ -233,7 +233,12 @@ struct Vec16<double> {
 // per-call zeroing and the cluster barrier before the first DSMEM store are
 // skipped.  Rows a call does not write keep finite values of the previous
 // call (ReLU outputs) and only ever meet the zero-padded weight columns.
-template <typename T, int C, bool FUSE, bool RESIDENT = false>
+#ifndef CYR_WARP_SPECIALISE
+#define CYR_WARP_SPECIALISE 1
+#endif
+constexpr bool kLatSpecialiseE10 = CYR_WARP_SPECIALISE;
+
+template <typename T, int C, bool FUSE, bool RESIDENT = false, int KE = 0>
 __device__ __forceinline__ void cluster_slot(const ActorLaunch& p, const int32_t* alloc,
                                              const double* eps) {
   namespace cg = cooperative_groups;
@@ -416,8 +421,8 @@ __device__ __forceinline__ void cluster_slot(const ActorLaunch& p, const int32_t
     // K3 for the slot(s) on rank 0: logits never leave shared memory
     if (g != 0) return;
     __shared__ RowScratch sc;
-    codebook_rows<T>(raw_s, alloc, eps, 0, p.ncols, p.cap, p.E, p.L, p.cb, nullptr, nullptr,
-                     nullptr, nullptr, p.status, sc, tr);
+    codebook_rows<T, KE>(raw_s, alloc, eps, 0, p.ncols, p.cap, p.E, p.L, p.cb, nullptr, nullptr,
+                         nullptr, nullptr, p.status, sc, tr);
     if (p.cb_host != nullptr) {
       __syncthreads();
       const int n = p.S * (p.cap + 1) * p.E;
@@ -427,12 +432,12 @@ __device__ __forceinline__ void cluster_slot(const ActorLaunch& p, const int32_t
   }
 }
 
-template <typename T, int C, bool FUSE>
+template <typename T, int C, bool FUSE, int KE = 0>
 __global__ void __launch_bounds__(kLatThreads, 1)
     actor_cluster_kernel(const ActorLaunch p, const __grid_constant__ SlotInline inl) {
   const int32_t* alloc = p.inline_inputs ? inl.alloc : p.alloc;
   const double* eps = p.inline_inputs ? (p.eps ? inl.eps : nullptr) : p.eps;
-  cluster_slot<T, C, FUSE>(p, alloc, eps);
+  cluster_slot<T, C, FUSE, false, KE>(p, alloc, eps);
 }
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -451,7 +456,7 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // launch, graph launch or event sits on the per-call path.  The server
 // leaves on `quit` or after idle_ns without a request; the host relaunches
 // it on demand (abi.cu, slot_server_call).
-template <typename T, int C>
+template <typename T, int C, int KE = 0>
 __global__ void __launch_bounds__(kLatThreads, 1)
     slot_server_kernel(const ActorLaunch p, SlotMailbox* mb, uint32_t last,
                        unsigned long long idle_ns) {
@@ -517,7 +522,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
     const uint32_t cmd = s_cmd;
     if (cmd == 0u) break;  // cluster-uniform
     last = cmd;
-    cluster_slot<T, C, true, true>(p, s_alloc, p.eps != nullptr ? s_eps : nullptr);
+    cluster_slot<T, C, true, true, KE>(p, s_alloc, p.eps != nullptr ? s_eps : nullptr);
     if (g == 0) {
       __syncthreads();  // the codebook copy into the mailbox is complete
       if (tid == 0) {
@@ -537,8 +542,12 @@ int launch_slot_server(const ActorLaunch& p, int G, SlotMailbox* mb, uint32_t la
                        unsigned long long idle_ns, cudaStream_t stream) {
   const size_t smem = (2ull * p.desc.max_rows * C + (size_t)C * 2 * p.E) * sizeof(T);
   if (smem + 4096 > (size_t)kSmemLimit) return CYR_UNSUPPORTED;
-  auto kern = slot_server_kernel<T, C>;
-  static AttrCache configured;
+  // cfg2's E = 10 with the user count compiled into the fused K3 (as in
+  // codebook.cu's batch kernels)
+  const bool e10 = kLatSpecialiseE10 && p.E == 10;
+  auto kern = e10 ? slot_server_kernel<T, C, 10> : slot_server_kernel<T, C, 0>;
+  static AttrCache configured_e[2];
+  AttrCache& configured = configured_e[e10 ? 1 : 0];
   if (!ensure_func_attr(configured, (int)smem, [&] {
         return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem) == cudaSuccess &&
@@ -567,8 +576,10 @@ int launch_actor_cluster(const ActorLaunch& p, int G, cudaStream_t stream,
                          const SlotInline* inl = nullptr) {
   const size_t smem = (2ull * p.desc.max_rows * C + (FUSE ? (size_t)C * 2 * p.E : 0)) * sizeof(T);
   if (smem > (size_t)kSmemLimit) return CYR_UNSUPPORTED;
-  auto kern = actor_cluster_kernel<T, C, FUSE>;
-  static AttrCache configured;
+  const bool e10 = FUSE && kLatSpecialiseE10 && p.E == 10;
+  auto kern = e10 ? actor_cluster_kernel<T, C, FUSE, 10> : actor_cluster_kernel<T, C, FUSE, 0>;
+  static AttrCache configured_e[2];
+  AttrCache& configured = configured_e[e10 ? 1 : 0];
   if (!ensure_func_attr(configured, (int)smem, [&] {
         return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem) == cudaSuccess &&
