@@ -48,7 +48,7 @@ constexpr int kLaneWarps = 4;
 #endif
 constexpr int kLaneMinBlocks = CYR_LANE_MINB;  // <= 72 registers: 28 warps per SM at E = 10 (5 / 6 / 7 / 8: 1,004 / 983 / 972 / 988 us, deepest cfg2 level)
 
-template <typename RawT>
+template <typename RawT, int KE = 0>
 __global__ void __launch_bounds__(32 * kLaneWarps) codebook_lane_kernel(
     const RawT* __restrict__ raw, const int32_t* __restrict__ alloc,
     const double* __restrict__ eps, int S, int E, int L, int cap, int32_t* __restrict__ cb,
@@ -62,8 +62,8 @@ __global__ void __launch_bounds__(32 * kLaneWarps) codebook_lane_kernel(
   const int slots = (int)min((long long)gpw, S - s0);
   const long long row0 = s0 * cap;
   const SlotIO io{alloc, eps, cb, m_out, nu_out, margin_out, iters_out, E, cap};
-  codebook_rows_lane<RawT, SlotIO>(raw + row0 * 2 * E, row0, slots * cap, cap, E, L, io, status,
-                                   lane_smem + (size_t)w * lane_scratch_bytes(E));
+  codebook_rows_lane<RawT, SlotIO, KE>(raw + row0 * 2 * E, row0, slots * cap, cap, E, L, io,
+                                       status, lane_smem + (size_t)w * lane_scratch_bytes(E));
 }
 
 // ------------------------------------------------------------ Mode-T level
@@ -524,12 +524,11 @@ int cyr_launch_codebook(int precision, const void* raw, const int32_t* alloc, co
           static_cast<const double*>(raw), alloc, eps, S, E, L, cap, codebook, m_hat, nu, margin,
           iters, status);
     } else {
+      auto kern = E == 10 ? cyr::codebook_lane_kernel<float, 10> : cyr::codebook_lane_kernel<float, 0>;
       if (smem > 48 * 1024)
-        cudaFuncSetAttribute(cyr::codebook_lane_kernel<float>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cyr::codebook_lane_kernel<float><<<grid, block, smem, stream>>>(
-          static_cast<const float*>(raw), alloc, eps, S, E, L, cap, codebook, m_hat, nu, margin,
-          iters, status);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kern<<<grid, block, smem, stream>>>(static_cast<const float*>(raw), alloc, eps, S, E, L, cap,
+                                          codebook, m_hat, nu, margin, iters, status);
     }
     return cudaPeekAtLastError() == cudaSuccess ? CYR_OK : CYR_CUDA_ERROR;
   }
