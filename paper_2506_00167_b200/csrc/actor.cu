@@ -542,12 +542,13 @@ int launch_slot_server(const ActorLaunch& p, int G, SlotMailbox* mb, uint32_t la
                        unsigned long long idle_ns, cudaStream_t stream) {
   const size_t smem = (2ull * p.desc.max_rows * C + (size_t)C * 2 * p.E) * sizeof(T);
   if (smem + 4096 > (size_t)kSmemLimit) return CYR_UNSUPPORTED;
-  // cfg2's E = 10 with the user count compiled into the fused K3 (as in
-  // codebook.cu's batch kernels)
-  const bool e10 = kLatSpecialiseE10 && p.E == 10;
-  auto kern = e10 ? slot_server_kernel<T, C, 10> : slot_server_kernel<T, C, 0>;
-  static AttrCache configured_e[2];
-  AttrCache& configured = configured_e[e10 ? 1 : 0];
+  // cfg2's E = 10 and cfg1's E = 4 with the user count compiled into the
+  // fused K3 (as in codebook.cu's batch kernels)
+  const int ke = kLatSpecialiseE10 ? (p.E == 10 ? 1 : p.E == 4 ? 2 : 0) : 0;
+  auto kern = ke == 1 ? slot_server_kernel<T, C, 10>
+                      : ke == 2 ? slot_server_kernel<T, C, 4> : slot_server_kernel<T, C, 0>;
+  static AttrCache configured_e[3];
+  AttrCache& configured = configured_e[ke];
   if (!ensure_func_attr(configured, (int)smem, [&] {
         return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem) == cudaSuccess &&
@@ -576,10 +577,12 @@ int launch_actor_cluster(const ActorLaunch& p, int G, cudaStream_t stream,
                          const SlotInline* inl = nullptr) {
   const size_t smem = (2ull * p.desc.max_rows * C + (FUSE ? (size_t)C * 2 * p.E : 0)) * sizeof(T);
   if (smem > (size_t)kSmemLimit) return CYR_UNSUPPORTED;
-  const bool e10 = FUSE && kLatSpecialiseE10 && p.E == 10;
-  auto kern = e10 ? actor_cluster_kernel<T, C, FUSE, 10> : actor_cluster_kernel<T, C, FUSE, 0>;
-  static AttrCache configured_e[2];
-  AttrCache& configured = configured_e[e10 ? 1 : 0];
+  const int ke = (FUSE && kLatSpecialiseE10) ? (p.E == 10 ? 1 : p.E == 4 ? 2 : 0) : 0;
+  auto kern = ke == 1 ? actor_cluster_kernel<T, C, FUSE, 10>
+                      : ke == 2 ? actor_cluster_kernel<T, C, FUSE, 4>
+                                : actor_cluster_kernel<T, C, FUSE, 0>;
+  static AttrCache configured_e[3];
+  AttrCache& configured = configured_e[ke];
   if (!ensure_func_attr(configured, (int)smem, [&] {
         return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem) == cudaSuccess &&
