@@ -877,12 +877,14 @@ def mode_t_cpu(cell, hidden, sample_levels, gpu_slot0=None, seed=11):
     return out
 
 
-def mode_t_cfg3(cell, hidden, total=SLOTS, chunk=32):
+def mode_t_cfg3(cell, hidden, total=SLOTS, chunk=128):
     """BASELINE configs[2] in Mode T: 1024 independent slots, each with its
     full north-star tree (actor on every node state), processed as
     ``total / chunk`` tree batches back to back (the deepest level of one
-    32-slot batch is 2M actor columns; 1024 at once would need ~65 GB of
-    activation images).  Throughput per precision, CUDA events."""
+    128-slot batch is 8M actor columns).  Bigger batches amortise the small,
+    latency-bound levels (scripts/cfg3_chunk_probe.py, bf16: 32 / 64 / 128 /
+    256 slots per batch = 17.8 / 19.3 / 20.2 / 20.7k trees/s; fp32: 32 / 128
+    = 3.42 / 3.57k).  Throughput per precision, CUDA events."""
     import torch
     from paper_2506_00167_b200 import DevicePolicy, substream, tree
     actor = tree.make_mode_t_actor(cell, hidden, substream(0, "mode-t"))
