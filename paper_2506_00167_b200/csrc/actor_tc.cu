@@ -151,13 +151,12 @@ __device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 //   Mode R: [n/N (E), j/cap]
 //   Mode T: [n/N (E), k/cap, cum/N (E), mcs/mcs_scale (E), arrivals/(M*cap),
 //            (tau-1)/M]
-// The column's indices are decoded once and the per-user loads are issued in
-// independent batches of four, so their latencies overlap.
-// Shared-memory stores by address, without a "memory" clobber: through the
-// generic tile pointer every bf16 store was ordered before the next user's
-// global loads (possible alias), so each batch of loads paid its full
-// latency after the previous batch's stores (~4k cycles per 128-column tile
-// in the fused MLP, whose builders are on its critical path).
+// E = 4 / 10 / 16 take tc_feature_row below (registers, 16-byte stores).
+// The generic path decodes the column's indices once, issues every global
+// load first (the values parked in local memory) and then stores the bf16
+// values by shared-memory address without a "memory" clobber: through the
+// generic tile pointer each store was ordered before the next user's loads
+// (possible alias), so every batch of loads paid its full latency.
 __device__ __forceinline__ void tc_put(uint32_t a, int row, int t, int i, float x) {
   if (i >= t * 64 && i < t * 64 + 64) {
     const __nv_bfloat16 h = __float2bfloat16_rn(x);
