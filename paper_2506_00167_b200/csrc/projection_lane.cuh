@@ -344,6 +344,10 @@ __host__ __device__ constexpr size_t lane_scratch_bytes(int E) {
 // clock64 cycles of each phase summed into prof[0..7] (head, setup, water
 // level, threshold, coupled loop, finish, Huntington-Hill, emit), warps in
 // prof[8].  Diagnostics only (system-scope atomics on mapped memory).
+#ifndef CYR_HEAD_UNROLL
+#define CYR_HEAD_UNROLL 1
+#endif
+constexpr int kHeadUnroll = CYR_HEAD_UNROLL;  // head loop unroll (A/B)
 // KE > 0: the user count as a compile-time constant (every per-user loop
 // has a known trip count); 0: runtime E.
 template <typename RawT, typename IO, int KE = 0>
@@ -388,6 +392,7 @@ __device__ void codebook_rows_lane(const RawT* raw, long long row0, int nrows, i
     // head (neural.py:144-165, sac.py:348-355) and action_to_scs (neural.py:181-183)
     const RawT* rr = raw + (long long)lane * 2 * E;
     const double* eps = io.eps_row(grow, group, j);
+#pragma unroll (kHeadUnroll)
     for (int e = 0; e < E; ++e) {
       const double mu = (double)rr[e];
       const double ls = fmin(fmax((double)rr[E + e], kLogSigmaMin), kLogSigmaMax);
